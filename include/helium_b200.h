@@ -1,0 +1,213 @@
+/*
+ * helium_b200.h — C-ABI of the B200-native LLM-as-operator executor.
+ *
+ * Drop-in boundary for the reference's L4 execution layer
+ * (/root/reference/proj/include/helios/simulator.hpp, evaluator.hpp). Every
+ * entry point below names the reference interface it replaces. Plain
+ * pointers and sizes only; no C++ or torch types cross this boundary.
+ * Errors: functions return NULL / a negative status and hk_last_error()
+ * returns the message (thread-local). Messages thrown by the executor keep the
+ * reference's wording ("simulate: ...", simulator.cpp:226-244, :286, :361).
+ *
+ * ---------------------------------------------------------------------------
+ * HKPLAN01 — the executor input (little-endian, 8-byte words)
+ * ---------------------------------------------------------------------------
+ * It carries exactly what simulate(compiled, profile, call_tree, sigma, cfg)
+ * (simulator.hpp:128-130) reads. integration/plan_export.hpp produces it from
+ * the reference types.
+ *   u64 magic = 0x31304e414c504b48 ("HKPLAN01")
+ *   u64 batch                                  CompiledGraph::batch
+ *   u64 n_tok,  u64 tok[n_tok]                 interned token pool
+ *   u64 n_span, {u64 off, u64 len}[n_span]     spans into the pool
+ *   u64 n_node, per node (ascending id):
+ *       i64 id, u64 kind, u64 flags, f64 len_out, u64 n_a, i64 a[n_a]
+ *       kind 0 BOUND  (data/input/cache_fetch): a[q] = span of query q
+ *       kind 1 OUTPUT : a = {input node}
+ *       kind 2 LAMBDA : a = {fn (0 identity, 1 concat, 2 truncate), arg, inputs...}
+ *       kind 3 FORMAT : a = {(tag, v)...}: tag 0 literal span, tag 1 input node
+ *       kind 4 LLM    : a = {(tag, v)...}: prompt template in Evaluator::prompt
+ *                       order (role markers included): tag 0 span, tag 1 ref node
+ *       flags bit0 deterministic, bit1 has profile (len_out valid)
+ *   u64 n_out, i64 out[n_out]                  WorkflowGraph::outputs
+ *   u64 n_tnode, per call-tree node:           TemplatedRadixTree pool order
+ *       i64 parent, u64 is_leaf, i64 op, i64 query,
+ *       u64 n_parts, {u64 is_static, i64 span_or_source, i64 query}[n_parts],
+ *       u64 n_preds, i64 preds[n_preds]
+ *   u64 n_workers, per worker: u64 n, {i64 op, i64 query}[n]   Schedule sigma
+ */
+#ifndef HELIUM_B200_H
+#define HELIUM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HK_ABI_VERSION 1
+
+const char* hk_last_error(void);
+int hk_abi_version(void);
+
+/* ------------------------------------------------------------------ config */
+/* SimConfig + SimWorkerConfig (simulator.hpp:71-86). Arrays have n_workers entries. */
+typedef struct hk_sim_config {
+    uint32_t n_workers;
+    const uint64_t* capacity;       /* kv tokens per worker */
+    const uint64_t* block;          /* kv block size in tokens */
+    const uint64_t* prefill_budget; /* 0 = max(capacity/8, block) */
+    int32_t proactive_pin;
+    uint64_t pin_threshold;
+    double pin_capacity_frac;
+    uint64_t seed;
+    int32_t stochastic;
+    int32_t collect_trace;
+    uint64_t max_iterations; /* 0 = 10M guard */
+} hk_sim_config;
+
+/* SimMetrics counters (simulator.hpp:108-120) + B200 additions. */
+typedef struct hk_metrics {
+    uint64_t iterations;
+    uint64_t prompt_tokens;
+    uint64_t cache_served_tokens;
+    uint64_t prefill_computed_tokens;
+    uint64_t decode_tokens;
+    double hit_rate_pct;
+    uint64_t calls;
+    uint64_t recompute_tokens;  /* last position of fully cached prompts re-run on device */
+    uint64_t pin_compute_tokens; /* summed over workers */
+} hk_metrics;
+
+typedef struct hk_run hk_run;
+typedef struct hk_engine hk_engine;
+typedef struct hk_kvcache hk_kvcache;
+
+/* ---------------------------------------------------------------- executor */
+/* Replaces simulate() (simulator.cpp:222-389). engine == NULL runs the
+ * synthetic LLM body (synth_llm_output, evaluator.cpp:53-58) with the same
+ * control plane; otherwise the LLM body is the device transformer of `engine`
+ * (one engine worker per schedule worker).
+ * flags: bit0 = verify device trie lookups against the host tree. */
+hk_run* hk_simulate(const uint8_t* plan, size_t plan_len, const hk_sim_config* cfg, hk_engine* engine,
+                    uint32_t flags);
+int hk_run_metrics(const hk_run* run, hk_metrics* out);
+/* per-worker vectors of SimMetrics: which 0 = pinned_tokens, 1 = evicted_tokens,
+ * 2 = pin_compute_tokens. Returns the count; copies min(count, cap). */
+size_t hk_run_worker_stat(const hk_run* run, int which, uint64_t* out, size_t cap);
+/* which: 0 = sim_metrics_json (simulator.cpp:393-405), 1 = sim_calls_csv
+ * (:407-415), 2 = sim_trace_csv (:417-425). Returns bytes needed (incl. NUL). */
+size_t hk_run_report(const hk_run* run, int which, char* buf, size_t cap);
+/* SimMetrics::outputs flattened as u64 words:
+ *   n_nodes, {node_id, batch, {len, tokens[len]}[batch]}[n_nodes]
+ * Returns the word count; copies min(count, cap) words. */
+size_t hk_run_outputs(const hk_run* run, uint64_t* out, size_t cap);
+/* executor wall time split (seconds): [0] pin precompute, [1] iterations. */
+int hk_run_timing(const hk_run* run, double out[2]);
+void hk_run_free(hk_run* run);
+
+/* ------------------------------------------------------------------ KvCache */
+/* class KvCache (simulator.hpp:18-62), same node numbering/LRU/holds/pins. */
+hk_kvcache* hk_kv_create(size_t capacity_tokens, size_t block_tokens);
+size_t hk_kv_lookup(hk_kvcache* c, const uint64_t* seq, size_t n, uint64_t hold);
+size_t hk_kv_insert(hk_kvcache* c, const uint64_t* seq, size_t n, size_t len, int pinned, uint64_t hold);
+void hk_kv_release(hk_kvcache* c, uint64_t hold);
+/* out = {used_tokens, pinned_tokens, evicted_tokens} */
+void hk_kv_counters(const hk_kvcache* c, uint64_t out[3]);
+void hk_kv_destroy(hk_kvcache* c);
+
+/* static_pin_prefixes (simulator.hpp:67-69) for `worker` of `plan`. Pins are
+ * written back to back into tokens (cap words) with their lengths in lens
+ * (lens_cap). Returns the number of pins, or -1. */
+int64_t hk_static_pin_prefixes(const uint8_t* plan, size_t plan_len, int worker, size_t block, size_t threshold,
+                               size_t budget_tokens, uint64_t* tokens, size_t cap, uint64_t* lens, size_t lens_cap);
+
+/* --------------------------------------------------------- LLM body (synth) */
+/* synth_llm_len / synth_llm_output (evaluator.hpp:29-32). */
+size_t hk_synth_llm_len(const uint64_t* prompt, size_t n, double len_out, int deterministic, uint64_t seed,
+                        int stochastic);
+size_t hk_synth_llm_output(const uint64_t* prompt, size_t n, double len_out, int deterministic, uint64_t seed,
+                           int stochastic, uint64_t* out, size_t cap);
+/* tokens.hpp:16-28 */
+uint64_t hk_fnv1a64(const void* data, size_t len, uint64_t seed);
+uint64_t hk_hash_combine(uint64_t h, uint64_t v);
+/* model-mode token maps (new definitions) */
+uint32_t hk_vocab_of(uint64_t token, uint32_t vocab);
+uint64_t hk_gen_token(uint32_t id, uint32_t vocab);
+
+/* ================================================================ device */
+/* Random-init decoder-only transformer (Llama-3 / Qwen2.5 family). */
+typedef struct hk_model_config {
+    uint32_t n_layers;
+    uint32_t d_model;
+    uint32_t n_heads;
+    uint32_t n_kv_heads;
+    uint32_t head_dim;
+    uint32_t ffn_dim;
+    uint32_t vocab;
+    uint32_t qkv_bias;   /* Qwen2.5 has q/k/v biases */
+    float rope_theta;
+    float rms_eps;
+    uint64_t seed;       /* counter-based weight init seed */
+    uint32_t fp32;       /* 1 = fp32 storage + fp32 math (parity mode) */
+    uint32_t reserved;
+} hk_model_config;
+
+typedef struct hk_engine_config {
+    int32_t device;             /* CUDA ordinal */
+    uint32_t n_workers;         /* KV pools (one per schedule worker on this device) */
+    uint32_t pages_per_worker;  /* physical 16-token KV pages per pool */
+    uint32_t block_tokens;      /* page size in tokens (must equal SimWorkerConfig::block) */
+    uint32_t max_calls;         /* live call slots per worker */
+    uint32_t max_step_tokens;   /* max tokens in one ragged forward */
+    uint32_t max_ctx_tokens;    /* max context length of one call */
+    uint32_t use_device_trie;   /* admission lookups through the device trie (K2) */
+} hk_engine_config;
+
+/* K1-K5 live on the engine. Weights are initialised on device from the seed. */
+hk_engine* hk_engine_create(const hk_model_config* model, const hk_engine_config* cfg);
+void hk_engine_destroy(hk_engine* e);
+/* bytes of one KV page (all layers, K and V) */
+size_t hk_engine_page_bytes(const hk_engine* e);
+/* resets pools, slots and tries of every worker */
+int hk_engine_reset(hk_engine* e);
+
+/* K1 block pool: page-granular gather / scatter / copy on the device.
+ * dst/src are device pointers of n * page_bytes bytes. */
+int hk_pool_gather(hk_engine* e, int worker, const int32_t* pages, size_t n, void* dst_device);
+int hk_pool_scatter(hk_engine* e, int worker, const void* src_device, const int32_t* pages, size_t n);
+int hk_pool_copy(hk_engine* e, int worker, const int32_t* src_pages, const int32_t* dst_pages, size_t n);
+
+/* K2 device trie. Node journal entries mirror KvTree creates/erases. */
+typedef struct hk_trie_op {
+    int32_t node;
+    int32_t parent;
+    int32_t page;
+    int32_t erase;
+    uint64_t phash;
+    const uint64_t* key; /* block_tokens tokens (creates only) */
+} hk_trie_op;
+int hk_trie_apply(hk_engine* e, int worker, const hk_trie_op* ops, size_t n);
+/* Batched longest-block-prefix match of n prompts (tokens concatenated,
+ * offsets[n+1]). For prompt i writes matched block count, node path and page
+ * table rows (stride = max blocks per prompt). Equals KvCache::lookup's
+ * matched length and walk (simulator.cpp:69-87) without its side effects. */
+int hk_trie_match(hk_engine* e, int worker, const uint64_t* tokens, const uint64_t* offsets, size_t n,
+                  int32_t* matched_blocks, int32_t* node_path, int32_t* page_table, size_t stride);
+
+/* Stand-alone greedy generation of one prompt (vocab ids) through the paged
+ * engine — prefill then n_new decode steps — used by model parity tests.
+ * logits (optional) receives the vocab logits of each sampled position. */
+int hk_generate(hk_engine* e, const uint32_t* ids, size_t n, size_t n_new, uint32_t* out_ids, float* logits);
+
+/* Device time (ms) per kernel family accumulated since the last reset, for
+ * roofline reporting: names "gemm", "attn_shared", "attn_private", "attn_prefill",
+ * "attn_merge", "small", "trie", "kvcopy". Returns -1 for an unknown name. */
+double hk_engine_kernel_ms(const hk_engine* e, const char* family, uint64_t* launches, double* bytes);
+int hk_engine_profile(hk_engine* e, int enable);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HELIUM_B200_H */

@@ -1,0 +1,206 @@
+// extern "C" entry points of include/helium_b200.h for the host side
+// (executor, KvCache, pins, synth, hashes). Device entry points live in
+// csrc/cuda/engine.cu.
+#include <cstring>
+#include <memory>
+
+#include "../../../include/helium_b200.h"
+#include "hk_host.hpp"
+
+namespace hk {
+thread_local std::string g_last_error;
+void set_error(const std::string& s) { g_last_error = s; }
+// Implemented in csrc/cuda/engine.cu.
+std::unique_ptr<LlmBody> make_device_body(hk_engine* e, const Plan& plan, const SimConfig& cfg);
+}  // namespace hk
+
+struct hk_run {
+    hk::SimMetrics m;
+    std::string reports[3];
+};
+
+struct hk_kvcache {
+    hk::KvTree tree;
+    hk_kvcache(std::size_t c, std::size_t b) : tree(c, b) {}
+};
+
+namespace {
+
+template <typename F>
+auto guard(F&& f, decltype(f()) on_error) -> decltype(f()) {
+    try {
+        return f();
+    } catch (const std::exception& e) {
+        hk::set_error(e.what());
+        return on_error;
+    }
+}
+
+hk::SimConfig to_sim_config(const hk_sim_config* c) {
+    if (!c) throw std::runtime_error("hk_simulate: null config");
+    hk::SimConfig s;
+    for (uint32_t w = 0; w < c->n_workers; ++w)
+        s.workers.push_back(hk::SimWorkerConfig{c->capacity[w], c->block[w], c->prefill_budget[w]});
+    s.proactive_pin = c->proactive_pin != 0;
+    s.pin_threshold = c->pin_threshold;
+    s.pin_capacity_frac = c->pin_capacity_frac;
+    s.seed = c->seed;
+    s.stochastic = c->stochastic != 0;
+    s.collect_trace = c->collect_trace != 0;
+    s.max_iterations = c->max_iterations;
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hk_last_error(void) { return hk::g_last_error.c_str(); }
+int hk_abi_version(void) { return HK_ABI_VERSION; }
+
+hk_run* hk_simulate(const uint8_t* plan, size_t plan_len, const hk_sim_config* cfg, hk_engine* engine,
+                    uint32_t flags) {
+    return guard(
+        [&]() -> hk_run* {
+            hk::Plan p = hk::parse_plan(plan, plan_len);
+            hk::SimConfig sc = to_sim_config(cfg);
+            auto run = std::make_unique<hk_run>();
+            hk::ExecOptions eo;
+            eo.verify_device_lookup = (flags & 1u) != 0;
+            if (engine) {
+                std::unique_ptr<hk::LlmBody> body = hk::make_device_body(engine, p, sc);
+                run->m = hk::simulate(p, sc, *body, eo);
+            } else {
+                hk::SyntheticBody body(sc.seed, sc.stochastic);
+                run->m = hk::simulate(p, sc, body, eo);
+            }
+            run->reports[0] = hk::sim_metrics_json(run->m);
+            run->reports[1] = hk::sim_calls_csv(run->m);
+            run->reports[2] = hk::sim_trace_csv(run->m);
+            return run.release();
+        },
+        nullptr);
+}
+
+int hk_run_metrics(const hk_run* r, hk_metrics* o) {
+    if (!r || !o) return -1;
+    o->iterations = r->m.iterations;
+    o->prompt_tokens = r->m.prompt_tokens;
+    o->cache_served_tokens = r->m.cache_served_tokens;
+    o->prefill_computed_tokens = r->m.prefill_computed_tokens;
+    o->decode_tokens = r->m.decode_tokens;
+    o->hit_rate_pct = r->m.hit_rate_pct;
+    o->calls = r->m.calls.size();
+    o->recompute_tokens = r->m.recompute_tokens;
+    o->pin_compute_tokens = 0;
+    for (auto v : r->m.pin_compute_tokens) o->pin_compute_tokens += v;
+    return 0;
+}
+
+size_t hk_run_worker_stat(const hk_run* r, int which, uint64_t* out, size_t cap) {
+    if (!r) return 0;
+    std::vector<uint64_t> v;
+    if (which == 0)
+        for (auto x : r->m.pinned_tokens) v.push_back(x);
+    else if (which == 1)
+        for (auto x : r->m.evicted_tokens) v.push_back(x);
+    else
+        for (auto x : r->m.pin_compute_tokens) v.push_back(x);
+    for (size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
+    return v.size();
+}
+
+size_t hk_run_report(const hk_run* r, int which, char* buf, size_t cap) {
+    if (!r || which < 0 || which > 2) return 0;
+    const std::string& s = r->reports[which];
+    if (buf && cap > 0) {
+        size_t n = std::min(cap - 1, s.size());
+        std::memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    }
+    return s.size() + 1;
+}
+
+size_t hk_run_outputs(const hk_run* r, uint64_t* out, size_t cap) {
+    if (!r) return 0;
+    std::vector<uint64_t> w;
+    w.push_back(r->m.outputs.size());
+    for (const auto& [id, vals] : r->m.outputs) {
+        w.push_back(static_cast<uint64_t>(id));
+        w.push_back(vals.size());
+        for (const auto& v : vals) {
+            w.push_back(v.size());
+            w.insert(w.end(), v.begin(), v.end());
+        }
+    }
+    for (size_t i = 0; i < w.size() && i < cap; ++i) out[i] = w[i];
+    return w.size();
+}
+
+int hk_run_timing(const hk_run* r, double out[2]) {
+    if (!r) return -1;
+    out[0] = r->m.pin_seconds;
+    out[1] = r->m.iter_seconds;
+    return 0;
+}
+
+void hk_run_free(hk_run* r) { delete r; }
+
+hk_kvcache* hk_kv_create(size_t cap, size_t block) {
+    return guard([&]() -> hk_kvcache* { return new hk_kvcache(cap, block); }, nullptr);
+}
+size_t hk_kv_lookup(hk_kvcache* c, const uint64_t* s, size_t n, uint64_t hold) {
+    return c->tree.lookup(s, n, hold);
+}
+size_t hk_kv_insert(hk_kvcache* c, const uint64_t* s, size_t n, size_t len, int pinned, uint64_t hold) {
+    return c->tree.insert(s, n, len, pinned != 0, hold);
+}
+void hk_kv_release(hk_kvcache* c, uint64_t hold) { c->tree.release(hold); }
+void hk_kv_counters(const hk_kvcache* c, uint64_t out[3]) {
+    out[0] = c->tree.used_tokens();
+    out[1] = c->tree.pinned_tokens();
+    out[2] = c->tree.evicted_tokens();
+}
+void hk_kv_destroy(hk_kvcache* c) { delete c; }
+
+int64_t hk_static_pin_prefixes(const uint8_t* plan, size_t plan_len, int worker, size_t block, size_t threshold,
+                               size_t budget, uint64_t* tokens, size_t cap, uint64_t* lens, size_t lens_cap) {
+    return guard(
+        [&]() -> int64_t {
+            hk::Plan p = hk::parse_plan(plan, plan_len);
+            std::vector<hk::TokenSeq> pins = hk::static_pin_prefixes(p, worker, block, threshold, budget);
+            size_t off = 0;
+            for (size_t i = 0; i < pins.size(); ++i) {
+                if (i < lens_cap) lens[i] = pins[i].size();
+                for (uint64_t t : pins[i]) {
+                    if (off < cap) tokens[off] = t;
+                    ++off;
+                }
+            }
+            return static_cast<int64_t>(pins.size());
+        },
+        int64_t{-1});
+}
+
+size_t hk_synth_llm_len(const uint64_t* p, size_t n, double len_out, int det, uint64_t seed, int stochastic) {
+    return guard([&]() { return hk::synth_llm_len(hk::TokenSeq(p, p + n), len_out, det != 0, seed, stochastic != 0); },
+                 size_t{0});
+}
+
+size_t hk_synth_llm_output(const uint64_t* p, size_t n, double len_out, int det, uint64_t seed, int stochastic,
+                           uint64_t* out, size_t cap) {
+    return guard(
+        [&]() {
+            hk::TokenSeq o = hk::synth_llm_output(hk::TokenSeq(p, p + n), len_out, det != 0, seed, stochastic != 0);
+            for (size_t i = 0; i < o.size() && i < cap; ++i) out[i] = o[i];
+            return o.size();
+        },
+        size_t{0});
+}
+
+uint64_t hk_fnv1a64(const void* d, size_t n, uint64_t seed) { return hk::fnv1a64(d, n, seed); }
+uint64_t hk_hash_combine(uint64_t h, uint64_t v) { return hk::hash_combine(h, v); }
+uint32_t hk_vocab_of(uint64_t t, uint32_t v) { return hk::vocab_of(t, v); }
+uint64_t hk_gen_token(uint32_t id, uint32_t v) { return hk::gen_token(id, v); }
+
+}  // extern "C"

@@ -1,0 +1,249 @@
+"""Python mirror of the reference's L4 execution API over the C-ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/helios/simulator.hpp and evaluator.hpp so parity
+tests read like the reference's own tests (test_simulator.cpp). All work is
+done by libhelium_b200.so; this module only marshals arguments.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+
+# ------------------------------------------------------------------ KvCache
+class KvCache:
+    """class KvCache (simulator.hpp:18-62)."""
+
+    def __init__(self, capacity_tokens: int, block_tokens: int):
+        lib = _lib.load()
+        self._h = lib.hk_kv_create(capacity_tokens, block_tokens)
+        if not self._h:
+            raise RuntimeError(_lib.last_error())
+        self._cap, self._block = capacity_tokens, block_tokens
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.load().hk_kv_destroy(h)
+            self._h = None
+
+    def capacity(self) -> int:
+        return self._cap
+
+    def block(self) -> int:
+        return self._block
+
+    def _counters(self):
+        out = (C.c_uint64 * 3)()
+        _lib.load().hk_kv_counters(self._h, out)
+        return list(out)
+
+    def used_tokens(self) -> int:
+        return self._counters()[0]
+
+    def pinned_tokens(self) -> int:
+        return self._counters()[1]
+
+    def evicted_tokens(self) -> int:
+        return self._counters()[2]
+
+    def lookup(self, seq: Sequence[int], hold: int = 0) -> int:
+        a, p = _lib.u64_array(seq)
+        return _lib.load().hk_kv_lookup(self._h, p, len(a), hold)
+
+    def insert(self, seq: Sequence[int], length: int, pinned: bool, hold: int = 0) -> int:
+        a, p = _lib.u64_array(seq)
+        return _lib.load().hk_kv_insert(self._h, p, len(a), length, int(pinned), hold)
+
+    def release(self, hold: int) -> None:
+        _lib.load().hk_kv_release(self._h, hold)
+
+
+# ------------------------------------------------------------------- config
+@dataclass
+class SimWorkerConfig:
+    capacity: int = 4096
+    block: int = 16
+    prefill_budget: int = 0
+
+
+@dataclass
+class SimConfig:
+    workers: List[SimWorkerConfig] = field(default_factory=list)
+    proactive_pin: bool = True
+    pin_threshold: int = 200
+    pin_capacity_frac: float = 0.5
+    seed: int = 0
+    stochastic: bool = False
+    collect_trace: bool = False
+    max_iterations: int = 0
+
+    def to_c(self):
+        n = len(self.workers)
+        cap = (C.c_uint64 * n)(*[w.capacity for w in self.workers])
+        blk = (C.c_uint64 * n)(*[w.block for w in self.workers])
+        bud = (C.c_uint64 * n)(*[w.prefill_budget for w in self.workers])
+        c = _lib.SimConfigC(n, cap, blk, bud, int(self.proactive_pin), self.pin_threshold,
+                            self.pin_capacity_frac, self.seed, int(self.stochastic), int(self.collect_trace),
+                            self.max_iterations)
+        c._keep = (cap, blk, bud)
+        return c
+
+
+@dataclass
+class SimMetrics:
+    """SimMetrics (simulator.hpp:108-120) + the reports of simulator.cpp:393-425."""
+    iterations: int
+    prompt_tokens: int
+    cache_served_tokens: int
+    prefill_computed_tokens: int
+    decode_tokens: int
+    hit_rate_pct: float
+    calls: int
+    pinned_tokens: List[int]
+    evicted_tokens: List[int]
+    outputs: Dict[int, List[List[int]]]
+    metrics_json: str
+    calls_csv: str
+    trace_csv: str
+    recompute_tokens: int = 0
+    pin_compute_tokens: List[int] = field(default_factory=list)
+    pin_seconds: float = 0.0
+    iter_seconds: float = 0.0
+
+
+def _report(h, which: int) -> str:
+    lib = _lib.load()
+    n = lib.hk_run_report(h, which, None, 0)
+    buf = C.create_string_buffer(n)
+    lib.hk_run_report(h, which, buf, n)
+    return buf.value.decode()
+
+
+def _worker_stat(h, which: int) -> List[int]:
+    lib = _lib.load()
+    n = lib.hk_run_worker_stat(h, which, None, 0)
+    out = (C.c_uint64 * max(n, 1))()
+    lib.hk_run_worker_stat(h, which, out, n)
+    return list(out)[:n]
+
+
+def _outputs(h) -> Dict[int, List[List[int]]]:
+    lib = _lib.load()
+    n = lib.hk_run_outputs(h, None, 0)
+    buf = np.zeros(max(n, 1), dtype=np.uint64)
+    lib.hk_run_outputs(h, buf.ctypes.data_as(_lib.u64p), n)
+    words = buf[:n].tolist()
+    out, i = {}, 1
+    for _ in range(words[0]):
+        nid = int(np.int64(np.uint64(words[i])))
+        b = words[i + 1]
+        i += 2
+        vals = []
+        for _ in range(b):
+            ln = words[i]
+            vals.append(words[i + 1:i + 1 + ln])
+            i += 1 + ln
+        out[nid] = vals
+    return out
+
+
+def simulate(plan: bytes, cfg: SimConfig, engine=None, verify_lookup: bool = False) -> SimMetrics:
+    """simulate() (simulator.hpp:128-130) on a flattened HKPLAN01 plan.
+
+    engine=None runs the synthetic LLM body (reference mode S); an Engine runs
+    the device transformer (mode T). Raises RuntimeError with the reference's
+    messages ("simulate: ...") on invalid schedules/configs.
+    """
+    lib = _lib.load()
+    buf = (C.c_uint8 * len(plan)).from_buffer_copy(plan)
+    c = cfg.to_c()
+    h = lib.hk_simulate(buf, len(plan), C.byref(c), engine.handle if engine is not None else None,
+                        1 if verify_lookup else 0)
+    if not h:
+        raise RuntimeError(_lib.last_error())
+    try:
+        mc = _lib.MetricsC()
+        lib.hk_run_metrics(h, C.byref(mc))
+        t = (C.c_double * 2)()
+        lib.hk_run_timing(h, t)
+        return SimMetrics(
+            iterations=mc.iterations, prompt_tokens=mc.prompt_tokens, cache_served_tokens=mc.cache_served_tokens,
+            prefill_computed_tokens=mc.prefill_computed_tokens, decode_tokens=mc.decode_tokens,
+            hit_rate_pct=mc.hit_rate_pct, calls=mc.calls, pinned_tokens=_worker_stat(h, 0),
+            evicted_tokens=_worker_stat(h, 1), outputs=_outputs(h), metrics_json=_report(h, 0),
+            calls_csv=_report(h, 1), trace_csv=_report(h, 2), recompute_tokens=mc.recompute_tokens,
+            pin_compute_tokens=_worker_stat(h, 2), pin_seconds=t[0], iter_seconds=t[1])
+    finally:
+        lib.hk_run_free(h)
+
+
+def sim_metrics_json(m: SimMetrics) -> str:
+    return m.metrics_json
+
+
+def sim_calls_csv(m: SimMetrics) -> str:
+    return m.calls_csv
+
+
+def sim_trace_csv(m: SimMetrics) -> str:
+    return m.trace_csv
+
+
+def static_pin_prefixes(plan: bytes, worker: int, block: int, threshold: int, budget_tokens: int) -> List[List[int]]:
+    """static_pin_prefixes (simulator.hpp:67-69)."""
+    lib = _lib.load()
+    buf = (C.c_uint8 * len(plan)).from_buffer_copy(plan)
+    cap = 1 << 22
+    toks = np.zeros(cap, dtype=np.uint64)
+    lens = np.zeros(4096, dtype=np.uint64)
+    n = lib.hk_static_pin_prefixes(buf, len(plan), worker, block, threshold, budget_tokens,
+                                   toks.ctypes.data_as(_lib.u64p), cap, lens.ctypes.data_as(_lib.u64p), 4096)
+    if n < 0:
+        raise RuntimeError(_lib.last_error())
+    out, off = [], 0
+    for i in range(n):
+        ln = int(lens[i])
+        out.append(toks[off:off + ln].tolist())
+        off += ln
+    return out
+
+
+def synth_llm_len(prompt: Sequence[int], len_out: float, deterministic: bool, seed: int = 0,
+                  stochastic: bool = False) -> int:
+    a, p = _lib.u64_array(prompt)
+    if len_out < 0:
+        raise RuntimeError("negative len_out")
+    return _lib.load().hk_synth_llm_len(p, len(a), len_out, int(deterministic), seed, int(stochastic))
+
+
+def synth_llm_output(prompt: Sequence[int], len_out: float, deterministic: bool, seed: int = 0,
+                     stochastic: bool = False) -> List[int]:
+    a, p = _lib.u64_array(prompt)
+    n = synth_llm_len(prompt, len_out, deterministic, seed, stochastic)
+    out = np.zeros(max(n, 1), dtype=np.uint64)
+    _lib.load().hk_synth_llm_output(p, len(a), len_out, int(deterministic), seed, int(stochastic),
+                                    out.ctypes.data_as(_lib.u64p), n)
+    return out[:n].tolist()
+
+
+def fnv1a64(data: bytes, seed: int = 0xcbf29ce484222325) -> int:
+    return _lib.load().hk_fnv1a64(data, len(data), seed)
+
+
+def hash_combine(h: int, v: int) -> int:
+    return _lib.load().hk_hash_combine(h, v)
+
+
+def vocab_of(token: int, vocab: int) -> int:
+    return _lib.load().hk_vocab_of(token, vocab)
+
+
+def gen_token(vid: int, vocab: int) -> int:
+    return _lib.load().hk_gen_token(vid, vocab)
