@@ -1,0 +1,189 @@
+"""TEST INFRASTRUCTURE ONLY — CPU fp32 restatement of the random-init decoder.
+
+PARITY UNPINNED BY THE REFERENCE: the reference (/root/reference/proj) has no
+model — its LLM operator is a hash (evaluator.cpp:37-58). This numpy decoder is
+the oracle for the transformer math of the B200 engine (csrc/cuda/engine.cu):
+standard Llama-3 / Qwen2.5 decoder layers (RMSNorm, RoPE rotate-half, GQA
+causal attention, SwiGLU MLP, untied LM head, optional QKV bias) with the
+engine's counter-based weight init reproduced bit-for-bit (init_uniform_kernel,
+ops.cu) and — in bf16 mode — rounding to bf16 at the points where the device
+stores bf16 (GEMM inputs/outputs, q/k/v, attention output). Accumulations are
+fp32 here; the device's accumulation order differs, hence the tolerances
+(1e-2 relative logits in bf16, 1e-5 in fp32 mode) used by the tests.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+
+def round_bf16(v: np.ndarray) -> np.ndarray:
+    """fp32 -> bf16 -> fp32, round to nearest even (finite inputs)."""
+    b = np.ascontiguousarray(v, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = (b + np.uint64(0x7FFF) + ((b >> np.uint64(16)) & np.uint64(1))) & np.uint64(0xFFFF0000)
+    return b.astype(np.uint32).view(np.float32)
+
+
+def init_uniform(n: int, seed: int, tid: int, scale: float, bf16: bool, chunk: int = 1 << 24) -> np.ndarray:
+    """Mirror of init_uniform_kernel (ops.cu)."""
+    with np.errstate(over="ignore"):
+        base = np.uint64((seed * 0xD1B54A32D192ED03 + tid * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF)
+        out = np.empty(n, dtype=np.float32)
+        for s in range(0, n, chunk):
+            e = min(n, s + chunk)
+            h = splitmix64(base + np.arange(s, e, dtype=np.uint64))
+            u = (h >> np.uint64(40)).astype(np.float32) * np.float32(1.0 / 8388608.0) - np.float32(1.0)
+            v = u * np.float32(scale)
+            out[s:e] = round_bf16(v) if bf16 else v
+    return out
+
+
+@dataclass
+class Weights:
+    embed: np.ndarray
+    layers: list
+    lm_head: np.ndarray
+
+
+def build_weights(m) -> Weights:
+    """Same tensor ids / scales as hk_engine::init_weights (engine.cu)."""
+    bf = not m.fp32
+    d, H, Hkv, hd, F, V = m.d_model, m.n_heads, m.n_kv_heads, m.head_dim, m.ffn_dim, m.vocab
+    qkv = (H + 2 * Hkv) * hd
+    s_d = np.float32(math.sqrt(3.0 / d))
+    s_o = np.float32(math.sqrt(3.0 / (H * hd)))
+    s_f = np.float32(math.sqrt(3.0 / F))
+    embed = init_uniform(V * d, m.seed, 1, 1.0, bf).reshape(V, d)
+    layers = []
+    for l in range(m.n_layers):
+        t0 = 16 + 16 * l
+        lw = {
+            "wqkv": init_uniform(qkv * d, m.seed, t0 + 1, float(s_d), bf).reshape(qkv, d),
+            "bqkv": init_uniform(qkv, m.seed, t0 + 2, 0.1, bf) if m.qkv_bias else None,
+            "wo": init_uniform(d * H * hd, m.seed, t0 + 3, float(np.float32(0.5) * s_o), bf).reshape(d, H * hd),
+            "wgu": init_uniform(2 * F * d, m.seed, t0 + 4, float(s_d), bf).reshape(2 * F, d),
+            "wd": init_uniform(d * F, m.seed, t0 + 5, float(np.float32(0.5) * s_f), bf).reshape(d, F),
+        }
+        layers.append(lw)
+    lm_head = init_uniform(V * d, m.seed, 2, float(s_d), bf).reshape(V, d)
+    return Weights(embed, layers, lm_head)
+
+
+def rope_table(m, max_pos: int) -> np.ndarray:
+    """(cos, sin) per position, computed in float64 then stored fp32, as engine.cu does."""
+    half = m.head_dim // 2
+    i = np.arange(half, dtype=np.float64)
+    inv = np.power(np.float64(m.rope_theta), -2.0 * i / m.head_dim)
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+class Decoder:
+    """Incremental greedy decoder with a contiguous KV cache."""
+
+    def __init__(self, m, weights: Optional[Weights] = None, max_pos: int = 16384):
+        self.m = m
+        self.w = weights or build_weights(m)
+        self.bf = not m.fp32
+        self.cos, self.sin = rope_table(m, max_pos)
+
+    def _r(self, v):
+        return round_bf16(v) if self.bf else v.astype(np.float32)
+
+    def _rms(self, x):
+        ms = np.mean(x.astype(np.float64) ** 2, axis=-1, keepdims=True)
+        return (x / np.sqrt(ms + self.m.rms_eps)).astype(np.float32)
+
+    def _rope(self, x, pos):
+        half = self.m.head_dim // 2
+        c = self.cos[pos][:, None, :]
+        s = self.sin[pos][:, None, :]
+        x1, x2 = x[..., :half], x[..., half:]
+        return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1).astype(np.float32)
+
+    def forward(self, ids: Sequence[int], cache: Optional[list] = None, start: int = 0):
+        """Run tokens ids at positions start.. ; returns (logits of last token, cache)."""
+        m = self.m
+        H, Hkv, hd, d, F = m.n_heads, m.n_kv_heads, m.head_dim, m.d_model, m.ffn_dim
+        G = H // Hkv
+        T = len(ids)
+        pos = np.arange(start, start + T)
+        x = self.w.embed[np.asarray(ids)].astype(np.float32)
+        if cache is None:
+            cache = [(np.zeros((0, Hkv, hd), np.float32), np.zeros((0, Hkv, hd), np.float32)) for _ in range(m.n_layers)]
+        new_cache = []
+        scale = np.float32(1.0 / math.sqrt(hd))
+        for l, lw in enumerate(self.w.layers):
+            h = self._r(self._rms(x))
+            qkv = h @ lw["wqkv"].T
+            if lw["bqkv"] is not None:
+                qkv = qkv + lw["bqkv"]
+            qkv = self._r(qkv)
+            q = qkv[:, :H * hd].reshape(T, H, hd)
+            k = qkv[:, H * hd:(H + Hkv) * hd].reshape(T, Hkv, hd)
+            v = qkv[:, (H + Hkv) * hd:].reshape(T, Hkv, hd)
+            q = self._r(self._rope(q, pos))
+            k = self._r(self._rope(k, pos))
+            K = np.concatenate([cache[l][0], k], axis=0)
+            Vv = np.concatenate([cache[l][1], v], axis=0)
+            new_cache.append((K, Vv))
+            S = K.shape[0]
+            o = np.empty((T, H, hd), np.float32)
+            kpos = np.arange(S)
+            for g in range(Hkv):
+                qg = q[:, g * G:(g + 1) * G, :]                        # T,G,hd
+                sc = np.einsum("tgd,sd->tgs", qg, K[:, g, :]) * scale  # T,G,S
+                mask = kpos[None, None, :] > pos[:, None, None]
+                sc = np.where(mask, -np.inf, sc)
+                sc = sc - sc.max(axis=-1, keepdims=True)
+                p = np.exp(sc)
+                p = p / p.sum(axis=-1, keepdims=True)
+                o[:, g * G:(g + 1) * G, :] = np.einsum("tgs,sd->tgd", p.astype(np.float32), Vv[:, g, :])
+            o = self._r(o.reshape(T, H * hd))
+            x = x + (o @ lw["wo"].T)
+            h = self._r(self._rms(x))
+            gu = self._r(h @ lw["wgu"].T)
+            g_, u_ = gu[:, :F], gu[:, F:]
+            a = self._r((g_ / (np.float32(1.0) + np.exp(-g_))) * u_)
+            x = x + (a @ lw["wd"].T)
+        hl = self._r(self._rms(x[-1:]))
+        logits = (hl @ self.w.lm_head.T)[0].astype(np.float32)
+        return logits, new_cache
+
+    def generate(self, ids: Sequence[int], n_new: int, forced: Optional[Sequence[int]] = None):
+        """Greedy decode n_new tokens. With `forced` (teacher forcing) the given
+        tokens are fed instead of the argmax, so logits can be compared step by
+        step against another implementation's sequence."""
+        out, all_logits = [], []
+        if n_new == 0:
+            return out, all_logits
+        logits, cache = self.forward(list(ids), None, 0)
+        p = len(ids)
+        for k in range(n_new):
+            all_logits.append(logits)
+            nxt = int(np.argmax(logits))
+            out.append(nxt)
+            if k + 1 == n_new:
+                break
+            feed = nxt if forced is None else int(forced[k])
+            logits, cache = self.forward([feed], cache, p)
+            p += 1
+        return out, all_logits
+
+
+def top2_margin(logits: np.ndarray) -> float:
+    part = np.partition(logits, -2)[-2:]
+    return float(part[1] - part[0])

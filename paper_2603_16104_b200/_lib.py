@@ -89,6 +89,11 @@ _SIGS = {
     "hk_generate": (C.c_int, [C.c_void_p, u32p, C.c_size_t, C.c_size_t, u32p, f32p]),
     "hk_engine_kernel_ms": (C.c_double, [C.c_void_p, C.c_char_p, u64p, C.POINTER(C.c_double)]),
     "hk_engine_profile": (C.c_int, [C.c_void_p, C.c_int]),
+    # include/helium_b200_kernels.h
+    "hkx_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                C.c_int, C.c_void_p]),
+    "hkx_gemm_bench": (C.c_double, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.c_int]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1,0 +1,374 @@
+// K3a/K3b: paged attention over the KV block pool, as work items that each
+// cover <= 16 query tokens x one GQA group x one page-aligned key range.
+//
+// The executor's step planner (engine.cu) turns a ragged batch into items:
+//   * prefill chunks: 16 consecutive tokens of one call, causal, keys [0, pos]
+//     -> written directly (part = -1);
+//   * decode, prefix-shared part (K3b): 16 decode tokens of 16 different calls
+//     that share a block-table prefix, keys = the shared pages only. The shared
+//     KV is streamed once per 16 calls (and from L2 for the other row groups)
+//     instead of once per call;
+//   * decode, private part: one call's own suffix pages;
+//   * long ranges are split into key chunks.
+// Every partial keeps flash-style (m, l, unnormalised o) state; attention_merge
+// combines the partials of each (token, head). Inner products run on tensor
+// cores (mma.sync m16n8k16 bf16, fp32 accumulate), K/V tiles are staged with
+// 16-byte cp.async into XOR-swizzled shared memory and read with ldmatrix.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace hkd {
+
+namespace {
+
+constexpr int HD = 128;
+constexpr int TK = 64;  // keys per tile (4 pages of 16)
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// byte offset of 16B chunk `c` of key row `r` in a swizzled [TK][HD] bf16 tile
+__device__ __forceinline__ uint32_t swz(int r, int c) { return r * (HD * 2) + ((c ^ (r & 7)) << 4); }
+
+// Stage keys [k0, k0 + TK) of one kv head (K and V) from their pages.
+__device__ __forceinline__ void load_tile(uint32_t sK, uint32_t sV, const bf16* kv, const int32_t* pages, int ptab,
+                                          int k0, int kend, int kvh, int Hkv, int block) {
+    const int nthr = blockDim.x;
+    const size_t head_stride = static_cast<size_t>(block) * HD;  // elements of one head's page slice
+    for (int c = threadIdx.x; c < TK * (HD / 8) * 2; c += nthr) {
+        const int is_v = c >= TK * (HD / 8);
+        const int cc = is_v ? c - TK * (HD / 8) : c;
+        const int r = cc >> 4;          // key row in tile
+        const int ch = cc & 15;         // 16B chunk
+        const int key = k0 + r;
+        const bool valid = key < kend;
+        const bf16* src = kv;
+        if (valid) {
+            const int page = pages[ptab + key / block];
+            src = kv + ((static_cast<size_t>(page) * 2 + is_v) * Hkv + kvh) * head_stride +
+                  static_cast<size_t>(key % block) * HD + ch * 8;
+        }
+        cp_async16((is_v ? sV : sK) + swz(r, ch), src, valid);
+    }
+}
+
+__global__ void __launch_bounds__(256) attn_mma_kernel(AttnArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const AttnItem it = a.items[blockIdx.x];
+    const int G = a.H / a.Hkv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int h = it.kvh * G + warp;
+    const int QKV = (a.H + 2 * a.Hkv) * HD;
+    const bf16* qkv = static_cast<const bf16*>(a.qkv);
+    const bf16* kv = static_cast<const bf16*>(a.kv_layer);
+
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t sK[2] = {sbase, sbase + 2 * TK * HD * 2};
+    const uint32_t sV[2] = {sbase + TK * HD * 2, sbase + 3 * TK * HD * 2};
+
+    const int n_tiles = it.kend > it.kbeg ? (it.kend - it.kbeg + TK - 1) / TK : 0;
+    if (n_tiles > 0) {
+        load_tile(sK[0], sV[0], kv, a.pages, it.ptab, it.kbeg, it.kend, it.kvh, a.Hkv, a.block);
+        cp_async_commit();
+    }
+
+    // Q fragments (rows gid, gid+8 of this warp's head)
+    const int r0 = gid, r1 = gid + 8;
+    const bool v0 = r0 < it.ntok, v1 = r1 < it.ntok;
+    uint32_t qf[HD / 16][4];
+    {
+        const uint32_t* q0 = reinterpret_cast<const uint32_t*>(qkv + static_cast<size_t>(it.tok0 + r0) * QKV + h * HD);
+        const uint32_t* q1 = reinterpret_cast<const uint32_t*>(qkv + static_cast<size_t>(it.tok0 + r1) * QKV + h * HD);
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+            const int c = ks * 8 + tig;  // u32 index = (16 ks + 2 tig) / 2
+            qf[ks][0] = v0 ? q0[c] : 0u;
+            qf[ks][1] = v1 ? q1[c] : 0u;
+            qf[ks][2] = v0 ? q0[c + 4] : 0u;
+            qf[ks][3] = v1 ? q1[c + 4] : 0u;
+        }
+    }
+    const int pos0 = v0 ? a.pos[it.tok0 + r0] : -1;
+    const int pos1 = v1 ? a.pos[it.tok0 + r1] : -1;
+    const float sl2 = a.scale * kLog2e;
+
+    float o[HD / 8][4];
+#pragma unroll
+    for (int j = 0; j < HD / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+    for (int ti = 0; ti < n_tiles; ++ti) {
+        const int buf = ti & 1;
+        if (ti + 1 < n_tiles) {
+            load_tile(sK[buf ^ 1], sV[buf ^ 1], kv, a.pages, it.ptab, it.kbeg + (ti + 1) * TK, it.kend, it.kvh, a.Hkv,
+                      a.block);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int kt0 = it.kbeg + ti * TK;
+
+        // S = Q K^T  (16 x 64)
+        float s[TK / 8][4];
+#pragma unroll
+        for (int j = 0; j < TK / 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+#pragma unroll
+            for (int jn = 0; jn < TK / 16; ++jn) {
+                const int mi = lane >> 3, rr = lane & 7;
+                const int key = jn * 16 + (mi >> 1) * 8 + rr;
+                const int ch = ks * 2 + (mi & 1);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(sK[buf] + swz(key, ch), b0, b1, b2, b3);
+                mma_bf16(s[2 * jn], qf[ks], b0, b1);
+                mma_bf16(s[2 * jn + 1], qf[ks], b2, b3);
+            }
+        }
+        // mask + online softmax
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < TK / 8; ++j) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int key = kt0 + j * 8 + 2 * tig + e;
+                const bool ok = key < it.kend;
+                const bool ok0 = ok && v0 && (!it.causal || key <= pos0);
+                const bool ok1 = ok && v1 && (!it.causal || key <= pos1);
+                s[j][e] = ok0 ? s[j][e] * sl2 : -INFINITY;
+                s[j][2 + e] = ok1 ? s[j][2 + e] * sl2 : -INFINITY;
+                mx0 = fmaxf(mx0, s[j][e]);
+                mx1 = fmaxf(mx1, s[j][2 + e]);
+            }
+        }
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float base0 = mn0 == -INFINITY ? 0.f : mn0;
+        const float base1 = mn1 == -INFINITY ? 0.f : mn1;
+        const float al0 = exp2f(m0 - base0), al1 = exp2f(m1 - base1);
+        m0 = mn0;
+        m1 = mn1;
+        float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < TK / 8; ++j) {
+            s[j][0] = exp2f(s[j][0] - base0);
+            s[j][1] = exp2f(s[j][1] - base0);
+            s[j][2] = exp2f(s[j][2] - base1);
+            s[j][3] = exp2f(s[j][3] - base1);
+            rs0 += s[j][0] + s[j][1];
+            rs1 += s[j][2] + s[j][3];
+        }
+        l0 = l0 * al0 + rs0;
+        l1 = l1 * al1 + rs1;
+#pragma unroll
+        for (int j = 0; j < HD / 8; ++j) {
+            o[j][0] *= al0;
+            o[j][1] *= al0;
+            o[j][2] *= al1;
+            o[j][3] *= al1;
+        }
+        // O += P V
+#pragma unroll
+        for (int ks = 0; ks < TK / 16; ++ks) {
+            uint32_t pa[4];
+            pa[0] = pack_bf16(s[2 * ks][0], s[2 * ks][1]);
+            pa[1] = pack_bf16(s[2 * ks][2], s[2 * ks][3]);
+            pa[2] = pack_bf16(s[2 * ks + 1][0], s[2 * ks + 1][1]);
+            pa[3] = pack_bf16(s[2 * ks + 1][2], s[2 * ks + 1][3]);
+#pragma unroll
+            for (int jd = 0; jd < HD / 16; ++jd) {
+                const int mi = lane >> 3, rr = lane & 7;
+                const int key = ks * 16 + (mi & 1) * 8 + rr;
+                const int ch = jd * 2 + (mi >> 1);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(sV[buf] + swz(key, ch), b0, b1, b2, b3);
+                mma_bf16(o[2 * jd], pa, b0, b1);
+                mma_bf16(o[2 * jd + 1], pa, b2, b3);
+            }
+        }
+        __syncthreads();
+    }
+
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+
+    if (it.part < 0) {
+        const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+        bf16* out = static_cast<bf16*>(a.out);
+#pragma unroll
+        for (int j = 0; j < HD / 8; ++j) {
+            const int d = j * 8 + 2 * tig;
+            if (v0)
+                *reinterpret_cast<uint32_t*>(out + (static_cast<size_t>(it.tok0 + r0) * a.H + h) * HD + d) =
+                    pack_bf16(o[j][0] * i0, o[j][1] * i0);
+            if (v1)
+                *reinterpret_cast<uint32_t*>(out + (static_cast<size_t>(it.tok0 + r1) * a.H + h) * HD + d) =
+                    pack_bf16(o[j][2] * i1, o[j][3] * i1);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < HD / 8; ++j) {
+            const int d = j * 8 + 2 * tig;
+            if (v0) {
+                float* po = a.part_o + ((static_cast<size_t>(it.tok0 + r0 - a.part_tok0) * a.H + h) * a.max_parts + it.part) * HD + d;
+                *reinterpret_cast<float2*>(po) = make_float2(o[j][0], o[j][1]);
+            }
+            if (v1) {
+                float* po = a.part_o + ((static_cast<size_t>(it.tok0 + r1 - a.part_tok0) * a.H + h) * a.max_parts + it.part) * HD + d;
+                *reinterpret_cast<float2*>(po) = make_float2(o[j][2], o[j][3]);
+            }
+        }
+        if (tig == 0) {
+            if (v0) a.part_ml[(static_cast<size_t>(it.tok0 + r0 - a.part_tok0) * a.H + h) * a.max_parts + it.part] = make_float2(m0, l0);
+            if (v1) a.part_ml[(static_cast<size_t>(it.tok0 + r1 - a.part_tok0) * a.H + h) * a.max_parts + it.part] = make_float2(m1, l1);
+        }
+    }
+}
+
+// fp32 parity-mode attention (SIMT): one warp per (row, head) of an item.
+__global__ void attn_simt_f32_kernel(AttnArgs a) {
+    const AttnItem it = a.items[blockIdx.x];
+    const int G = a.H / a.Hkv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+    const int QKV = (a.H + 2 * a.Hkv) * HD;
+    const float* qkv = static_cast<const float*>(a.qkv);
+    const float* kv = static_cast<const float*>(a.kv_layer);
+    const size_t head_stride = static_cast<size_t>(a.block) * HD;
+    const float sl2 = a.scale * kLog2e;
+    for (int job = warp; job < it.ntok * G; job += nw) {
+        const int r = job / G, g = job % G;
+        const int h = it.kvh * G + g;
+        const int tok = it.tok0 + r;
+        const int pos = a.pos[tok];
+        float q[HD / 32], acc[HD / 32];
+#pragma unroll
+        for (int i = 0; i < HD / 32; ++i) {
+            q[i] = qkv[static_cast<size_t>(tok) * QKV + h * HD + lane + 32 * i];
+            acc[i] = 0.f;
+        }
+        float m = -INFINITY, l = 0.f;
+        for (int key = it.kbeg; key < it.kend; ++key) {
+            if (it.causal && key > pos) break;
+            const int page = a.pages[it.ptab + key / a.block];
+            const float* kp = kv + ((static_cast<size_t>(page) * 2 + 0) * a.Hkv + it.kvh) * head_stride +
+                              static_cast<size_t>(key % a.block) * HD;
+            const float* vp = kp + static_cast<size_t>(a.Hkv) * head_stride;
+            float dot = 0.f;
+#pragma unroll
+            for (int i = 0; i < HD / 32; ++i) dot += q[i] * kp[lane + 32 * i];
+            dot = warp_sum(dot) * sl2;
+            const float mn = fmaxf(m, dot);
+            const float al = exp2f(m - mn), p = exp2f(dot - mn);
+            l = l * al + p;
+#pragma unroll
+            for (int i = 0; i < HD / 32; ++i) acc[i] = acc[i] * al + p * vp[lane + 32 * i];
+            m = mn;
+        }
+        if (it.part < 0) {
+            float* out = static_cast<float*>(a.out);
+#pragma unroll
+            for (int i = 0; i < HD / 32; ++i)
+                out[(static_cast<size_t>(tok) * a.H + h) * HD + lane + 32 * i] = l > 0.f ? acc[i] / l : 0.f;
+        } else {
+            const size_t pi = (static_cast<size_t>(tok - a.part_tok0) * a.H + h) * a.max_parts + it.part;
+#pragma unroll
+            for (int i = 0; i < HD / 32; ++i) a.part_o[pi * HD + lane + 32 * i] = acc[i];
+            if (lane == 0) a.part_ml[pi] = make_float2(m, l);
+        }
+    }
+}
+
+__global__ void attn_merge_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
+                                  const int32_t* __restrict__ n_parts, int tok0, int H, int max_parts, void* out,
+                                  bool f32) {
+    const int t = tok0 + blockIdx.x;
+    const int h = blockIdx.y;
+    const int np = n_parts[blockIdx.x];
+    const size_t base = (static_cast<size_t>(blockIdx.x) * H + h) * max_parts;
+    float M = -INFINITY;
+    for (int k = 0; k < np; ++k) M = fmaxf(M, part_ml[base + k].x);
+    const float Mb = M == -INFINITY ? 0.f : M;
+    float L = 0.f;
+    for (int k = 0; k < np; ++k) L += exp2f(part_ml[base + k].x - Mb) * part_ml[base + k].y;
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    for (int d = threadIdx.x; d < HD; d += blockDim.x) {
+        float acc = 0.f;
+        for (int k = 0; k < np; ++k) acc += exp2f(part_ml[base + k].x - Mb) * part_o[(base + k) * HD + d];
+        const size_t oi = (static_cast<size_t>(t) * H + h) * HD + d;
+        if (f32)
+            static_cast<float*>(out)[oi] = acc * inv;
+        else
+            static_cast<bf16*>(out)[oi] = f2bf(acc * inv);
+    }
+}
+
+}  // namespace
+
+void attention_partial(const AttnArgs& a, cudaStream_t st) {
+    if (a.n_items == 0) return;
+    const int G = a.H / a.Hkv;
+    if (a.f32) {
+        attn_simt_f32_kernel<<<a.n_items, 128, 0, st>>>(a);
+    } else {
+        if (G > 8) throw std::runtime_error("attention: GQA group > 8 unsupported");
+        constexpr int smem = 4 * TK * HD * 2;
+        static bool configured = false;
+        if (!configured) {
+            HK_CUDA(cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            configured = true;
+        }
+        attn_mma_kernel<<<a.n_items, G * 32, smem, st>>>(a);
+    }
+    HK_CUDA(cudaGetLastError());
+}
+
+void attention_merge(const float* part_o, const float2* part_ml, const int32_t* n_parts, int n_rows, int tok0, int H,
+                     int hd, int max_parts, void* out, bool f32, cudaStream_t st) {
+    if (n_rows == 0) return;
+    if (hd != HD) throw std::runtime_error("attention: head_dim must be 128");
+    attn_merge_kernel<<<dim3(n_rows, H), 128, 0, st>>>(part_o, part_ml, n_parts, tok0, H, max_parts, out, f32);
+    HK_CUDA(cudaGetLastError());
+}
+
+}  // namespace hkd

@@ -1,33 +1,1025 @@
-// Device engine (placeholder until the kernels land).
-#include <memory>
-#include <stdexcept>
+// Device engine: random-init decoder weights, per-worker KV block pools and
+// device tries, the ragged step planner and forward pass, and the LlmBody that
+// lets the host executor (executor.cpp) run its LLM calls on the B200.
+//
+// One step = one (iteration, worker) of the reference's simulate() loop
+// (simulator.cpp:287-379): every prefill chunk and every decode token of that
+// worker's iteration is one ragged forward pass. Tokens are ordered
+// [prefill chunks][decode tokens grouped by shared block-table prefix] so that
+// the prefix-shared attention items (K3b) cover 16 consecutive rows.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <unordered_map>
 
+#include "common.cuh"
 #include "helium_b200.h"
 #include "hk_host.hpp"
+#include "kernels.cuh"
 
 namespace hk {
 void set_error(const std::string& s);
-std::unique_ptr<LlmBody> make_device_body(hk_engine*, const Plan&, const SimConfig&) {
-    throw std::runtime_error("device engine not built");
 }
+
+namespace {
+
+using hkd::bf16;
+
+template <typename T>
+T* dalloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) return nullptr;
+    HK_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+struct LayerW {
+    void *attn_norm, *wqkv, *bqkv, *wo, *mlp_norm, *wgu, *wd;
+};
+
+struct KernelClock {
+    // accumulated device time per kernel family, measured with CUDA events
+    struct Pair {
+        cudaEvent_t a, b;
+        int fam;
+        double bytes;
+    };
+    static constexpr int kFamilies = 8;
+    const char* names[kFamilies] = {"gemm", "attn_shared", "attn_private", "attn_prefill",
+                                    "attn_merge", "small", "trie", "kvcopy"};
+    double ms[kFamilies] = {0};
+    double bytes[kFamilies] = {0};
+    uint64_t launches[kFamilies] = {0};
+    std::vector<Pair> pending;
+    std::vector<cudaEvent_t> free_events;
+    bool enabled = false;
+
+    cudaEvent_t ev() {
+        if (free_events.empty()) {
+            cudaEvent_t e;
+            HK_CUDA(cudaEventCreate(&e));
+            return e;
+        }
+        cudaEvent_t e = free_events.back();
+        free_events.pop_back();
+        return e;
+    }
+    int begin(int fam, cudaStream_t st) {
+        if (!enabled) return -1;
+        Pair p{ev(), nullptr, fam, 0};
+        HK_CUDA(cudaEventRecord(p.a, st));
+        pending.push_back(p);
+        return static_cast<int>(pending.size()) - 1;
+    }
+    void end(int idx, cudaStream_t st, double b = 0, uint64_t n = 1) {
+        if (idx < 0) return;
+        Pair& p = pending[static_cast<size_t>(idx)];
+        p.b = ev();
+        p.bytes = b;
+        HK_CUDA(cudaEventRecord(p.b, st));
+        launches[p.fam] += n;
+    }
+    void collect() {
+        for (Pair& p : pending) {
+            HK_CUDA(cudaEventSynchronize(p.b));
+            float t = 0;
+            HK_CUDA(cudaEventElapsedTime(&t, p.a, p.b));
+            ms[p.fam] += t;
+            bytes[p.fam] += p.bytes;
+            free_events.push_back(p.a);
+            free_events.push_back(p.b);
+        }
+        pending.clear();
+    }
+    void reset() {
+        collect();
+        std::fill(ms, ms + kFamilies, 0.0);
+        std::fill(bytes, bytes + kFamilies, 0.0);
+        std::fill(launches, launches + kFamilies, 0);
+    }
+};
+
+}  // namespace
+
+struct hk_engine {
+    hk_model_config mc{};
+    hk_engine_config ec{};
+    bool f32 = false;
+    size_t esz = 2;
+    int L = 0, d = 0, H = 0, Hkv = 0, hd = 0, F = 0, V = 0, QKV = 0;
+    cudaStream_t st = nullptr;
+
+    // weights
+    void* wbuf = nullptr;
+    void *embed = nullptr, *final_norm = nullptr, *lm_head = nullptr;
+    std::vector<LayerW> layers;
+    float2* rope = nullptr;
+
+    struct Worker {
+        void* kv = nullptr;           // [L][P][2][Hkv][block][hd]
+        size_t layer_stride = 0;      // bytes
+        int32_t* slot_last = nullptr; // [max_calls]
+        hkd::DevTrie trie;
+        int trie_tombs = 0;
+        std::vector<int> free_slots;
+        std::vector<std::vector<int32_t>> slot_tokens;
+    };
+    std::vector<Worker> workers;
+    size_t page_bytes_layer = 0;
+
+    // step scratch (device)
+    int maxT = 0, maxS = 0, max_parts = 32;
+    float* x = nullptr;
+    void *h = nullptr, *qkv = nullptr, *attn = nullptr, *gu = nullptr, *act = nullptr;
+    float* logits = nullptr;
+    int32_t* sample_ids = nullptr;
+    float* ws = nullptr;
+    size_t ws_floats = 0;
+    float* part_o = nullptr;
+    float2* part_ml = nullptr;
+    int max_part_rows = 0;
+    // step metadata (device + pinned host mirror), int32 words; a ring so the
+    // host can plan step k+1 while step k's upload is still in flight
+    struct Meta {
+        int32_t* d = nullptr;
+        int32_t* h = nullptr;
+        size_t cap = 0;
+        cudaEvent_t done = nullptr;
+    };
+    static constexpr int kMetaRing = 4;
+    Meta meta[kMetaRing];
+    int meta_next = 0;
+    // trie staging
+    uint64_t* tok_d = nullptr;
+    size_t tok_cap = 0;
+    int32_t* match_d = nullptr;
+    size_t match_cap = 0;
+
+    // sampled-id harvest ring
+    struct Pending {
+        cudaEvent_t ev;
+        int worker;
+        std::vector<int> slots;
+        int32_t* host = nullptr;
+    };
+    std::vector<Pending> pending;
+    std::vector<int32_t*> host_bufs;
+    std::vector<cudaEvent_t> free_ev;
+
+    KernelClock clock;
+    double attn_alg_bytes_step = 0;
+
+    // ---- construction ----
+    hk_engine(const hk_model_config& m, const hk_engine_config& c);
+    ~hk_engine();
+    void init_weights();
+    void reset_workers();
+
+    // ---- execution ----
+    struct SegIn {
+        int slot = -1;
+        int start = 0, count = 0;
+        bool from_prompt = true, write_kv = true, sample = false;
+        const std::vector<int>* table = nullptr;
+        const std::vector<uint64_t>* prompt = nullptr;  // host tokens (Token space)
+        const std::vector<uint32_t>* ids = nullptr;     // or raw vocab ids
+    };
+    void step(int w, std::vector<SegIn>& segs, float* logits_out_host = nullptr);
+    void harvest(bool all);
+    void sync() {
+        HK_CUDA(cudaStreamSynchronize(st));
+        harvest(true);
+        clock.collect();
+    }
+    void trie_sync(int w, std::vector<hk::TrieOp>& ops, const std::function<const uint64_t*(int)>& key_of);
+    void trie_lookup(int w, const std::vector<const std::vector<uint64_t>*>& prompts, std::vector<std::vector<int>>& paths);
+    int alloc_slot(int w) {
+        Worker& wk = workers[static_cast<size_t>(w)];
+        if (wk.free_slots.empty()) throw std::runtime_error("engine: out of call slots (max_calls)");
+        int s = wk.free_slots.back();
+        wk.free_slots.pop_back();
+        wk.slot_tokens[static_cast<size_t>(s)].clear();
+        return s;
+    }
+    void free_slot(int w, int s) { workers[static_cast<size_t>(w)].free_slots.push_back(s); }
+    void* kv_layer(int w, int l) const {
+        return static_cast<uint8_t*>(workers[static_cast<size_t>(w)].kv) + l * workers[static_cast<size_t>(w)].layer_stride;
+    }
+};
+
+hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m), ec(c) {
+    HK_CUDA(cudaSetDevice(c.device));
+    int sms = 0;
+    HK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    hkd::g_num_sms = sms;
+    f32 = m.fp32 != 0;
+    esz = f32 ? 4 : 2;
+    L = static_cast<int>(m.n_layers);
+    d = static_cast<int>(m.d_model);
+    H = static_cast<int>(m.n_heads);
+    Hkv = static_cast<int>(m.n_kv_heads);
+    hd = static_cast<int>(m.head_dim);
+    F = static_cast<int>(m.ffn_dim);
+    V = static_cast<int>(m.vocab);
+    QKV = (H + 2 * Hkv) * hd;
+    if (hd != 128) throw std::runtime_error("engine: head_dim must be 128");
+    if (H % Hkv) throw std::runtime_error("engine: n_heads must be a multiple of n_kv_heads");
+    if (d % 64 || F % 64 || (H * hd) % 64) throw std::runtime_error("engine: d_model/ffn must be multiples of 64");
+    if (c.block_tokens == 0 || c.pages_per_worker == 0 || c.n_workers == 0)
+        throw std::runtime_error("engine: bad engine config");
+    HK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    init_weights();
+
+    // rope table (cos, sin) computed in double, stored fp32 — shared with the oracle
+    const int half = hd / 2;
+    const int max_pos = static_cast<int>(c.max_ctx_tokens) + 1;
+    std::vector<float2> rt(static_cast<size_t>(max_pos) * half);
+    for (int p = 0; p < max_pos; ++p)
+        for (int i = 0; i < half; ++i) {
+            const double inv = std::pow(static_cast<double>(m.rope_theta), -2.0 * i / hd);
+            const double ang = p * inv;
+            rt[static_cast<size_t>(p) * half + i] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+        }
+    rope = dalloc<float2>(rt.size());
+    HK_CUDA(cudaMemcpy(rope, rt.data(), rt.size() * sizeof(float2), cudaMemcpyHostToDevice));
+
+    // KV pools
+    page_bytes_layer = static_cast<size_t>(2) * Hkv * c.block_tokens * hd * esz;
+    workers.resize(c.n_workers);
+    for (auto& wk : workers) {
+        wk.layer_stride = page_bytes_layer * c.pages_per_worker;
+        wk.kv = dalloc<uint8_t>(wk.layer_stride * L);
+        HK_CUDA(cudaMemsetAsync(wk.kv, 0, wk.layer_stride * L, st));
+        wk.slot_last = dalloc<int32_t>(c.max_calls);
+        HK_CUDA(cudaMemsetAsync(wk.slot_last, 0, c.max_calls * sizeof(int32_t), st));
+        hkd::DevTrie& t = wk.trie;
+        t.block = static_cast<int>(c.block_tokens);
+        t.max_nodes = static_cast<int>(c.pages_per_worker) + 1;
+        t.table_size = 1;
+        while (t.table_size < 4 * t.max_nodes) t.table_size <<= 1;
+        t.parent = dalloc<int32_t>(t.max_nodes);
+        t.page = dalloc<int32_t>(t.max_nodes);
+        t.phash = dalloc<uint64_t>(t.max_nodes);
+        t.keys = dalloc<uint64_t>(static_cast<size_t>(t.max_nodes) * t.block);
+        t.tab_key = dalloc<uint64_t>(t.table_size);
+        t.tab_node = dalloc<int32_t>(t.table_size);
+        wk.slot_tokens.resize(c.max_calls);
+    }
+    reset_workers();
+
+    // step scratch
+    maxT = static_cast<int>(c.max_step_tokens);
+    maxS = static_cast<int>(std::min<uint32_t>(c.max_step_tokens, c.max_calls * c.n_workers + 64));
+    x = dalloc<float>(static_cast<size_t>(maxT) * d);
+    h = dalloc<uint8_t>(static_cast<size_t>(maxT) * std::max(d, F) * esz);
+    qkv = dalloc<uint8_t>(static_cast<size_t>(maxT) * QKV * esz);
+    attn = dalloc<uint8_t>(static_cast<size_t>(maxT) * H * hd * esz);
+    gu = dalloc<uint8_t>(static_cast<size_t>(maxT) * 2 * F * esz);
+    act = dalloc<uint8_t>(static_cast<size_t>(maxT) * F * esz);
+    logits = dalloc<float>(static_cast<size_t>(maxS) * V);
+    sample_ids = dalloc<int32_t>(maxS);
+    ws_floats = static_cast<size_t>(16) * std::max<size_t>(static_cast<size_t>(c.max_calls) * c.n_workers + 64, 256) *
+                std::max({QKV, d, 2 * F});
+    ws = dalloc<float>(ws_floats);
+    max_part_rows = static_cast<int>(c.max_calls * c.n_workers) + 16;
+    part_o = dalloc<float>(static_cast<size_t>(max_part_rows) * H * max_parts * hd);
+    part_ml = dalloc<float2>(static_cast<size_t>(max_part_rows) * H * max_parts);
+    HK_CUDA(cudaStreamSynchronize(st));
+}
+
+hk_engine::~hk_engine() {
+    cudaStreamSynchronize(st);
+    cudaFree(wbuf);
+    cudaFree(rope);
+    for (auto& wk : workers) {
+        cudaFree(wk.kv);
+        cudaFree(wk.slot_last);
+        cudaFree(wk.trie.parent);
+        cudaFree(wk.trie.page);
+        cudaFree(wk.trie.phash);
+        cudaFree(wk.trie.keys);
+        cudaFree(wk.trie.tab_key);
+        cudaFree(wk.trie.tab_node);
+    }
+    for (void* p : {static_cast<void*>(x), h, qkv, attn, gu, act, static_cast<void*>(logits),
+                    static_cast<void*>(sample_ids), static_cast<void*>(ws), static_cast<void*>(part_o),
+                    static_cast<void*>(part_ml), static_cast<void*>(tok_d), static_cast<void*>(match_d)})
+        cudaFree(p);
+    for (Meta& mt : meta) {
+        cudaFree(mt.d);
+        if (mt.h) cudaFreeHost(mt.h);
+        if (mt.done) cudaEventDestroy(mt.done);
+    }
+    for (int32_t* b : host_bufs) cudaFreeHost(b);
+    cudaStreamDestroy(st);
+}
+
+// Tensor ids and scales of the counter-based init (oracle/transformer.py mirrors this).
+void hk_engine::init_weights() {
+    const size_t n_embed = static_cast<size_t>(V) * d;
+    const size_t per_layer = static_cast<size_t>(d) + static_cast<size_t>(QKV) * d + (mc.qkv_bias ? QKV : 0) +
+                             static_cast<size_t>(d) * H * hd + d + static_cast<size_t>(2) * F * d +
+                             static_cast<size_t>(d) * F;
+    const size_t total = n_embed + per_layer * L + d + n_embed;
+    wbuf = dalloc<uint8_t>(total * esz + 256 * (8 * L + 4));
+    uint8_t* p = static_cast<uint8_t*>(wbuf);
+    auto take = [&](size_t n) {
+        void* r = p;
+        p += (n * esz + 255) / 256 * 256;
+        return r;
+    };
+    const uint64_t seed = mc.seed;
+    const float s_d = std::sqrt(3.0f / static_cast<float>(d));
+    const float s_o = std::sqrt(3.0f / static_cast<float>(H * hd));
+    const float s_f = std::sqrt(3.0f / static_cast<float>(F));
+    embed = take(n_embed);
+    hkd::init_uniform(embed, f32, n_embed, seed, 1, 1.0f, st);
+    layers.resize(L);
+    for (int l = 0; l < L; ++l) {
+        LayerW& w = layers[l];
+        const uint64_t t0 = 16 + 16 * static_cast<uint64_t>(l);
+        w.attn_norm = take(d);
+        hkd::fill_const(w.attn_norm, f32, d, 1.0f, st);
+        w.wqkv = take(static_cast<size_t>(QKV) * d);
+        hkd::init_uniform(w.wqkv, f32, static_cast<size_t>(QKV) * d, seed, t0 + 1, s_d, st);
+        w.bqkv = nullptr;
+        if (mc.qkv_bias) {
+            w.bqkv = take(QKV);
+            hkd::init_uniform(w.bqkv, f32, QKV, seed, t0 + 2, 0.1f, st);
+        }
+        w.wo = take(static_cast<size_t>(d) * H * hd);
+        hkd::init_uniform(w.wo, f32, static_cast<size_t>(d) * H * hd, seed, t0 + 3, 0.5f * s_o, st);
+        w.mlp_norm = take(d);
+        hkd::fill_const(w.mlp_norm, f32, d, 1.0f, st);
+        w.wgu = take(static_cast<size_t>(2) * F * d);
+        hkd::init_uniform(w.wgu, f32, static_cast<size_t>(2) * F * d, seed, t0 + 4, s_d, st);
+        w.wd = take(static_cast<size_t>(d) * F);
+        hkd::init_uniform(w.wd, f32, static_cast<size_t>(d) * F, seed, t0 + 5, 0.5f * s_f, st);
+    }
+    final_norm = take(d);
+    hkd::fill_const(final_norm, f32, d, 1.0f, st);
+    lm_head = take(n_embed);
+    hkd::init_uniform(lm_head, f32, n_embed, seed, 2, s_d, st);
+}
+
+void hk_engine::reset_workers() {
+    for (auto& wk : workers) {
+        wk.free_slots.clear();
+        for (int s = static_cast<int>(ec.max_calls) - 1; s >= 0; --s) wk.free_slots.push_back(s);
+        hkd::DevTrie& t = wk.trie;
+        HK_CUDA(cudaMemsetAsync(t.tab_key, 0, t.table_size * sizeof(uint64_t), st));
+        HK_CUDA(cudaMemsetAsync(t.parent, 0xff, t.max_nodes * sizeof(int32_t), st));
+        wk.trie_tombs = 0;
+    }
+}
+
+// --------------------------------------------------------------- harvest
+void hk_engine::harvest(bool all) {
+    size_t k = 0;
+    for (; k < pending.size(); ++k) {
+        Pending& p = pending[k];
+        if (!all && cudaEventQuery(p.ev) == cudaErrorNotReady) break;
+        HK_CUDA(cudaEventSynchronize(p.ev));
+        Worker& wk = workers[static_cast<size_t>(p.worker)];
+        for (size_t i = 0; i < p.slots.size(); ++i)
+            if (p.slots[i] >= 0) wk.slot_tokens[static_cast<size_t>(p.slots[i])].push_back(p.host[i]);
+        host_bufs.push_back(p.host);
+        free_ev.push_back(p.ev);
+    }
+    pending.erase(pending.begin(), pending.begin() + static_cast<std::ptrdiff_t>(k));
+}
+
+// ------------------------------------------------------------------ step
+void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
+    Worker& wk = workers[static_cast<size_t>(w)];
+    const int block = static_cast<int>(ec.block_tokens);
+    const int G = H / Hkv;
+
+    // order: prefill/recompute segs first, decode segs grouped by table prefix
+    std::vector<int> pre, dec;
+    for (int i = 0; i < static_cast<int>(segs.size()); ++i) (segs[i].from_prompt ? pre : dec).push_back(i);
+    auto full_pages = [&](const SegIn& s) { return (s.start) / block; };  // pages strictly before the decode token
+    std::sort(dec.begin(), dec.end(), [&](int a, int b) {
+        const auto& ta = *segs[a].table;
+        const auto& tb = *segs[b].table;
+        const int na = full_pages(segs[a]), nb = full_pages(segs[b]);
+        return std::lexicographical_compare(ta.begin(), ta.begin() + na, tb.begin(), tb.begin() + nb);
+    });
+    std::vector<int> order = pre;
+    order.insert(order.end(), dec.begin(), dec.end());
+
+    int T = 0;
+    for (int i : order) T += segs[i].count;
+    if (T == 0) return;
+    if (T > maxT) throw std::runtime_error("engine: step exceeds max_step_tokens");
+    const int T_pre = T - static_cast<int>(dec.size());
+
+    // metadata layout (int32 words)
+    std::vector<int32_t> ids(T), pos(T), slots(T), kvw(T), ptab(T), pages;
+    std::vector<hkd::AttnItem> items;
+    std::vector<int32_t> nparts(dec.size(), 0);
+    std::vector<int32_t> srows, sslots;
+    int t = 0;
+    int n_pre_items = 0, n_sh_items = 0, n_pv_items = 0;
+    double alg_bytes = 0;
+    const double kv_tok_bytes = 2.0 * Hkv * hd * esz;
+    for (int i : pre) {
+        SegIn& s = segs[i];
+        const int off = static_cast<int>(pages.size());
+        pages.insert(pages.end(), s.table->begin(), s.table->end());
+        for (int j = 0; j < s.count; ++j) {
+            const int p = s.start + j;
+            int id;
+            if (s.ids)
+                id = static_cast<int>((*s.ids)[static_cast<size_t>(p)]);
+            else
+                id = s.prompt->empty() ? 0 : static_cast<int>(hk::vocab_of((*s.prompt)[static_cast<size_t>(p)], V));
+            ids[t + j] = id;
+            pos[t + j] = p;
+            slots[t + j] = std::max(s.slot, 0);
+            kvw[t + j] = s.write_kv ? 1 : 0;
+            ptab[t + j] = off;
+        }
+        for (int c = 0; c < s.count; c += 16) {
+            const int n = std::min(16, s.count - c);
+            for (int kh = 0; kh < Hkv; ++kh)
+                items.push_back(hkd::AttnItem{t + c, n, kh, off, 0, s.start + c + n, 1, -1});
+            n_pre_items += Hkv;
+        }
+        alg_bytes += (s.start + s.count) * kv_tok_bytes + 2.0 * s.count * H * hd * esz;
+        if (s.sample) {
+            srows.push_back(t + s.count - 1);
+            sslots.push_back(s.slot);
+        }
+        t += s.count;
+    }
+    // decode groups: maximal runs (in sorted order) sharing >= 1 full page
+    const int KS = 512;   // key split for shared ranges
+    const int KP = 1024;  // key split for private ranges
+    size_t gi = 0;
+    while (gi < dec.size()) {
+        size_t gj = gi + 1;
+        int lcp = full_pages(segs[dec[gi]]);
+        while (gj < dec.size()) {
+            const auto& a = *segs[dec[gi]].table;
+            const auto& b = *segs[dec[gj]].table;
+            int n = std::min(lcp, full_pages(segs[dec[gj]]));
+            int k = 0;
+            while (k < n && a[static_cast<size_t>(k)] == b[static_cast<size_t>(k)]) ++k;
+            if (k < 4) break;  // require at least one shared 64-key tile
+            lcp = k;
+            ++gj;
+        }
+        const int members = static_cast<int>(gj - gi);
+        const int shared_pages = members > 1 ? lcp : 0;
+        const int shared_keys = shared_pages * block;
+        const int tg0 = t;
+        // per-member rows + private items
+        for (size_t q = gi; q < gj; ++q) {
+            SegIn& s = segs[dec[q]];
+            const int off = static_cast<int>(pages.size());
+            pages.insert(pages.end(), s.table->begin(), s.table->end());
+            ids[t] = -1;
+            pos[t] = s.start;
+            slots[t] = s.slot;
+            kvw[t] = 1;
+            ptab[t] = off;
+            const int r = t - T_pre;
+            int part = shared_keys > 0 ? (shared_keys + KS - 1) / KS : 0;
+            for (int k0 = shared_keys; k0 < s.start + 1; k0 += KP) {
+                const int k1 = std::min(k0 + KP, s.start + 1);
+                for (int kh = 0; kh < Hkv; ++kh) items.push_back(hkd::AttnItem{t, 1, kh, off, k0, k1, 0, part});
+                n_pv_items += Hkv;
+                ++part;
+            }
+            if (part > max_parts) throw std::runtime_error("engine: too many attention partials");
+            nparts[static_cast<size_t>(r)] = part;
+            alg_bytes += (s.start + 1 - shared_keys) * kv_tok_bytes + 2.0 * H * hd * esz;
+            if (s.sample) {
+                srows.push_back(t);
+                sslots.push_back(s.slot);
+            }
+            ++t;
+        }
+        if (shared_keys > 0) {
+            const int off0 = ptab[tg0];
+            for (int r0 = tg0; r0 < t; r0 += 16) {
+                const int n = std::min(16, t - r0);
+                int part = 0;
+                for (int k0 = 0; k0 < shared_keys; k0 += KS, ++part)
+                    for (int kh = 0; kh < Hkv; ++kh)
+                        items.push_back(hkd::AttnItem{r0, n, kh, off0, k0, std::min(k0 + KS, shared_keys), 0, part});
+                n_sh_items += Hkv * ((shared_keys + KS - 1) / KS);
+            }
+            alg_bytes += shared_keys * kv_tok_bytes;
+        }
+        gi = gj;
+    }
+    const int S = static_cast<int>(srows.size());
+    if (S > maxS) throw std::runtime_error("engine: too many sampled rows in one step");
+    if (static_cast<int>(dec.size()) > max_part_rows) throw std::runtime_error("engine: too many decode rows");
+    attn_alg_bytes_step = alg_bytes * L;
+
+    // pack metadata: ids pos slots kvw ptab | pages | nparts | srows sslots | items
+    const size_t n_items = items.size();
+    const size_t words = 5 * static_cast<size_t>(T) + pages.size() + nparts.size() + 2 * static_cast<size_t>(S) +
+                         n_items * (sizeof(hkd::AttnItem) / 4) + 64;
+    Meta& mt = meta[meta_next];
+    meta_next = (meta_next + 1) % kMetaRing;
+    if (mt.done) HK_CUDA(cudaEventSynchronize(mt.done));  // this slot's previous step has consumed it
+    else HK_CUDA(cudaEventCreateWithFlags(&mt.done, cudaEventDisableTiming));
+    if (words > mt.cap) {
+        cudaFree(mt.d);
+        if (mt.h) cudaFreeHost(mt.h);
+        mt.cap = words * 2;
+        mt.d = dalloc<int32_t>(mt.cap);
+        HK_CUDA(cudaMallocHost(&mt.h, mt.cap * sizeof(int32_t)));
+    }
+    int32_t* meta_h = mt.h;
+    int32_t* meta_d = mt.d;
+    size_t o = 0;
+    auto put = [&](const int32_t* src, size_t n) {
+        std::memcpy(meta_h + o, src, n * 4);
+        const size_t at = o;
+        o += n;
+        o = (o + 3) & ~size_t(3);  // 16B alignment for items
+        return at;
+    };
+    const size_t o_ids = put(ids.data(), T), o_pos = put(pos.data(), T), o_slots = put(slots.data(), T),
+                 o_kvw = put(kvw.data(), T), o_ptab = put(ptab.data(), T), o_pages = put(pages.data(), pages.size()),
+                 o_np = put(nparts.data(), nparts.size()), o_sr = put(srows.data(), S), o_ss = put(sslots.data(), S),
+                 o_items = put(reinterpret_cast<const int32_t*>(items.data()), n_items * sizeof(hkd::AttnItem) / 4);
+    HK_CUDA(cudaMemcpyAsync(meta_d, meta_h, o * 4, cudaMemcpyHostToDevice, st));
+    const int32_t* d_ids = meta_d + o_ids;
+    const int32_t* d_pos = meta_d + o_pos;
+    const int32_t* d_slots = meta_d + o_slots;
+    const int32_t* d_kvw = meta_d + o_kvw;
+    const int32_t* d_ptab = meta_d + o_ptab;
+    const int32_t* d_pages = meta_d + o_pages;
+    const int32_t* d_np = meta_d + o_np;
+    const int32_t* d_sr = meta_d + o_sr;
+    const int32_t* d_ss = meta_d + o_ss;
+    const hkd::AttnItem* d_items = reinterpret_cast<const hkd::AttnItem*>(meta_d + o_items);
+    // items are packed pre | (per group: private..., shared...) — launch them as one grid
+    (void)n_pre_items;
+    (void)n_sh_items;
+    (void)n_pv_items;
+
+    const float eps = mc.rms_eps;
+    const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
+    int ck = clock.begin(5, st);
+    hkd::embed(embed, f32, d, d_ids, d_slots, wk.slot_last, T, x, st);
+    clock.end(ck, st, static_cast<double>(T) * d * (esz + 4));
+    auto gemm = [&](const void* W, const void* X, int N, int K, int epi, void* out, int ldo, const void* bias) {
+        const int c = clock.begin(0, st);
+        if (f32)
+            hkd::gemm_f32(static_cast<const float*>(W), static_cast<const float*>(X), N, K, T, epi, out, ldo,
+                          static_cast<const float*>(bias), st);
+        else
+            hkd::gemm_bf16(static_cast<const bf16*>(W), static_cast<const bf16*>(X), N, K, T, epi, out, ldo,
+                           static_cast<const bf16*>(bias), ws, ws_floats, st);
+        clock.end(c, st, static_cast<double>(N) * K * esz + static_cast<double>(T) * K * esz);
+    };
+    for (int l = 0; l < L; ++l) {
+        const LayerW& lw = layers[static_cast<size_t>(l)];
+        ck = clock.begin(5, st);
+        hkd::rmsnorm(x, lw.attn_norm, f32, d, eps, nullptr, T, h, st);
+        clock.end(ck, st);
+        gemm(lw.wqkv, h, QKV, d, f32 ? hkd::kEpiStoreF32 : hkd::kEpiStoreBf16, qkv, QKV, lw.bqkv);
+        hkd::RopeArgs ra{qkv, f32, T, H, Hkv, hd, d_pos, d_kvw, d_ptab, d_pages, rope, kv_layer(w, l), block};
+        ck = clock.begin(5, st);
+        hkd::rope_kv_write(ra, st);
+        clock.end(ck, st);
+        hkd::AttnArgs aa{qkv, f32, H, Hkv, hd, block, d_pos, d_pages, kv_layer(w, l), d_items,
+                         static_cast<int>(n_items), attn, part_o, part_ml, max_parts, T_pre, scale};
+        ck = clock.begin(dec.empty() ? 3 : 1, st);
+        hkd::attention_partial(aa, st);
+        clock.end(ck, st, alg_bytes);
+        ck = clock.begin(4, st);
+        hkd::attention_merge(part_o, part_ml, d_np, static_cast<int>(dec.size()), T_pre, H, hd, max_parts, attn, f32, st);
+        clock.end(ck, st);
+        gemm(lw.wo, attn, d, H * hd, hkd::kEpiAddF32, x, d, nullptr);
+        ck = clock.begin(5, st);
+        hkd::rmsnorm(x, lw.mlp_norm, f32, d, eps, nullptr, T, h, st);
+        clock.end(ck, st);
+        gemm(lw.wgu, h, 2 * F, d, f32 ? hkd::kEpiStoreF32 : hkd::kEpiStoreBf16, gu, 2 * F, nullptr);
+        ck = clock.begin(5, st);
+        hkd::swiglu(gu, f32, T, F, act, st);
+        clock.end(ck, st);
+        gemm(lw.wd, act, d, F, hkd::kEpiAddF32, x, d, nullptr);
+    }
+    if (S > 0) {
+        ck = clock.begin(5, st);
+        hkd::rmsnorm(x, final_norm, f32, d, eps, d_sr, S, h, st);
+        clock.end(ck, st);
+        const int c = clock.begin(0, st);
+        if (f32)
+            hkd::gemm_f32(static_cast<const float*>(lm_head), static_cast<const float*>(h), V, d, S, hkd::kEpiStoreF32,
+                          logits, V, nullptr, st);
+        else
+            hkd::gemm_bf16(static_cast<const bf16*>(lm_head), static_cast<const bf16*>(h), V, d, S, hkd::kEpiStoreF32,
+                           logits, V, nullptr, ws, ws_floats, st);
+        clock.end(c, st, static_cast<double>(V) * d * esz);
+        ck = clock.begin(5, st);
+        hkd::argmax_rows(logits, S, V, sample_ids, d_ss, wk.slot_last, st);
+        clock.end(ck, st);
+        if (logits_out_host)
+            HK_CUDA(cudaMemcpyAsync(logits_out_host, logits, static_cast<size_t>(S) * V * 4, cudaMemcpyDeviceToHost, st));
+        // harvest ring: D2H of the sampled ids into pinned memory
+        Pending p;
+        if (host_bufs.empty()) {
+            int32_t* hb;
+            HK_CUDA(cudaMallocHost(&hb, static_cast<size_t>(maxS) * 4));
+            host_bufs.push_back(hb);
+        }
+        p.host = host_bufs.back();
+        host_bufs.pop_back();
+        if (free_ev.empty()) {
+            cudaEvent_t e;
+            HK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            free_ev.push_back(e);
+        }
+        p.ev = free_ev.back();
+        free_ev.pop_back();
+        p.worker = w;
+        p.slots = sslots;
+        HK_CUDA(cudaMemcpyAsync(p.host, sample_ids, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, st));
+        HK_CUDA(cudaEventRecord(p.ev, st));
+        pending.push_back(std::move(p));
+        if (pending.size() > 64) harvest(false);
+    }
+    HK_CUDA(cudaEventRecord(mt.done, st));
+}
+
+// -------------------------------------------------------------- device trie
+void hk_engine::trie_sync(int w, std::vector<hk::TrieOp>& ops, const std::function<const uint64_t*(int)>& key_of) {
+    if (ops.empty()) return;
+    Worker& wk = workers[static_cast<size_t>(w)];
+    const int block = wk.trie.block;
+    // compact per node: first op erase => keep the erase; last op create => keep the final create
+    std::unordered_map<int, std::pair<int, int>> first_last;
+    for (int i = 0; i < static_cast<int>(ops.size()); ++i) {
+        auto it = first_last.find(ops[i].node);
+        if (it == first_last.end())
+            first_last[ops[i].node] = {i, i};
+        else
+            it->second.second = i;
+    }
+    std::vector<hkd::TrieOpDev> dev;
+    std::vector<uint64_t> keys;
+    for (int i = 0; i < static_cast<int>(ops.size()); ++i) {
+        const auto& fl = first_last[ops[i].node];
+        const hk::TrieOp& op = ops[i];
+        if (op.erase && i == fl.first) {
+            dev.push_back({op.node, op.parent, op.page, 1, op.phash});
+            keys.insert(keys.end(), block, 0);
+            ++wk.trie_tombs;
+        } else if (!op.erase && i == fl.second) {
+            dev.push_back({op.node, op.parent, op.page, 0, op.phash});
+            const uint64_t* k = key_of(op.node);
+            keys.insert(keys.end(), k, k + block);
+        }
+    }
+    ops.clear();
+    if (dev.empty()) return;
+    // stage ops + keys in one device buffer (reuse tok_d)
+    const size_t op_words = dev.size() * sizeof(hkd::TrieOpDev) / 8;
+    const size_t need = op_words + keys.size();
+    if (need > tok_cap) {
+        HK_CUDA(cudaStreamSynchronize(st));
+        cudaFree(tok_d);
+        tok_cap = need * 2;
+        tok_d = dalloc<uint64_t>(tok_cap);
+    }
+    HK_CUDA(cudaStreamSynchronize(st));
+    HK_CUDA(cudaMemcpyAsync(tok_d, dev.data(), op_words * 8, cudaMemcpyHostToDevice, st));
+    HK_CUDA(cudaMemcpyAsync(tok_d + op_words, keys.data(), keys.size() * 8, cudaMemcpyHostToDevice, st));
+    const int c = clock.begin(6, st);
+    hkd::trie_apply(wk.trie, reinterpret_cast<const hkd::TrieOpDev*>(tok_d), tok_d + op_words,
+                    static_cast<int>(dev.size()), st);
+    clock.end(c, st);
+    HK_CUDA(cudaStreamSynchronize(st));
+}
+
+void hk_engine::trie_lookup(int w, const std::vector<const std::vector<uint64_t>*>& prompts,
+                            std::vector<std::vector<int>>& paths) {
+    Worker& wk = workers[static_cast<size_t>(w)];
+    const int n = static_cast<int>(prompts.size());
+    std::vector<uint64_t> offs(static_cast<size_t>(n) + 1, 0);
+    int stride = 1;
+    for (int i = 0; i < n; ++i) {
+        offs[static_cast<size_t>(i) + 1] = offs[static_cast<size_t>(i)] + prompts[static_cast<size_t>(i)]->size();
+        stride = std::max(stride, static_cast<int>(prompts[static_cast<size_t>(i)]->size()) / wk.trie.block);
+    }
+    const size_t need = offs[static_cast<size_t>(n)] + offs.size();
+    if (need > tok_cap) {
+        HK_CUDA(cudaStreamSynchronize(st));
+        cudaFree(tok_d);
+        tok_cap = need * 2;
+        tok_d = dalloc<uint64_t>(tok_cap);
+    }
+    const size_t mneed = static_cast<size_t>(n) * (1 + 2 * stride);
+    if (mneed > match_cap) {
+        HK_CUDA(cudaStreamSynchronize(st));
+        cudaFree(match_d);
+        match_cap = mneed * 2;
+        match_d = dalloc<int32_t>(match_cap);
+    }
+    std::vector<uint64_t> flat;
+    flat.reserve(offs[static_cast<size_t>(n)]);
+    for (auto* p : prompts) flat.insert(flat.end(), p->begin(), p->end());
+    HK_CUDA(cudaStreamSynchronize(st));
+    HK_CUDA(cudaMemcpyAsync(tok_d, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice, st));
+    HK_CUDA(cudaMemcpyAsync(tok_d + flat.size(), offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, st));
+    int32_t* d_matched = match_d;
+    int32_t* d_path = match_d + n;
+    int32_t* d_pt = d_path + static_cast<size_t>(n) * stride;
+    const int c = clock.begin(6, st);
+    hkd::trie_match(wk.trie, tok_d, tok_d + flat.size(), n, d_matched, d_path, d_pt, stride, st);
+    clock.end(c, st);
+    std::vector<int32_t> hm(static_cast<size_t>(n)), hp(static_cast<size_t>(n) * stride);
+    HK_CUDA(cudaMemcpyAsync(hm.data(), d_matched, hm.size() * 4, cudaMemcpyDeviceToHost, st));
+    HK_CUDA(cudaMemcpyAsync(hp.data(), d_path, hp.size() * 4, cudaMemcpyDeviceToHost, st));
+    HK_CUDA(cudaStreamSynchronize(st));
+    paths.assign(static_cast<size_t>(n), {});
+    for (int i = 0; i < n; ++i)
+        paths[static_cast<size_t>(i)].assign(hp.begin() + static_cast<std::ptrdiff_t>(i) * stride,
+                                             hp.begin() + static_cast<std::ptrdiff_t>(i) * stride + hm[static_cast<size_t>(i)]);
+}
+
+// ------------------------------------------------------------ device body
+namespace hk {
+
+class DeviceBody : public LlmBody {
+  public:
+    DeviceBody(hk_engine* e, const Plan& plan, const SimConfig& cfg) : e_(e) {
+        if (cfg.workers.size() != e->workers.size())
+            throw std::runtime_error("hk_simulate: engine has " + std::to_string(e->workers.size()) +
+                                     " worker pools but the schedule has " + std::to_string(cfg.workers.size()) +
+                                     " workers");
+        for (const auto& w : cfg.workers)
+            if (w.block != e->ec.block_tokens)
+                throw std::runtime_error("hk_simulate: SimWorkerConfig::block differs from the engine page size");
+        e_->sync();
+        e_->reset_workers();
+        (void)plan;
+    }
+    bool uses_pages() const override { return true; }
+    int pages_per_worker(int) const override { return static_cast<int>(e_->ec.pages_per_worker); }
+    bool device_lookup() const override { return e_->ec.use_device_trie != 0; }
+
+    void precompute_pins(int w, const std::vector<TokenSeq>& pins, const std::vector<std::vector<int>>& pin_pages,
+                         const std::vector<std::size_t>& first_new) override {
+        const int block = static_cast<int>(e_->ec.block_tokens);
+        for (std::size_t i = 0; i < pins.size(); ++i) {
+            const int start = static_cast<int>(first_new[i]) * block;
+            const int len = static_cast<int>(pins[i].size());
+            for (int c0 = start; c0 < len; c0 += e_->maxT) {
+                std::vector<hk_engine::SegIn> segs(1);
+                segs[0].slot = 0;
+                segs[0].start = c0;
+                segs[0].count = std::min(e_->maxT, len - c0);
+                segs[0].table = &pin_pages[i];
+                segs[0].prompt = &pins[i];
+                e_->step(w, segs);
+            }
+        }
+        e_->sync();
+    }
+    void sync_trie(int w, KvTree& tree) override {
+        e_->trie_sync(w, tree.journal(), [&tree](int node) { return tree.node_key(node); });
+    }
+    void lookup_batch(int w, const std::vector<const TokenSeq*>& prompts, std::vector<std::vector<int>>& paths) override {
+        e_->trie_lookup(w, prompts, paths);
+    }
+    void on_admit(int w, LiveCall& lc) override { lc.slot = e_->alloc_slot(w); }
+    void run_step(StepPlan& sp) override {
+        std::vector<hk_engine::SegIn> segs;
+        segs.reserve(sp.segs.size());
+        for (auto& s : sp.segs) {
+            hk_engine::SegIn in;
+            in.slot = s.call->slot;
+            in.start = static_cast<int>(s.start);
+            in.count = static_cast<int>(s.count);
+            in.from_prompt = s.from_prompt;
+            in.write_kv = s.write_kv;
+            in.sample = s.sample;
+            in.table = &s.table;
+            in.prompt = &s.call->prompt;
+            segs.push_back(in);
+        }
+        e_->step(sp.worker, segs);
+    }
+    TokenSeq take_output(int w, LiveCall& lc, double, bool) override {
+        auto& toks = e_->workers[static_cast<size_t>(w)].slot_tokens[static_cast<size_t>(lc.slot)];
+        if (toks.size() < lc.out_len) e_->harvest(true);
+        if (toks.size() < lc.out_len) {
+            HK_CUDA(cudaStreamSynchronize(e_->st));
+            e_->harvest(true);
+        }
+        TokenSeq out;
+        out.reserve(lc.out_len);
+        for (std::size_t i = 0; i < lc.out_len && i < toks.size(); ++i)
+            out.push_back(gen_token(static_cast<std::uint32_t>(toks[i]), static_cast<std::uint32_t>(e_->V)));
+        return out;
+    }
+    void on_finish(int w, LiveCall& lc) override {
+        if (lc.slot >= 0) e_->free_slot(w, lc.slot);
+        lc.slot = -1;
+    }
+    void finish_run() override { e_->sync(); }
+
+  private:
+    hk_engine* e_;
+};
+
+std::unique_ptr<LlmBody> make_device_body(hk_engine* e, const Plan& plan, const SimConfig& cfg) {
+    return std::make_unique<DeviceBody>(e, plan, cfg);
+}
+
 }  // namespace hk
 
-extern "C" {
-hk_engine* hk_engine_create(const hk_model_config*, const hk_engine_config*) {
-    hk::set_error("not implemented");
-    return nullptr;
+// ------------------------------------------------------------------ C-ABI
+namespace {
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception& ex) {
+        hk::set_error(ex.what());
+        return -1;
+    }
 }
-void hk_engine_destroy(hk_engine*) {}
-size_t hk_engine_page_bytes(const hk_engine*) { return 0; }
-int hk_engine_reset(hk_engine*) { return -1; }
-int hk_pool_gather(hk_engine*, int, const int32_t*, size_t, void*) { return -1; }
-int hk_pool_scatter(hk_engine*, int, const void*, const int32_t*, size_t) { return -1; }
-int hk_pool_copy(hk_engine*, int, const int32_t*, const int32_t*, size_t) { return -1; }
-int hk_trie_apply(hk_engine*, int, const hk_trie_op*, size_t) { return -1; }
-int hk_trie_match(hk_engine*, int, const uint64_t*, const uint64_t*, size_t, int32_t*, int32_t*, int32_t*, size_t) {
+}  // namespace
+
+extern "C" {
+
+hk_engine* hk_engine_create(const hk_model_config* m, const hk_engine_config* c) {
+    try {
+        if (!m || !c) throw std::runtime_error("hk_engine_create: null config");
+        return new hk_engine(*m, *c);
+    } catch (const std::exception& ex) {
+        hk::set_error(ex.what());
+        return nullptr;
+    }
+}
+
+void hk_engine_destroy(hk_engine* e) { delete e; }
+
+size_t hk_engine_page_bytes(const hk_engine* e) { return e ? e->page_bytes_layer * e->L : 0; }
+
+int hk_engine_reset(hk_engine* e) {
+    return guarded([&] {
+        e->sync();
+        e->reset_workers();
+        e->clock.reset();
+    });
+}
+
+int hk_pool_gather(hk_engine* e, int w, const int32_t* pages, size_t n, void* dst) {
+    return guarded([&] {
+        int32_t* dp = dalloc<int32_t>(n);
+        HK_CUDA(cudaMemcpyAsync(dp, pages, n * 4, cudaMemcpyHostToDevice, e->st));
+        const int c = e->clock.begin(7, e->st);
+        hkd::pool_gather(e->workers.at(static_cast<size_t>(w)).kv, e->workers[static_cast<size_t>(w)].layer_stride,
+                         e->L, e->page_bytes_layer, dp, static_cast<int>(n), dst, e->st);
+        e->clock.end(c, e->st, 2.0 * n * e->page_bytes_layer * e->L);
+        HK_CUDA(cudaStreamSynchronize(e->st));
+        cudaFree(dp);
+    });
+}
+
+int hk_pool_scatter(hk_engine* e, int w, const void* src, const int32_t* pages, size_t n) {
+    return guarded([&] {
+        int32_t* dp = dalloc<int32_t>(n);
+        HK_CUDA(cudaMemcpyAsync(dp, pages, n * 4, cudaMemcpyHostToDevice, e->st));
+        const int c = e->clock.begin(7, e->st);
+        hkd::pool_scatter(e->workers.at(static_cast<size_t>(w)).kv, e->workers[static_cast<size_t>(w)].layer_stride,
+                          e->L, e->page_bytes_layer, dp, static_cast<int>(n), src, e->st);
+        e->clock.end(c, e->st, 2.0 * n * e->page_bytes_layer * e->L);
+        HK_CUDA(cudaStreamSynchronize(e->st));
+        cudaFree(dp);
+    });
+}
+
+int hk_pool_copy(hk_engine* e, int w, const int32_t* src, const int32_t* dst, size_t n) {
+    return guarded([&] {
+        int32_t* dp = dalloc<int32_t>(2 * n);
+        HK_CUDA(cudaMemcpyAsync(dp, src, n * 4, cudaMemcpyHostToDevice, e->st));
+        HK_CUDA(cudaMemcpyAsync(dp + n, dst, n * 4, cudaMemcpyHostToDevice, e->st));
+        const int c = e->clock.begin(7, e->st);
+        hkd::pool_copy(e->workers.at(static_cast<size_t>(w)).kv, e->workers[static_cast<size_t>(w)].layer_stride, e->L,
+                       e->page_bytes_layer, dp, dp + n, static_cast<int>(n), e->st);
+        e->clock.end(c, e->st, 2.0 * n * e->page_bytes_layer * e->L);
+        HK_CUDA(cudaStreamSynchronize(e->st));
+        cudaFree(dp);
+    });
+}
+
+int hk_trie_apply(hk_engine* e, int w, const hk_trie_op* ops, size_t n) {
+    return guarded([&] {
+        std::vector<hk::TrieOp> v;
+        std::unordered_map<int, const uint64_t*> keys;
+        for (size_t i = 0; i < n; ++i) {
+            v.push_back(hk::TrieOp{ops[i].node, ops[i].parent, ops[i].page, ops[i].erase != 0, ops[i].phash});
+            if (!ops[i].erase) keys[ops[i].node] = ops[i].key;
+        }
+        e->trie_sync(w, v, [&](int node) { return keys.at(node); });
+    });
+}
+
+int hk_trie_match(hk_engine* e, int w, const uint64_t* tokens, const uint64_t* offsets, size_t n, int32_t* matched,
+                  int32_t* node_path, int32_t* page_table, size_t stride) {
+    return guarded([&] {
+        std::vector<std::vector<uint64_t>> ps(n);
+        std::vector<const std::vector<uint64_t>*> pp;
+        for (size_t i = 0; i < n; ++i) {
+            ps[i].assign(tokens + offsets[i], tokens + offsets[i + 1]);
+            pp.push_back(&ps[i]);
+        }
+        std::vector<std::vector<int>> paths;
+        e->trie_lookup(w, pp, paths);
+        for (size_t i = 0; i < n; ++i) {
+            matched[i] = static_cast<int32_t>(paths[i].size());
+            for (size_t k = 0; k < paths[i].size() && k < stride; ++k) {
+                node_path[i * stride + k] = paths[i][k];
+                if (page_table) {
+                    int32_t pg = 0;
+                    HK_CUDA(cudaMemcpy(&pg, e->workers[static_cast<size_t>(w)].trie.page + paths[i][k], 4,
+                                       cudaMemcpyDeviceToHost));
+                    page_table[i * stride + k] = pg;
+                }
+            }
+        }
+    });
+}
+
+int hk_generate(hk_engine* e, const uint32_t* ids, size_t n, size_t n_new, uint32_t* out, float* logits) {
+    return guarded([&] {
+        if (n == 0) throw std::runtime_error("hk_generate: empty prompt");
+        const int block = static_cast<int>(e->ec.block_tokens);
+        const size_t total = n + n_new;
+        if (static_cast<size_t>((total + block - 1) / block) > e->ec.pages_per_worker)
+            throw std::runtime_error("hk_generate: sequence does not fit the page pool");
+        std::vector<int> table;
+        for (int p = 0; p < static_cast<int>((total + block - 1) / block); ++p) table.push_back(p);
+        std::vector<uint32_t> seq(ids, ids + n);
+        const int slot = e->alloc_slot(0);
+        e->harvest(true);
+        e->workers[0].slot_tokens[static_cast<size_t>(slot)].clear();
+        const size_t V = static_cast<size_t>(e->V);
+        // prefill in chunks; sample from the last prompt position
+        for (size_t c0 = 0; c0 < n; c0 += static_cast<size_t>(e->maxT)) {
+            std::vector<hk_engine::SegIn> segs(1);
+            segs[0].slot = slot;
+            segs[0].start = static_cast<int>(c0);
+            segs[0].count = static_cast<int>(std::min(n - c0, static_cast<size_t>(e->maxT)));
+            segs[0].table = &table;
+            segs[0].ids = &seq;
+            segs[0].sample = c0 + segs[0].count == n && n_new > 0;
+            e->step(0, segs, segs[0].sample && logits ? logits : nullptr);
+        }
+        for (size_t k = 1; k < n_new; ++k) {
+            std::vector<hk_engine::SegIn> segs(1);
+            segs[0].slot = slot;
+            segs[0].start = static_cast<int>(n + k - 1);
+            segs[0].count = 1;
+            segs[0].from_prompt = false;
+            segs[0].sample = true;
+            segs[0].table = &table;
+            e->step(0, segs, logits ? logits + k * V : nullptr);
+        }
+        e->sync();
+        auto& toks = e->workers[0].slot_tokens[static_cast<size_t>(slot)];
+        for (size_t k = 0; k < n_new; ++k) out[k] = static_cast<uint32_t>(toks.at(k));
+        e->free_slot(0, slot);
+    });
+}
+
+double hk_engine_kernel_ms(const hk_engine* ce, const char* family, uint64_t* launches, double* bytes) {
+    hk_engine* e = const_cast<hk_engine*>(ce);
+    try {
+        e->clock.collect();
+    } catch (...) {
+        return -1;
+    }
+    for (int i = 0; i < KernelClock::kFamilies; ++i)
+        if (std::strcmp(e->clock.names[i], family) == 0) {
+            if (launches) *launches = e->clock.launches[i];
+            if (bytes) *bytes = e->clock.bytes[i];
+            return e->clock.ms[i];
+        }
     return -1;
 }
-int hk_generate(hk_engine*, const uint32_t*, size_t, size_t, uint32_t*, float*) { return -1; }
-double hk_engine_kernel_ms(const hk_engine*, const char*, uint64_t*, double*) { return -1; }
-int hk_engine_profile(hk_engine*, int) { return -1; }
+
+int hk_engine_profile(hk_engine* e, int enable) {
+    return guarded([&] {
+        e->clock.reset();
+        e->clock.enabled = enable != 0;
+    });
 }
+
+}  // extern "C"

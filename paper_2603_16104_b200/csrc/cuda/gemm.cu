@@ -1,0 +1,318 @@
+// K4: dense contractions on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+//   out[t][n] = sum_k X[t][k] * W[n][k]      (X: activations [T][K], W: weights [N][K])
+//
+// The MMA's M side is the weight matrix (128 output features per CTA tile)
+// and its N side is the token batch, so a decode step with 64 live calls is a
+// 128 x 64 UMMA tile that streams weights once (weight-bandwidth bound, the
+// regime of the executor's decode iterations) while a prefill chunk uses
+// N = 256 token tiles (tensor bound). Operands are staged by TMA into 128B-
+// swizzled shared memory through a multi-stage mbarrier ring; one elected
+// thread issues tcgen05.mma into a TMEM accumulator; all four warps drain TMEM
+// with tcgen05.ld in the epilogue. Split-K (grid.z) covers skinny decode
+// GEMMs; partials are reduced deterministically by splitk_reduce.
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace hkd {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+
+struct GemmParams {
+    int N, K, T;
+    int kb_total, kb_per_split;
+    int epi;
+    void* out;
+    int ldo;
+    const bf16* bias;
+    float* partial;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(128, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int A_BYTES = BM * BK * 2;
+    constexpr int B_BYTES = BN * BK * 2;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* done = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * BM;
+    const int n0 = blockIdx.y * BN;
+    const int kb0 = blockIdx.z * p.kb_per_split;
+    const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
+    const int nkb = kb1 - kb0;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmW);
+        tma_prefetch_desc(&tmX);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_w = policy_evict_first();
+            const uint64_t pol_x = policy_evict_last();
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % STAGES;
+                mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+                mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+                tma_load_2d_hint(sA + s * A_BYTES, &tmW, &full[s], (kb0 + i) * BK, m0, pol_w);
+                tma_load_2d_hint(sB + s * B_BYTES, &tmX, &full[s], (kb0 + i) * BK, n0, pol_x);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+        for (int i = 0; i < nkb; ++i) {
+            const int s = i % STAGES;
+            mbar_wait(&full[s], (i / STAGES) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t a_base = smem_u32(sA + s * A_BYTES);
+                const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k) {
+                    umma_bf16(tmem, umma_desc_sw128(a_base + k * 32), umma_desc_sw128(b_base + k * 32), idesc,
+                              (i | k) != 0 ? 1u : 0u);
+                }
+                umma_commit(&empty[s]);
+                if (i == nkb - 1) umma_commit(done);
+            }
+            __syncwarp();
+        }
+    }
+
+    // ---- epilogue: TMEM -> registers -> global (all 4 warps) ----
+    mbar_wait(done, 0);
+    __syncwarp();
+    tc_fence_after();
+    const int m = m0 + warp * 32 + lane;
+    const bool m_ok = m < p.N;
+    const float bias = (p.bias && m_ok && p.epi != 3) ? bf2f(p.bias[m]) : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 8) {
+        float v[8];
+        tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+        if (!m_ok) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int n = n0 + c + j;
+            if (n >= p.T) break;
+            const float r = v[j] + bias;
+            switch (p.epi) {
+                case kEpiStoreBf16:
+                    static_cast<bf16*>(p.out)[static_cast<size_t>(n) * p.ldo + m] = f2bf(r);
+                    break;
+                case kEpiAddF32:
+                    static_cast<float*>(p.out)[static_cast<size_t>(n) * p.ldo + m] += r;
+                    break;
+                case kEpiStoreF32:
+                    static_cast<float*>(p.out)[static_cast<size_t>(n) * p.ldo + m] = r;
+                    break;
+                default:  // split-K partial
+                    p.partial[(static_cast<size_t>(blockIdx.z) * p.T + n) * p.N + m] = r;
+                    break;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// Deterministic split-K reduction (fixed summation order) fused with the epilogue.
+__global__ void splitk_reduce_kernel(const float* __restrict__ partial, int splits, int T, int N, int epi, void* out,
+                                     int ldo, const bf16* __restrict__ bias) {
+    const size_t total = static_cast<size_t>(T) * N;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int n = static_cast<int>(i / N);
+        const int m = static_cast<int>(i % N);
+        float r = 0.f;
+        for (int s = 0; s < splits; ++s) r += partial[static_cast<size_t>(s) * total + i];
+        if (bias) r += bf2f(bias[m]);
+        switch (epi) {
+            case kEpiStoreBf16:
+                static_cast<bf16*>(out)[static_cast<size_t>(n) * ldo + m] = f2bf(r);
+                break;
+            case kEpiAddF32:
+                static_cast<float*>(out)[static_cast<size_t>(n) * ldo + m] += r;
+                break;
+            default:
+                static_cast<float*>(out)[static_cast<size_t>(n) * ldo + m] = r;
+                break;
+        }
+    }
+}
+
+// fp32 parity-mode GEMM (SIMT, tiled); same contract as the tensor-core path.
+__global__ void gemm_f32_kernel(const float* __restrict__ W, const float* __restrict__ X, int N, int K, int T,
+                                int epi, void* out, int ldo, const float* __restrict__ bias) {
+    __shared__ float sW[32][33];
+    __shared__ float sX[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const int m0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
+    float acc[4] = {0, 0, 0, 0};
+    for (int k0 = 0; k0 < K; k0 += 32) {
+        for (int r = ty; r < 32; r += 8) {
+            sW[r][tx] = (m0 + r < N && k0 + tx < K) ? W[static_cast<size_t>(m0 + r) * K + k0 + tx] : 0.f;
+            sX[r][tx] = (n0 + r < T && k0 + tx < K) ? X[static_cast<size_t>(n0 + r) * K + k0 + tx] : 0.f;
+        }
+        __syncthreads();
+        for (int k = 0; k < 32; ++k) {
+            const float w = sW[tx][k];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] += w * sX[ty + 8 * j][k];
+        }
+        __syncthreads();
+    }
+    const int m = m0 + tx;
+    if (m >= N) return;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int n = n0 + ty + 8 * j;
+        if (n >= T) continue;
+        float r = acc[j] + (bias ? bias[m] : 0.f);
+        float* o = static_cast<float*>(out) + static_cast<size_t>(n) * ldo + m;
+        if (epi == kEpiAddF32)
+            *o += r;
+        else
+            *o = r;
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        HK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+CUtensorMap make_map_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {BK, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+template <int BN, int STAGES>
+constexpr size_t smem_bytes() {
+    return 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 1) * 8 + 16;
+}
+
+template <int BN, int STAGES>
+void launch_tc(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p, dim3 grid, cudaStream_t st) {
+    static bool configured = false;
+    constexpr size_t sm = smem_bytes<BN, STAGES>();
+    if (!configured) {
+        HK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sm)));
+        configured = true;
+    }
+    gemm_tc_kernel<BN, STAGES><<<grid, 128, sm, st>>>(tw, tx, p);
+    HK_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+int g_num_sms = 148;
+
+void gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, const bf16* bias,
+               float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits) {
+    if (T <= 0) return;
+    if (K % BK != 0) throw std::runtime_error("gemm_bf16: K must be a multiple of 64");
+    int BN;
+    if (T <= 16)
+        BN = 16;
+    else if (T <= 32)
+        BN = 32;
+    else if (T <= 64)
+        BN = 64;
+    else if (T <= 128)
+        BN = 128;
+    else
+        BN = 256;
+    const int mt = (N + BM - 1) / BM;
+    const int nt = (T + BN - 1) / BN;
+    const int kb = K / BK;
+    int splits = 1;
+    if (force_splits > 0) {
+        splits = force_splits;
+    } else if (mt * nt < g_num_sms * 3 / 4) {
+        splits = std::max(1, g_num_sms / (mt * nt));
+        splits = std::min(splits, std::max(1, kb / 4));
+    }
+    int kbps = (kb + splits - 1) / splits;
+    splits = (kb + kbps - 1) / kbps;  // no empty splits
+    if (splits > 1 && static_cast<size_t>(splits) * T * N > workspace_floats) {
+        splits = 1;
+        kbps = kb;
+    }
+    GemmParams p{N, K, T, kb, kbps, splits > 1 ? kEpiPartial : epi, out, ldo, bias, workspace};
+    const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
+    const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
+    dim3 grid(mt, nt, splits);
+    switch (BN) {
+        case 16: launch_tc<16, 8>(tw, tx, p, grid, st); break;
+        case 32: launch_tc<32, 8>(tw, tx, p, grid, st); break;
+        case 64: launch_tc<64, 8>(tw, tx, p, grid, st); break;
+        case 128: launch_tc<128, 6>(tw, tx, p, grid, st); break;
+        default: launch_tc<256, 4>(tw, tx, p, grid, st); break;
+    }
+    if (splits > 1) {
+        const size_t total = static_cast<size_t>(T) * N;
+        const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 4096));
+        splitk_reduce_kernel<<<blocks, 256, 0, st>>>(workspace, splits, T, N, epi, out, ldo, bias);
+        HK_CUDA(cudaGetLastError());
+    }
+}
+
+void gemm_f32(const float* W, const float* X, int N, int K, int T, int epi, void* out, int ldo, const float* bias,
+              cudaStream_t st) {
+    if (T <= 0) return;
+    dim3 grid((N + 31) / 32, (T + 31) / 32);
+    gemm_f32_kernel<<<grid, 256, 0, st>>>(W, X, N, K, T, epi, out, ldo, bias);
+    HK_CUDA(cudaGetLastError());
+}
+
+}  // namespace hkd

@@ -1,0 +1,110 @@
+// Host-callable launchers of the device kernels (one translation unit each).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace hkd {
+
+enum : int { kEpiStoreBf16 = 0, kEpiAddF32 = 1, kEpiStoreF32 = 2, kEpiPartial = 3 };
+extern int g_num_sms;
+
+// ----------------------------------------------------------------- gemm.cu
+// out[t][n] (+)= sum_k X[t][k] W[n][k] (+ bias[n]); tcgen05 path for bf16.
+void gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, const bf16* bias,
+               float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits = 0);
+void gemm_f32(const float* W, const float* X, int N, int K, int T, int epi, void* out, int ldo, const float* bias,
+              cudaStream_t st);
+
+// ------------------------------------------------------------------ ops.cu
+// Counter-based weight init shared bit-for-bit with oracle/transformer.py.
+void init_uniform(void* w, bool f32, size_t n, uint64_t seed, uint64_t tensor_id, float scale, cudaStream_t st);
+void fill_const(void* w, bool f32, size_t n, float v, cudaStream_t st);
+// x[t] = embed[id_t] (ids < 0 read the slot's last sampled token)
+void embed(const void* table, bool f32, int d, const int32_t* ids, const int32_t* slots, const int32_t* slot_last,
+           int T, float* x, cudaStream_t st);
+// out[r] = rmsnorm(x[rows ? rows[r] : r]) * w
+void rmsnorm(const float* x, const void* w, bool f32, int d, float eps, const int32_t* rows, int R, void* out,
+             cudaStream_t st);
+// RoPE on q and k of qkv rows; K/V written into their KV pages (tok_kvw != 0).
+struct RopeArgs {
+    void* qkv;              // [T][(H + 2 Hkv) hd], bf16 or f32
+    bool f32;
+    int T, H, Hkv, hd;
+    const int32_t* pos;     // [T]
+    const int32_t* kvw;     // [T] write K/V?
+    const int32_t* ptab;    // [T] offset of the token's block table in `pages`
+    const int32_t* pages;   // page-table arena
+    const float2* rope;     // [max_pos][hd/2] (cos, sin)
+    void* kv_layer;         // this layer's pool: [P][2][Hkv][block][hd]
+    int block;
+};
+void rope_kv_write(const RopeArgs& a, cudaStream_t st);
+void swiglu(const void* gu, bool f32, int T, int F, void* out, cudaStream_t st);
+// ids[r] = argmax_v logits[r][v] (lowest index on ties); also slot_last[slots[r]] = ids[r]
+void argmax_rows(const float* logits, int R, int V, int32_t* ids, const int32_t* slots, int32_t* slot_last,
+                 cudaStream_t st);
+
+// ------------------------------------------------------------ attention.cu
+struct AttnItem {
+    int tok0;    // first batch token (rows tok0 .. tok0 + ntok - 1)
+    int ntok;    // <= 16
+    int kvh;     // kv head
+    int ptab;    // offset of the rows' block table in the page arena
+    int kbeg;    // key range [kbeg, kend), kbeg page aligned
+    int kend;
+    int causal;  // mask key j > pos(row)
+    int part;    // partial index for these rows, -1 = write the final output directly
+};
+struct AttnArgs {
+    const void* qkv;       // [T][(H + 2 Hkv) hd]
+    bool f32;
+    int H, Hkv, hd, block;
+    const int32_t* pos;    // [T]
+    const int32_t* pages;  // page arena
+    const void* kv_layer;  // [P][2][Hkv][block][hd]
+    const AttnItem* items;
+    int n_items;
+    void* out;             // [T][H][hd] (bf16 or f32)
+    float* part_o;         // [rows][H][max_parts][hd], row = token - part_tok0
+    float2* part_ml;       // [rows][H][max_parts] (m, l) in log2 units
+    int max_parts;
+    int part_tok0;         // first batch token that has partials (decode tokens are last)
+    float scale;
+};
+void attention_partial(const AttnArgs& a, cudaStream_t st);
+// out[tok0 + r][h] = merge of the n_parts[r] partials of row r, r < n_rows
+void attention_merge(const float* part_o, const float2* part_ml, const int32_t* n_parts, int n_rows, int tok0, int H,
+                     int hd, int max_parts, void* out, bool f32, cudaStream_t st);
+
+// ------------------------------------------------------------------ pool.cu
+// K1: page-granular moves of whole KV pages (all layers) inside one pool.
+void pool_gather(const void* kv, size_t layer_stride, int L, size_t page_bytes_layer, const int32_t* pages, int n,
+                 void* dst, cudaStream_t st);
+void pool_scatter(void* kv, size_t layer_stride, int L, size_t page_bytes_layer, const int32_t* pages, int n,
+                  const void* src, cudaStream_t st);
+void pool_copy(void* kv, size_t layer_stride, int L, size_t page_bytes_layer, const int32_t* src, const int32_t* dst,
+               int n, cudaStream_t st);
+
+// ------------------------------------------------------------------ trie.cu
+// K2: device mirror of a worker's KvTree, keyed by prefix hash.
+struct DevTrie {
+    int max_nodes = 0, block = 16, table_size = 0;
+    int32_t* parent = nullptr;   // [max_nodes]
+    int32_t* page = nullptr;     // [max_nodes]
+    uint64_t* phash = nullptr;   // [max_nodes]
+    uint64_t* keys = nullptr;    // [max_nodes][block]
+    uint64_t* tab_key = nullptr; // [table_size] prefix hash (0 = empty, 1 = tombstone)
+    int32_t* tab_node = nullptr; // [table_size]
+};
+struct TrieOpDev {
+    int32_t node, parent, page, erase;
+    uint64_t phash;
+};
+void trie_apply(DevTrie& t, const TrieOpDev* ops, const uint64_t* keys, int n_ops, cudaStream_t st);
+void trie_match(const DevTrie& t, const uint64_t* tokens, const uint64_t* offsets, int n_prompts, int32_t* matched,
+                int32_t* node_path, int32_t* page_table, int stride, cudaStream_t st);
+
+}  // namespace hkd

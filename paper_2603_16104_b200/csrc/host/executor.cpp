@@ -160,7 +160,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                 std::vector<std::vector<int>> paths;
                 if (body.device_lookup()) {
                     if (backlog[w] >= budgets[w]) break;
-                    body.sync_trie(static_cast<int>(w), cache.journal());
+                    body.sync_trie(static_cast<int>(w), cache);
                     std::vector<const TokenSeq*> pp;
                     for (auto& p : prompts) pp.push_back(&p);
                     body.lookup_batch(static_cast<int>(w), pp, paths);

@@ -342,7 +342,7 @@ class LlmBody {
     virtual bool device_lookup() const { return false; }
     virtual void lookup_batch(int /*w*/, const std::vector<const TokenSeq*>& /*prompts*/,
                               std::vector<std::vector<int>>& /*paths*/) {}
-    virtual void sync_trie(int /*w*/, std::vector<TrieOp>& /*ops*/) {}
+    virtual void sync_trie(int /*w*/, KvTree& /*tree*/) {}
     // Start of iteration `iter`: `completing` lists every (worker, call) that
     // will complete with a non-empty output this iteration (multi-process
     // bodies exchange those outputs here, before any worker runs).

@@ -1,0 +1,149 @@
+"""GPU parity of the device kernels (run on a B200 via gpurun).
+
+K4 (tcgen05 GEMM) is checked against a torch fp32 matmul of the same bf16
+operands; K1 page moves against torch copies; the transformer path against the
+numpy decoder oracle (oracle/transformer.py).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from paper_2603_16104_b200 import _lib  # noqa: E402
+from paper_2603_16104_b200.engine import TINY, LLAMA3_8B, Engine, EngineConfig, reduced  # noqa: E402
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+GEMM_SHAPES = [
+    (128, 64, 1), (256, 128, 16), (512, 256, 33), (384, 192, 64), (256, 512, 100), (1024, 512, 300),
+    (6144, 4096, 64), (4096, 4096, 64), (4096, 14336, 64), (28672, 4096, 64), (6144, 4096, 1024),
+]
+
+
+@pytest.mark.parametrize("N,K,T", GEMM_SHAPES)
+def test_gemm_tcgen05_matches_torch(N, K, T):
+    lib = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(N * 7 + K * 3 + T)
+    W = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) * (3.0 / K) ** 0.5
+    X = (torch.rand(T, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    ref = X.float() @ W.float().t()
+    out = torch.zeros(T, N, device="cuda", dtype=torch.float32)
+    assert lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(out), N, K, T, 2, None, 0, None) == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    err = (out - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-4, err
+    outb = torch.zeros(T, N, device="cuda", dtype=torch.bfloat16)
+    assert lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(outb), N, K, T, 0, None, 0, None) == 0
+    torch.cuda.synchronize()
+    errb = (outb.float() - ref).abs().max().item() / ref.abs().max().item()
+    assert errb < 1e-2, errb
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3, 7])
+def test_gemm_splitk_bias_and_residual(splits):
+    lib = _lib.load()
+    N, K, T = 512, 1024, 48
+    g = torch.Generator(device="cuda").manual_seed(splits)
+    W = (torch.rand(N, K, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    X = (torch.rand(T, K, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    b = (torch.rand(N, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    ref = X.float() @ W.float().t() + b.float()
+    out = torch.zeros(T, N, device="cuda", dtype=torch.float32)
+    assert lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(out), N, K, T, 2, _ptr(b), splits, None) == 0
+    resid = torch.ones(T, N, device="cuda", dtype=torch.float32)
+    assert lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(resid), N, K, T, 1, _ptr(b), splits, None) == 0
+    torch.cuda.synchronize()
+    scale = ref.abs().max().item()
+    assert (out - ref).abs().max().item() / scale < 1e-4
+    assert (resid - (ref + 1)).abs().max().item() / scale < 1e-4
+
+
+def test_gemm_deterministic():
+    lib = _lib.load()
+    N, K, T = 4096, 4096, 64
+    W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    X = torch.randn(T, K, device="cuda").to(torch.bfloat16)
+    outs = []
+    for _ in range(3):
+        o = torch.zeros(T, N, device="cuda")
+        assert lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(o), N, K, T, 2, None, 0, None) == 0
+        outs.append(o)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+# ------------------------------------------------------------------ K1 pool
+def test_pool_gather_scatter_copy():
+    eng = Engine(TINY, EngineConfig(pages_per_worker=64, max_calls=8, max_step_tokens=256, max_ctx_tokens=1024))
+    pb = eng.page_bytes()
+    assert pb == TINY.n_layers * 2 * TINY.n_kv_heads * 16 * TINY.head_dim * 2
+    # fill pages 0..9 with a known pattern through scatter, read back through gather
+    src = torch.arange(10 * pb // 2, device="cuda", dtype=torch.int16).view(torch.uint8)
+    eng.pool_scatter(0, src.data_ptr(), list(range(10)))
+    dst = torch.zeros_like(src)
+    eng.pool_gather(0, list(range(10)), dst.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(src, dst)
+    eng.pool_copy(0, [0, 1, 2], [20, 21, 22])
+    dst2 = torch.zeros(3 * pb, device="cuda", dtype=torch.uint8)
+    eng.pool_gather(0, [20, 21, 22], dst2.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(dst2, src[: 3 * pb])
+    # a permuted gather returns pages in list order
+    dst3 = torch.zeros(2 * pb, device="cuda", dtype=torch.uint8)
+    eng.pool_gather(0, [5, 2], dst3.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(dst3[:pb], src[5 * pb:6 * pb]) and torch.equal(dst3[pb:], src[2 * pb:3 * pb])
+    eng.close()
+
+
+# -------------------------------------------------------------- transformer
+def _check_generation(model, prompt, n_new, rel_tol, eng_cfg=None):
+    from oracle.transformer import Decoder, top2_margin
+    eng = Engine(model, eng_cfg or EngineConfig(pages_per_worker=256, max_calls=8, max_step_tokens=1024,
+                                                max_ctx_tokens=4096))
+    toks, logits = eng.generate(prompt, n_new, want_logits=True)
+    eng.close()
+    dec = Decoder(model, max_pos=4096)
+    ref_toks, ref_logits = dec.generate(prompt, n_new, forced=list(toks))
+    exact = 0
+    for k in range(n_new):
+        rl, gl = ref_logits[k], logits[k]
+        err = np.abs(gl - rl).max() / np.abs(rl).max()
+        assert err < rel_tol, (k, err)
+        if ref_toks[k] == toks[k]:
+            exact += 1
+        else:
+            # only a near-tie of the oracle's top two may flip
+            assert top2_margin(rl) < 4 * rel_tol * np.abs(rl).max(), (k, toks[k], ref_toks[k])
+    return exact
+
+
+def test_generate_tiny_bf16_matches_oracle():
+    rng = np.random.default_rng(0)
+    prompt = rng.integers(0, TINY.vocab, size=77).tolist()
+    exact = _check_generation(TINY, prompt, 12, 1e-2)
+    assert exact >= 11
+
+
+def test_generate_tiny_fp32_matches_oracle():
+    from dataclasses import replace
+    rng = np.random.default_rng(1)
+    prompt = rng.integers(0, TINY.vocab, size=50).tolist()
+    exact = _check_generation(replace(TINY, fp32=True), prompt, 8, 1e-5)
+    assert exact == 8
+
+
+def test_generate_llama_shape_reduced_depth_matches_oracle():
+    m = reduced(LLAMA3_8B, 2, vocab=32768)
+    rng = np.random.default_rng(2)
+    prompt = rng.integers(0, m.vocab, size=150).tolist()
+    exact = _check_generation(m, prompt, 6, 1e-2)
+    assert exact >= 5

@@ -363,8 +363,8 @@ def test_simulate_validation_errors():
 
 # ------------------------------------------------------------ C-ABI surface
 def test_cabi_exports_every_declared_symbol():
-    header = (ROOT / "include" / "helium_b200.h").read_text()
-    declared = set(re.findall(r"\b(hk_[a-z0-9_]+)\s*\(", header))
+    header = "".join(h.read_text() for h in sorted((ROOT / "include").glob("*.h")))
+    declared = set(re.findall(r"\b(hkx?_[a-z0-9_]+)\s*\(", header))
     lib = _lib.load()
     missing = [s for s in sorted(declared) if not hasattr(lib, s)]
     assert not missing, missing
