@@ -1,0 +1,267 @@
+"""Benchmark of the B200 LLM-as-operator executor (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+A "step" is one complete run of the workflow through the executor
+(hk_simulate): pin precompute + every iteration of the reference's simulate()
+loop, with the Llama-3-8B-shaped random-init model as the LLM body. At N=1 the
+workload is configs[1] (64 branches x 2K shared prefix, 256 greedy tokens);
+at N>1 it is the weak-scaled form c2xN (N operators of configs[1], one per
+worker/GPU, one process per GPU). Metric: workflow tokens/s = generated
+(decode) tokens of all ranks / max-over-ranks device time of the K runs.
+
+  value  : device time from CUDA events on the engine stream, inputs resident
+  e2e    : wall time of the C-ABI call hk_simulate(host plan -> host metrics +
+           outputs), including every host<->device copy the executor makes
+  roofline / attention_roofline : per-kernel-family device time of one extra
+           profiled run (CUDA events around every launch) vs MEASURED_PEAKS.json
+  cpu_baseline : the numpy oracle port on the host cores, bounded sample
+  --impl reference : the reference's own CPU path (oracle/_ref run_workflow,
+           whose LLM operator is a hash — no model math) on the same workflow
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "workflow tokens/sec @ Llama-3-8B shape"
+UNIT = "tokens/s"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return j["hbm_gbs"], j.get("bf16_tflops_sustained", j["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = Path(f"/tmp/bench_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = [r.split(", ") for r in self.path.read_text().strip().split("\n") if r.strip()]
+        sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 7 for i in range(4) if r[3 + i].strip() == "Active"})
+        load = [s for s in sm if s > 600] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args, ws, rank):
+    """Reference arm: the reference's own CPU implementation of the path."""
+    if rank != 0:
+        return
+    from oracle import refpy
+    from paper_2603_16104_b200 import workloads as wl
+    wf, inp, prof, spec = wl.c2_branches() if args.gpus == 1 else wl.c2_per_gpu(args.gpus)
+    if not refpy.LIB.exists():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhelios_ref.so not built"}))
+        return
+    times = []
+    mj = None
+    for i in range(args.warmup + args.steps):
+        t, mj = refpy.time_run_workflow(wf, inp, prof, spec, reps=1)
+        if i >= args.warmup:
+            times.append(t)
+    m = json.loads(mj)
+    total = sum(times)
+    value = m["decode_tokens"] * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 hash tokens",
+        "data": "synthetic", "config": {"workload": "configs[1]" if args.gpus == 1 else f"c2x{args.gpus}",
+                                        "decode_tokens_per_step": m["decode_tokens"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": "whole workflow: unmodified reference run_workflow (bind->plan->simulate), "
+                                   "single-threaded; its LLM operator is a hash (evaluator.cpp:37-58), no model math"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--model", default="llama3_8b")
+    ap.add_argument("--workload", default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    if ws > 1 and args.gpus != ws:
+        args.gpus = ws
+
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+
+    import torch
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    from paper_2603_16104_b200 import helios
+    from paper_2603_16104_b200 import workloads as wl
+    from paper_2603_16104_b200.engine import PRESETS, Engine, EngineConfig, pages_for
+
+    model = PRESETS[args.model]
+    workload = args.workload or ("c2" if args.gpus == 1 else f"c2x{args.gpus}")
+    blob, meta = wl.load_plan(workload)
+    sc = wl.sim_config_from_meta(meta)
+    W = len(sc.workers)
+    only = rank if W > 1 else -1
+    if W > 1 and W != ws:
+        raise SystemExit(f"workload {workload} has {W} workers but {ws} ranks")
+    device = local if ws > 1 else 0
+    max_calls = 160
+    eng = Engine(model, EngineConfig(device=device, n_workers=1, pages_per_worker=pages_for(sc, max_calls, 512),
+                                     max_calls=max_calls, max_step_tokens=8192 + 256, max_ctx_tokens=8192,
+                                     use_device_trie=True))
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(device)
+
+    def one_run():
+        m = helios.simulate(blob, sc, engine=eng, only_worker=only)
+        return m, eng.stats()
+
+    for _ in range(args.warmup):
+        one_run()
+    dev_ms, wall_s, decode, h2d, d2h, launches, pin_ms = 0.0, 0.0, 0, 0, 0, 0, 0.0
+    last_m = None
+    with ClockSampler(device) as clk:
+        for _ in range(args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            m, st = one_run()
+            wall_s += time.perf_counter() - t0
+            barrier()
+            dev_ms += st["pin_ms"] + st["iter_ms"]
+            pin_ms += st["pin_ms"]
+            decode += m.decode_tokens
+            h2d += st["h2d_bytes"]
+            d2h += st["d2h_bytes"]
+            launches += st["launches"]
+            last_m = m
+    clocks = clk.summary()
+
+    # max over ranks of device time; sum of tokens
+    if ws > 1:
+        t = torch.tensor([dev_ms, wall_s, float(decode)], dtype=torch.float64, device=f"cuda:{device}")
+        mx = t.clone()
+        torch.distributed.all_reduce(mx[:2], op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(t[2:], op=torch.distributed.ReduceOp.SUM)
+        dev_ms, wall_s, decode = mx[0].item(), mx[1].item(), int(t[2].item())
+
+    # profiled run (not timed): per kernel-family device time
+    prof = {}
+    if not args.no_profile:
+        eng.profile(True)
+        one_run()
+        for fam in ("gemm", "attn_shared", "attn_prefill", "attn_merge", "small", "trie"):
+            ms, n, b = eng.kernel_ms(fam)
+            prof[fam] = {"ms": ms, "launches": n, "bytes": b}
+        prof_stats = eng.stats()
+        eng.profile(False)
+
+    if rank != 0:
+        eng.close()
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    hbm, tflops, peak_src = peaks()
+    value = decode / (dev_ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, reference workflow)",
+        "config": {"workload": f"{workload}: {meta['description']}", "model": model.name,
+                   "decode_tokens_per_step": decode // args.steps, "iterations": last_m.iterations,
+                   "hit_rate_pct": last_m.hit_rate_pct, "parallelism": f"{args.gpus} worker(s), one per GPU",
+                   "l2": "inputs > L2: 15 GB of weights streamed every decode iteration",
+                   "pin_precompute_ms_per_step": pin_ms / args.steps},
+        "e2e": {"value": decode / wall_s, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+                "d2h_bytes_per_step": d2h // args.steps},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if prof:
+        g = prof["gemm"]
+        gemm_ach = g["bytes"] / (g["ms"] / 1e3) / 1e9 if g["ms"] > 0 else None
+        line["roofline"] = {"bound": "hbm", "kernel": "gemm_tc_kernel (tcgen05 weight streaming, all GEMMs)",
+                            "achieved": gemm_ach, "peak": hbm, "unit": "GB/s",
+                            "frac": gemm_ach / hbm if gemm_ach else None,
+                            "traffic": None, "peak_source": peak_src,
+                            "share_of_step": g["ms"] / (prof_stats["pin_ms"] + prof_stats["iter_ms"])}
+        a = prof["attn_shared"]
+        if a["ms"] > 0:
+            ach = a["bytes"] / (a["ms"] / 1e3) / 1e9
+            line["attention_roofline"] = {"bound": "hbm", "kernel": "attn_mma_kernel (prefix-shared decode)",
+                                          "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                                          "traffic": None, "peak_source": peak_src}
+        line["kernel_ms_per_step"] = {k: v["ms"] for k, v in prof.items()}
+    if not args.no_cpu_baseline:
+        from oracle.cpu_sample import decode_step_sample
+        s = decode_step_sample()
+        line["cpu_baseline"] = {"value": s["tokens_per_s"], "unit": UNIT, "cores": s["cores"], "kind": "port",
+                                "sample": s["sample"]}
+    eng.close()
+    print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

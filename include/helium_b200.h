@@ -102,6 +102,9 @@ size_t hk_run_report(const hk_run* run, int which, char* buf, size_t cap);
  *   n_nodes, {node_id, batch, {len, tokens[len]}[batch]}[n_nodes]
  * Returns the word count; copies min(count, cap) words. */
 size_t hk_run_outputs(const hk_run* run, uint64_t* out, size_t cap);
+/* Generated tokens of every llm call (not only workflow outputs), as u64 words:
+ *   n_calls, {op, query, len, tokens[len]}[n_calls]  in (op, query) order. */
+size_t hk_run_call_outputs(const hk_run* run, uint64_t* out, size_t cap);
 /* executor wall time split (seconds): [0] pin precompute, [1] iterations. */
 int hk_run_timing(const hk_run* run, double out[2]);
 void hk_run_free(hk_run* run);
@@ -199,6 +202,21 @@ int hk_trie_match(hk_engine* e, int worker, const uint64_t* tokens, const uint64
  * engine — prefill then n_new decode steps — used by model parity tests.
  * logits (optional) receives the vocab logits of each sampled position. */
 int hk_generate(hk_engine* e, const uint32_t* ids, size_t n, size_t n_new, uint32_t* out_ids, float* logits);
+
+/* Statistics of the last hk_simulate run on this engine: device time measured
+ * with CUDA events on the engine stream (pin precompute, iteration loop), the
+ * host<->device bytes the executor moved, and kernel launches issued. */
+typedef struct hk_engine_stats {
+    double pin_ms;
+    double iter_ms;
+    uint64_t h2d_bytes;
+    uint64_t d2h_bytes;
+    uint64_t launches;
+    uint64_t steps;
+    uint64_t step_tokens;
+    double attn_bytes; /* algorithmic attention bytes (KV read once per group + Q/O) */
+} hk_engine_stats;
+int hk_engine_stats_get(const hk_engine* e, hk_engine_stats* out);
 
 /* Device time (ms) per kernel family accumulated since the last reset, for
  * roofline reporting: names "gemm", "attn_shared", "attn_private", "attn_prefill",

@@ -359,7 +359,7 @@ class SimCfg:
 
 def simulate(p: Plan, cfg: SimCfg, body: Optional[Callable[[List[int], int, float, bool], List[int]]] = None):
     """Returns (metrics dict, calls rows, trace rows, outputs, prompts{(op,q): prompt}).
-    body(prompt, out_len, len_out, det) -> output tokens; None = synth_llm_output."""
+    body(prompt, out_len, len_out, det, call) -> output tokens; None = synth_llm_output."""
     W = len(p.sigma)
     if W == 0:
         raise RuntimeError("simulate: no workers")
@@ -465,7 +465,7 @@ def simulate(p: Plan, cfg: SimCfg, body: Optional[Callable[[List[int], int, floa
                 if body is None:
                     out = synth_llm_output(lc["prompt"], nd["len_out"], nd["det"], cfg.seed, cfg.stochastic)
                 else:
-                    out = body(lc["prompt"], lc["out_len"], nd["len_out"], nd["det"]) if lc["out_len"] else []
+                    out = body(lc["prompt"], lc["out_len"], nd["len_out"], nd["det"], lc["id"]) if lc["out_len"] else []
                 if len(out) != lc["out_len"]:
                     raise RuntimeError("simulate: output length drifted from plan")
                 ev.memo[(op, q)] = out

@@ -52,7 +52,14 @@ class TrieOpC(C.Structure):
                 ("phash", C.c_uint64), ("key", u64p)]
 
 
+class EngineStatsC(C.Structure):
+    _fields_ = [("pin_ms", C.c_double), ("iter_ms", C.c_double), ("h2d_bytes", C.c_uint64),
+                ("d2h_bytes", C.c_uint64), ("launches", C.c_uint64), ("steps", C.c_uint64),
+                ("step_tokens", C.c_uint64), ("attn_bytes", C.c_double)]
+
+
 _SIGS = {
+    "hk_engine_stats_get": (C.c_int, [C.c_void_p, C.POINTER(EngineStatsC)]),
     "hk_last_error": (C.c_char_p, []),
     "hk_abi_version": (C.c_int, []),
     "hk_simulate": (C.c_void_p, [u8p, C.c_size_t, C.POINTER(SimConfigC), C.c_void_p, C.c_uint32]),
@@ -61,6 +68,7 @@ _SIGS = {
     "hk_run_report": (C.c_size_t, [C.c_void_p, C.c_int, C.c_char_p, C.c_size_t]),
     "hk_run_outputs": (C.c_size_t, [C.c_void_p, u64p, C.c_size_t]),
     "hk_run_timing": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
+    "hk_run_call_outputs": (C.c_size_t, [C.c_void_p, u64p, C.c_size_t]),
     "hk_run_free": (None, [C.c_void_p]),
     "hk_kv_create": (C.c_void_p, [C.c_size_t, C.c_size_t]),
     "hk_kv_lookup": (C.c_size_t, [C.c_void_p, u64p, C.c_size_t, C.c_uint64]),

@@ -8,11 +8,16 @@
 //     that share a block-table prefix, keys = the shared pages only. The shared
 //     KV is streamed once per 16 calls (and from L2 for the other row groups)
 //     instead of once per call;
-//   * decode, private part: one call's own suffix pages;
+//   * decode, private part: one call's own suffix pages (single-token items);
 //   * long ranges are split into key chunks.
-// Every partial keeps flash-style (m, l, unnormalised o) state; attention_merge
-// combines the partials of each (token, head). Inner products run on tensor
-// cores (mma.sync m16n8k16 bf16, fp32 accumulate), K/V tiles are staged with
+// MMA rows are (token, q-head) pairs of one GQA group: row r -> token r / G,
+// head r % G, so the G query heads that share a kv head share every K/V tile
+// and a single decode token fills G of the 16 rows of one warp (not 1).
+// Multi-token items run G warps with 64-key tiles; single-token items run one
+// warp with 32-key tiles (7 CTAs/SM keep enough KV bytes in flight).
+// Every partial keeps flash-style (m, l, unnormalised o) state in log2 units;
+// attention_merge combines the partials of each (token, head). QK^T and PV run
+// on tensor cores (mma.sync m16n8k16 bf16 -> f32), K/V tiles are staged with
 // 16-byte cp.async into XOR-swizzled shared memory and read with ldmatrix.
 #include <cfloat>
 
@@ -24,7 +29,7 @@ namespace hkd {
 namespace {
 
 constexpr int HD = 128;
-constexpr int TK = 64;  // keys per tile (4 pages of 16)
+constexpr int BLK = 16;  // tokens per KV page (engine enforces block_tokens == 16)
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
@@ -36,7 +41,6 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -62,67 +66,72 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // byte offset of 16B chunk `c` of key row `r` in a swizzled [TK][HD] bf16 tile
 __device__ __forceinline__ uint32_t swz(int r, int c) { return r * (HD * 2) + ((c ^ (r & 7)) << 4); }
 
-// Stage keys [k0, k0 + TK) of one kv head (K and V) from their pages.
-__device__ __forceinline__ void load_tile(uint32_t sK, uint32_t sV, const bf16* kv, const int32_t* pages, int ptab,
-                                          int k0, int kend, int kvh, int Hkv, int block) {
+// Stage keys [k0, k0 + TK) of one kv head (K and V) from their pages: each
+// thread issues 16-byte cp.async for whole chunks; rows past kend zero-fill.
+template <int TK>
+__device__ __forceinline__ void load_tile(uint32_t sK, uint32_t sV, const bf16* __restrict__ kv,
+                                          const int32_t* __restrict__ pages, int k0, int kend, size_t head_off,
+                                          size_t page_stride, size_t kv_half) {
     const int nthr = blockDim.x;
-    const size_t head_stride = static_cast<size_t>(block) * HD;  // elements of one head's page slice
-    for (int c = threadIdx.x; c < TK * (HD / 8) * 2; c += nthr) {
-        const int is_v = c >= TK * (HD / 8);
-        const int cc = is_v ? c - TK * (HD / 8) : c;
-        const int r = cc >> 4;          // key row in tile
-        const int ch = cc & 15;         // 16B chunk
+#pragma unroll 4
+    for (int c = threadIdx.x; c < TK * 32; c += nthr) {
+        const int r = c >> 5;          // key row in tile
+        const int isv = (c >> 4) & 1;  // K or V
+        const int ch = c & 15;         // 16B chunk within the 256-byte row
         const int key = k0 + r;
         const bool valid = key < kend;
         const bf16* src = kv;
-        if (valid) {
-            const int page = pages[ptab + key / block];
-            src = kv + ((static_cast<size_t>(page) * 2 + is_v) * Hkv + kvh) * head_stride +
-                  static_cast<size_t>(key % block) * HD + ch * 8;
-        }
-        cp_async16((is_v ? sV : sK) + swz(r, ch), src, valid);
+        if (valid)
+            src = kv + static_cast<size_t>(pages[key >> 4]) * page_stride + isv * kv_half + head_off +
+                  (key & (BLK - 1)) * HD + ch * 8;
+        cp_async16((isv ? sV : sK) + swz(r, ch), src, valid);
     }
 }
 
+template <int TK>
 __global__ void __launch_bounds__(256) attn_mma_kernel(AttnArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const AttnItem it = a.items[blockIdx.x];
     const int G = a.H / a.Hkv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
-    const int h = it.kvh * G + warp;
     const int QKV = (a.H + 2 * a.Hkv) * HD;
     const bf16* qkv = static_cast<const bf16*>(a.qkv);
     const bf16* kv = static_cast<const bf16*>(a.kv_layer);
+    const int32_t* pages = a.pages + it.ptab;
+    const size_t kv_half = static_cast<size_t>(a.Hkv) * BLK * HD;
+    const size_t page_stride = 2 * kv_half;
+    const size_t head_off = static_cast<size_t>(it.kvh) * BLK * HD;
 
-    const uint32_t sbase = smem_u32(smem);
-    const uint32_t sK[2] = {sbase, sbase + 2 * TK * HD * 2};
-    const uint32_t sV[2] = {sbase + TK * HD * 2, sbase + 3 * TK * HD * 2};
+    constexpr uint32_t TILE = TK * HD * 2;
+    const uint32_t sbase = smem_u32(smem);  // [stage][K|V] tiles
 
     const int n_tiles = it.kend > it.kbeg ? (it.kend - it.kbeg + TK - 1) / TK : 0;
     if (n_tiles > 0) {
-        load_tile(sK[0], sV[0], kv, a.pages, it.ptab, it.kbeg, it.kend, it.kvh, a.Hkv, a.block);
+        load_tile<TK>(sbase, sbase + TILE, kv, pages, it.kbeg, it.kend, head_off, page_stride, kv_half);
         cp_async_commit();
     }
 
-    // Q fragments (rows gid, gid+8 of this warp's head)
-    const int r0 = gid, r1 = gid + 8;
-    const bool v0 = r0 < it.ntok, v1 = r1 < it.ntok;
+    // rows of this warp: (token, head) pairs
+    const int ra = warp * 16 + gid, rb = ra + 8;
+    const int ta = ra / G, tb = rb / G;
+    const int ha = it.kvh * G + ra % G, hb = it.kvh * G + rb % G;
+    const bool va = ta < it.ntok, vb = tb < it.ntok;
     uint32_t qf[HD / 16][4];
     {
-        const uint32_t* q0 = reinterpret_cast<const uint32_t*>(qkv + static_cast<size_t>(it.tok0 + r0) * QKV + h * HD);
-        const uint32_t* q1 = reinterpret_cast<const uint32_t*>(qkv + static_cast<size_t>(it.tok0 + r1) * QKV + h * HD);
+        const uint32_t* q0 = reinterpret_cast<const uint32_t*>(qkv + static_cast<size_t>(it.tok0 + ta) * QKV + ha * HD);
+        const uint32_t* q1 = reinterpret_cast<const uint32_t*>(qkv + static_cast<size_t>(it.tok0 + tb) * QKV + hb * HD);
 #pragma unroll
         for (int ks = 0; ks < HD / 16; ++ks) {
-            const int c = ks * 8 + tig;  // u32 index = (16 ks + 2 tig) / 2
-            qf[ks][0] = v0 ? q0[c] : 0u;
-            qf[ks][1] = v1 ? q1[c] : 0u;
-            qf[ks][2] = v0 ? q0[c + 4] : 0u;
-            qf[ks][3] = v1 ? q1[c + 4] : 0u;
+            const int c = ks * 8 + tig;
+            qf[ks][0] = va ? q0[c] : 0u;
+            qf[ks][1] = vb ? q1[c] : 0u;
+            qf[ks][2] = va ? q0[c + 4] : 0u;
+            qf[ks][3] = vb ? q1[c + 4] : 0u;
         }
     }
-    const int pos0 = v0 ? a.pos[it.tok0 + r0] : -1;
-    const int pos1 = v1 ? a.pos[it.tok0 + r1] : -1;
+    const int pos0 = va ? a.pos[it.tok0 + ta] : -1;
+    const int pos1 = vb ? a.pos[it.tok0 + tb] : -1;
     const float sl2 = a.scale * kLog2e;
 
     float o[HD / 8][4];
@@ -131,10 +140,11 @@ __global__ void __launch_bounds__(256) attn_mma_kernel(AttnArgs a) {
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
     for (int ti = 0; ti < n_tiles; ++ti) {
-        const int buf = ti & 1;
+        const uint32_t sK = sbase + (ti & 1) * 2 * TILE;
+        const uint32_t sV = sK + TILE;
         if (ti + 1 < n_tiles) {
-            load_tile(sK[buf ^ 1], sV[buf ^ 1], kv, a.pages, it.ptab, it.kbeg + (ti + 1) * TK, it.kend, it.kvh, a.Hkv,
-                      a.block);
+            const uint32_t nK = sbase + ((ti + 1) & 1) * 2 * TILE;
+            load_tile<TK>(nK, nK + TILE, kv, pages, it.kbeg + (ti + 1) * TK, it.kend, head_off, page_stride, kv_half);
             cp_async_commit();
             cp_async_wait<1>();
         } else {
@@ -143,7 +153,6 @@ __global__ void __launch_bounds__(256) attn_mma_kernel(AttnArgs a) {
         __syncthreads();
         const int kt0 = it.kbeg + ti * TK;
 
-        // S = Q K^T  (16 x 64)
         float s[TK / 8][4];
 #pragma unroll
         for (int j = 0; j < TK / 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
@@ -152,28 +161,31 @@ __global__ void __launch_bounds__(256) attn_mma_kernel(AttnArgs a) {
 #pragma unroll
             for (int jn = 0; jn < TK / 16; ++jn) {
                 const int mi = lane >> 3, rr = lane & 7;
-                const int key = jn * 16 + (mi >> 1) * 8 + rr;
-                const int ch = ks * 2 + (mi & 1);
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4(sK[buf] + swz(key, ch), b0, b1, b2, b3);
+                ldsm_x4(sK + swz(jn * 16 + (mi >> 1) * 8 + rr, ks * 2 + (mi & 1)), b0, b1, b2, b3);
                 mma_bf16(s[2 * jn], qf[ks], b0, b1);
                 mma_bf16(s[2 * jn + 1], qf[ks], b2, b3);
             }
         }
-        // mask + online softmax
+        const bool need_mask = it.causal || kt0 + TK > it.kend;
         float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
         for (int j = 0; j < TK / 8; ++j) {
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int key = kt0 + j * 8 + 2 * tig + e;
-                const bool ok = key < it.kend;
-                const bool ok0 = ok && v0 && (!it.causal || key <= pos0);
-                const bool ok1 = ok && v1 && (!it.causal || key <= pos1);
-                s[j][e] = ok0 ? s[j][e] * sl2 : -INFINITY;
-                s[j][2 + e] = ok1 ? s[j][2 + e] * sl2 : -INFINITY;
-                mx0 = fmaxf(mx0, s[j][e]);
-                mx1 = fmaxf(mx1, s[j][2 + e]);
+                float x0 = s[j][e] * sl2, x1 = s[j][2 + e] * sl2;
+                if (need_mask) {
+                    const int key = kt0 + j * 8 + 2 * tig + e;
+                    const bool ok = key < it.kend;
+                    if (!(ok && (!it.causal || key <= pos0))) x0 = -INFINITY;
+                    if (!(ok && (!it.causal || key <= pos1))) x1 = -INFINITY;
+                }
+                if (!va) x0 = -INFINITY;
+                if (!vb) x1 = -INFINITY;
+                s[j][e] = x0;
+                s[j][2 + e] = x1;
+                mx0 = fmaxf(mx0, x0);
+                mx1 = fmaxf(mx1, x1);
             }
         }
         mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
@@ -205,7 +217,6 @@ __global__ void __launch_bounds__(256) attn_mma_kernel(AttnArgs a) {
             o[j][2] *= al1;
             o[j][3] *= al1;
         }
-        // O += P V
 #pragma unroll
         for (int ks = 0; ks < TK / 16; ++ks) {
             uint32_t pa[4];
@@ -216,10 +227,8 @@ __global__ void __launch_bounds__(256) attn_mma_kernel(AttnArgs a) {
 #pragma unroll
             for (int jd = 0; jd < HD / 16; ++jd) {
                 const int mi = lane >> 3, rr = lane & 7;
-                const int key = ks * 16 + (mi & 1) * 8 + rr;
-                const int ch = jd * 2 + (mi >> 1);
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4_t(sV[buf] + swz(key, ch), b0, b1, b2, b3);
+                ldsm_x4_t(sV + swz(ks * 16 + (mi & 1) * 8 + rr, jd * 2 + (mi >> 1)), b0, b1, b2, b3);
                 mma_bf16(o[2 * jd], pa, b0, b1);
                 mma_bf16(o[2 * jd + 1], pa, b2, b3);
             }
@@ -235,32 +244,26 @@ __global__ void __launch_bounds__(256) attn_mma_kernel(AttnArgs a) {
     if (it.part < 0) {
         const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
         bf16* out = static_cast<bf16*>(a.out);
+        bf16* oa = out + (static_cast<size_t>(it.tok0 + ta) * a.H + ha) * HD;
+        bf16* ob = out + (static_cast<size_t>(it.tok0 + tb) * a.H + hb) * HD;
 #pragma unroll
         for (int j = 0; j < HD / 8; ++j) {
             const int d = j * 8 + 2 * tig;
-            if (v0)
-                *reinterpret_cast<uint32_t*>(out + (static_cast<size_t>(it.tok0 + r0) * a.H + h) * HD + d) =
-                    pack_bf16(o[j][0] * i0, o[j][1] * i0);
-            if (v1)
-                *reinterpret_cast<uint32_t*>(out + (static_cast<size_t>(it.tok0 + r1) * a.H + h) * HD + d) =
-                    pack_bf16(o[j][2] * i1, o[j][3] * i1);
+            if (va) *reinterpret_cast<uint32_t*>(oa + d) = pack_bf16(o[j][0] * i0, o[j][1] * i0);
+            if (vb) *reinterpret_cast<uint32_t*>(ob + d) = pack_bf16(o[j][2] * i1, o[j][3] * i1);
         }
     } else {
+        const size_t pa_ = (static_cast<size_t>(it.tok0 + ta - a.part_tok0) * a.H + ha) * a.max_parts + it.part;
+        const size_t pb_ = (static_cast<size_t>(it.tok0 + tb - a.part_tok0) * a.H + hb) * a.max_parts + it.part;
 #pragma unroll
         for (int j = 0; j < HD / 8; ++j) {
             const int d = j * 8 + 2 * tig;
-            if (v0) {
-                float* po = a.part_o + ((static_cast<size_t>(it.tok0 + r0 - a.part_tok0) * a.H + h) * a.max_parts + it.part) * HD + d;
-                *reinterpret_cast<float2*>(po) = make_float2(o[j][0], o[j][1]);
-            }
-            if (v1) {
-                float* po = a.part_o + ((static_cast<size_t>(it.tok0 + r1 - a.part_tok0) * a.H + h) * a.max_parts + it.part) * HD + d;
-                *reinterpret_cast<float2*>(po) = make_float2(o[j][2], o[j][3]);
-            }
+            if (va) *reinterpret_cast<float2*>(a.part_o + pa_ * HD + d) = make_float2(o[j][0], o[j][1]);
+            if (vb) *reinterpret_cast<float2*>(a.part_o + pb_ * HD + d) = make_float2(o[j][2], o[j][3]);
         }
         if (tig == 0) {
-            if (v0) a.part_ml[(static_cast<size_t>(it.tok0 + r0 - a.part_tok0) * a.H + h) * a.max_parts + it.part] = make_float2(m0, l0);
-            if (v1) a.part_ml[(static_cast<size_t>(it.tok0 + r1 - a.part_tok0) * a.H + h) * a.max_parts + it.part] = make_float2(m1, l1);
+            if (va) a.part_ml[pa_] = make_float2(m0, l0);
+            if (vb) a.part_ml[pb_] = make_float2(m1, l1);
         }
     }
 }
@@ -319,28 +322,52 @@ __global__ void attn_simt_f32_kernel(AttnArgs a) {
     }
 }
 
+// out[t][h] = sum_k 2^(m_k - M) o_k / sum_k 2^(m_k - M) l_k ; one warp per (row, head)
 __global__ void attn_merge_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
-                                  const int32_t* __restrict__ n_parts, int tok0, int H, int max_parts, void* out,
-                                  bool f32) {
-    const int t = tok0 + blockIdx.x;
-    const int h = blockIdx.y;
-    const int np = n_parts[blockIdx.x];
-    const size_t base = (static_cast<size_t>(blockIdx.x) * H + h) * max_parts;
+                                  const int32_t* __restrict__ n_parts, int n_rows, int tok0, int H, int max_parts,
+                                  void* out, bool f32) {
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= n_rows * H) return;
+    const int row = wid / H, h = wid % H;
+    const int np = n_parts[row];
+    const size_t base = (static_cast<size_t>(row) * H + h) * max_parts;
     float M = -INFINITY;
     for (int k = 0; k < np; ++k) M = fmaxf(M, part_ml[base + k].x);
     const float Mb = M == -INFINITY ? 0.f : M;
     float L = 0.f;
-    for (int k = 0; k < np; ++k) L += exp2f(part_ml[base + k].x - Mb) * part_ml[base + k].y;
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    for (int d = threadIdx.x; d < HD; d += blockDim.x) {
-        float acc = 0.f;
-        for (int k = 0; k < np; ++k) acc += exp2f(part_ml[base + k].x - Mb) * part_o[(base + k) * HD + d];
-        const size_t oi = (static_cast<size_t>(t) * H + h) * HD + d;
-        if (f32)
-            static_cast<float*>(out)[oi] = acc * inv;
-        else
-            static_cast<bf16*>(out)[oi] = f2bf(acc * inv);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < np; ++k) {
+        const float2 ml = part_ml[base + k];
+        const float w = exp2f(ml.x - Mb);
+        L += w * ml.y;
+        const float4 v = reinterpret_cast<const float4*>(part_o + (base + k) * HD)[lane];
+        acc.x += w * v.x;
+        acc.y += w * v.y;
+        acc.z += w * v.z;
+        acc.w += w * v.w;
     }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    const size_t oi = (static_cast<size_t>(tok0 + row) * H + h) * HD + lane * 4;
+    if (f32) {
+        *reinterpret_cast<float4*>(static_cast<float*>(out) + oi) =
+            make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    } else {
+        bf16* o = static_cast<bf16*>(out) + oi;
+        *reinterpret_cast<uint2*>(o) =
+            make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+    }
+}
+
+template <int TK>
+void launch_mma(const AttnArgs& a, int warps, cudaStream_t st) {
+    constexpr int smem = 4 * TK * HD * 2;  // 2 stages x (K + V)
+    static bool configured = false;
+    if (!configured) {
+        HK_CUDA(cudaFuncSetAttribute(attn_mma_kernel<TK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        configured = true;
+    }
+    attn_mma_kernel<TK><<<a.n_items, warps * 32, smem, st>>>(a);
 }
 
 }  // namespace
@@ -351,24 +378,24 @@ void attention_partial(const AttnArgs& a, cudaStream_t st) {
     if (a.f32) {
         attn_simt_f32_kernel<<<a.n_items, 128, 0, st>>>(a);
     } else {
-        if (G > 8) throw std::runtime_error("attention: GQA group > 8 unsupported");
-        constexpr int smem = 4 * TK * HD * 2;
-        static bool configured = false;
-        if (!configured) {
-            HK_CUDA(cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            configured = true;
-        }
-        attn_mma_kernel<<<a.n_items, G * 32, smem, st>>>(a);
+        if (a.block != BLK) throw std::runtime_error("attention: KV page size must be 16 tokens");
+        if (G > 16) throw std::runtime_error("attention: GQA group > 16 unsupported");
+        if (a.single)
+            launch_mma<32>(a, (G + 15) / 16, st);
+        else
+            launch_mma<64>(a, G, st);
     }
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 void attention_merge(const float* part_o, const float2* part_ml, const int32_t* n_parts, int n_rows, int tok0, int H,
                      int hd, int max_parts, void* out, bool f32, cudaStream_t st) {
     if (n_rows == 0) return;
     if (hd != HD) throw std::runtime_error("attention: head_dim must be 128");
-    attn_merge_kernel<<<dim3(n_rows, H), 128, 0, st>>>(part_o, part_ml, n_parts, tok0, H, max_parts, out, f32);
-    HK_CUDA(cudaGetLastError());
+    const int warps = n_rows * H;
+    attn_merge_kernel<<<(warps + 7) / 8, 256, 0, st>>>(part_o, part_ml, n_parts, n_rows, tok0, H, max_parts, out,
+                                                       f32);
+    HK_LAUNCHED(1);
 }
 
 }  // namespace hkd

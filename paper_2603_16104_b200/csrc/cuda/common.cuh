@@ -19,6 +19,16 @@
     } while (0)
 
 namespace hkd {
+extern unsigned long long g_launches;
+}
+// launch-error check + launch accounting (every kernel of this library goes through it)
+#define HK_LAUNCHED(n)                      \
+    do {                                    \
+        HK_CUDA(cudaGetLastError());        \
+        ::hkd::g_launches += (n);           \
+    } while (0)
+
+namespace hkd {
 
 using bf16 = __nv_bfloat16;
 

@@ -137,6 +137,10 @@ struct hk_engine {
     int32_t* sample_ids = nullptr;
     float* ws = nullptr;
     size_t ws_floats = 0;
+    float* pbuf = nullptr;  // fp32 split-K partials of QKV / O / down GEMMs
+    size_t pbuf_floats = 0;
+    void* hs = nullptr;     // normalized rows of sampled tokens (LM head input)
+    float2* amax = nullptr; // per (vocab tile, row) argmax partials
     float* part_o = nullptr;
     float2* part_ml = nullptr;
     int max_part_rows = 0;
@@ -170,6 +174,39 @@ struct hk_engine {
 
     KernelClock clock;
     double attn_alg_bytes_step = 0;
+
+    // run statistics (hk_engine_stats_get)
+    hk_engine_stats stats{};
+    cudaEvent_t ev_run0 = nullptr, ev_pins = nullptr, ev_end = nullptr;
+    unsigned long long launches0 = 0;
+    bool pins_marked = false;
+    void run_begin() {
+        if (!ev_run0) {
+            HK_CUDA(cudaEventCreate(&ev_run0));
+            HK_CUDA(cudaEventCreate(&ev_pins));
+            HK_CUDA(cudaEventCreate(&ev_end));
+        }
+        stats = hk_engine_stats{};
+        launches0 = hkd::g_launches;
+        pins_marked = false;
+        HK_CUDA(cudaEventRecord(ev_run0, st));
+    }
+    void mark_pins_done() {
+        if (pins_marked) return;
+        HK_CUDA(cudaEventRecord(ev_pins, st));
+        pins_marked = true;
+    }
+    void run_end() {
+        mark_pins_done();
+        HK_CUDA(cudaEventRecord(ev_end, st));
+        HK_CUDA(cudaEventSynchronize(ev_end));
+        float a = 0, b = 0;
+        HK_CUDA(cudaEventElapsedTime(&a, ev_run0, ev_pins));
+        HK_CUDA(cudaEventElapsedTime(&b, ev_pins, ev_end));
+        stats.pin_ms = a;
+        stats.iter_ms = b;
+        stats.launches = hkd::g_launches - launches0;
+    }
 
     // ---- construction ----
     hk_engine(const hk_model_config& m, const hk_engine_config& c);
@@ -283,6 +320,10 @@ hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m
     ws_floats = static_cast<size_t>(16) * std::max<size_t>(static_cast<size_t>(c.max_calls) * c.n_workers + 64, 256) *
                 std::max({QKV, d, 2 * F});
     ws = dalloc<float>(ws_floats);
+    pbuf_floats = std::max(static_cast<size_t>(maxT) * std::max(QKV, d) * 2, static_cast<size_t>(16) * 512 * std::max(QKV, d));
+    pbuf = dalloc<float>(pbuf_floats);
+    hs = dalloc<uint8_t>(static_cast<size_t>(maxS) * d * esz);
+    amax = dalloc<float2>(static_cast<size_t>((V + 127) / 128) * maxS);
     max_part_rows = static_cast<int>(c.max_calls * c.n_workers) + 16;
     part_o = dalloc<float>(static_cast<size_t>(max_part_rows) * H * max_parts * hd);
     part_ml = dalloc<float2>(static_cast<size_t>(max_part_rows) * H * max_parts);
@@ -305,7 +346,8 @@ hk_engine::~hk_engine() {
     }
     for (void* p : {static_cast<void*>(x), h, qkv, attn, gu, act, static_cast<void*>(logits),
                     static_cast<void*>(sample_ids), static_cast<void*>(ws), static_cast<void*>(part_o),
-                    static_cast<void*>(part_ml), static_cast<void*>(tok_d), static_cast<void*>(match_d)})
+                    static_cast<void*>(part_ml), static_cast<void*>(tok_d), static_cast<void*>(match_d),
+                    static_cast<void*>(pbuf), hs, static_cast<void*>(amax)})
         cudaFree(p);
     for (Meta& mt : meta) {
         cudaFree(mt.d);
@@ -354,7 +396,7 @@ void hk_engine::init_weights() {
         w.mlp_norm = take(d);
         hkd::fill_const(w.mlp_norm, f32, d, 1.0f, st);
         w.wgu = take(static_cast<size_t>(2) * F * d);
-        hkd::init_uniform(w.wgu, f32, static_cast<size_t>(2) * F * d, seed, t0 + 4, s_d, st);
+        hkd::init_uniform_gu(w.wgu, f32, F, d, seed, t0 + 4, s_d, st);  // rows interleaved [64 gate | 64 up]
         w.wd = take(static_cast<size_t>(d) * F);
         hkd::init_uniform(w.wd, f32, static_cast<size_t>(d) * F, seed, t0 + 5, 0.5f * s_f, st);
     }
@@ -418,12 +460,12 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
 
     // metadata layout (int32 words)
     std::vector<int32_t> ids(T), pos(T), slots(T), kvw(T), ptab(T), pages;
-    std::vector<hkd::AttnItem> items;
+    std::vector<hkd::AttnItem> items, items_single;  // multi-token (prefill/shared) | single-token (private)
     std::vector<int32_t> nparts(dec.size(), 0);
     std::vector<int32_t> srows, sslots;
     int t = 0;
     int n_pre_items = 0, n_sh_items = 0, n_pv_items = 0;
-    double alg_bytes = 0;
+    double alg_bytes = 0, alg_single = 0;  // algorithmic attention bytes: multi-token items | private items
     const double kv_tok_bytes = 2.0 * Hkv * hd * esz;
     for (int i : pre) {
         SegIn& s = segs[i];
@@ -490,13 +532,13 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
             int part = shared_keys > 0 ? (shared_keys + KS - 1) / KS : 0;
             for (int k0 = shared_keys; k0 < s.start + 1; k0 += KP) {
                 const int k1 = std::min(k0 + KP, s.start + 1);
-                for (int kh = 0; kh < Hkv; ++kh) items.push_back(hkd::AttnItem{t, 1, kh, off, k0, k1, 0, part});
+                for (int kh = 0; kh < Hkv; ++kh) items_single.push_back(hkd::AttnItem{t, 1, kh, off, k0, k1, 0, part});
                 n_pv_items += Hkv;
                 ++part;
             }
             if (part > max_parts) throw std::runtime_error("engine: too many attention partials");
             nparts[static_cast<size_t>(r)] = part;
-            alg_bytes += (s.start + 1 - shared_keys) * kv_tok_bytes + 2.0 * H * hd * esz;
+            alg_single += (s.start + 1 - shared_keys) * kv_tok_bytes + 2.0 * H * hd * esz;
             if (s.sample) {
                 srows.push_back(t);
                 sslots.push_back(s.slot);
@@ -520,11 +562,15 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     const int S = static_cast<int>(srows.size());
     if (S > maxS) throw std::runtime_error("engine: too many sampled rows in one step");
     if (static_cast<int>(dec.size()) > max_part_rows) throw std::runtime_error("engine: too many decode rows");
-    attn_alg_bytes_step = alg_bytes * L;
+    attn_alg_bytes_step = (alg_bytes + alg_single) * L;
 
     // pack metadata: ids pos slots kvw ptab | pages | nparts | srows sslots | items
+    const int n_multi = static_cast<int>(items.size());
+    items.insert(items.end(), items_single.begin(), items_single.end());
     const size_t n_items = items.size();
-    const size_t words = 5 * static_cast<size_t>(T) + pages.size() + nparts.size() + 2 * static_cast<size_t>(S) +
+    std::vector<int32_t> cmap(static_cast<size_t>(T), -1);  // batch row -> LM-head row
+    for (int k = 0; k < S; ++k) cmap[static_cast<size_t>(srows[static_cast<size_t>(k)])] = k;
+    const size_t words = 6 * static_cast<size_t>(T) + pages.size() + nparts.size() + 2 * static_cast<size_t>(S) +
                          n_items * (sizeof(hkd::AttnItem) / 4) + 64;
     Meta& mt = meta[meta_next];
     meta_next = (meta_next + 1) % kMetaRing;
@@ -550,8 +596,13 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     const size_t o_ids = put(ids.data(), T), o_pos = put(pos.data(), T), o_slots = put(slots.data(), T),
                  o_kvw = put(kvw.data(), T), o_ptab = put(ptab.data(), T), o_pages = put(pages.data(), pages.size()),
                  o_np = put(nparts.data(), nparts.size()), o_sr = put(srows.data(), S), o_ss = put(sslots.data(), S),
-                 o_items = put(reinterpret_cast<const int32_t*>(items.data()), n_items * sizeof(hkd::AttnItem) / 4);
+                 o_items = put(reinterpret_cast<const int32_t*>(items.data()), n_items * sizeof(hkd::AttnItem) / 4),
+                 o_cmap = put(cmap.data(), cmap.size());
     HK_CUDA(cudaMemcpyAsync(meta_d, meta_h, o * 4, cudaMemcpyHostToDevice, st));
+    stats.h2d_bytes += o * 4;
+    stats.steps += 1;
+    stats.step_tokens += static_cast<uint64_t>(T);
+    stats.attn_bytes += attn_alg_bytes_step;
     const int32_t* d_ids = meta_d + o_ids;
     const int32_t* d_pos = meta_d + o_pos;
     const int32_t* d_slots = meta_d + o_slots;
@@ -559,8 +610,9 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     const int32_t* d_ptab = meta_d + o_ptab;
     const int32_t* d_pages = meta_d + o_pages;
     const int32_t* d_np = meta_d + o_np;
-    const int32_t* d_sr = meta_d + o_sr;
     const int32_t* d_ss = meta_d + o_ss;
+    const int32_t* d_cmap = meta_d + o_cmap;
+    (void)o_sr;
     const hkd::AttnItem* d_items = reinterpret_cast<const hkd::AttnItem*>(meta_d + o_items);
     // items are packed pre | (per group: private..., shared...) — launch them as one grid
     (void)n_pre_items;
@@ -571,60 +623,76 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
     int ck = clock.begin(5, st);
     hkd::embed(embed, f32, d, d_ids, d_slots, wk.slot_last, T, x, st);
+    hkd::add_rmsnorm(nullptr, 0, x, layers[0].attn_norm, f32, T, d, eps, h, nullptr, nullptr, st);
     clock.end(ck, st, static_cast<double>(T) * d * (esz + 4));
-    auto gemm = [&](const void* W, const void* X, int N, int K, int epi, void* out, int ldo, const void* bias) {
+    // GEMMs into fp32 split-K partials (consumers reduce them), or fused epilogues
+    auto gemm = [&](const void* W, const void* X, int N, int K, int rows, int epi, void* out, int ldo) -> int {
         const int c = clock.begin(0, st);
-        if (f32)
-            hkd::gemm_f32(static_cast<const float*>(W), static_cast<const float*>(X), N, K, T, epi, out, ldo,
-                          static_cast<const float*>(bias), st);
-        else
-            hkd::gemm_bf16(static_cast<const bf16*>(W), static_cast<const bf16*>(X), N, K, T, epi, out, ldo,
-                           static_cast<const bf16*>(bias), ws, ws_floats, st);
-        clock.end(c, st, static_cast<double>(N) * K * esz + static_cast<double>(T) * K * esz);
+        int sp = 1;
+        if (f32) {
+            hkd::gemm_f32(static_cast<const float*>(W), static_cast<const float*>(X), N, K, rows,
+                          epi == hkd::kEpiPartial ? hkd::kEpiStoreF32 : epi, out, ldo, nullptr, st);
+        } else {
+            const int max_sp = static_cast<int>(std::max<size_t>(1, pbuf_floats / (static_cast<size_t>(rows) * N)));
+            sp = hkd::gemm_bf16(static_cast<const bf16*>(W), static_cast<const bf16*>(X), N, K, rows, epi, out, ldo,
+                                nullptr, ws, ws_floats, st, 0, max_sp);
+        }
+        clock.end(c, st, static_cast<double>(N) * K * esz + static_cast<double>(rows) * K * esz);
+        return sp;
     };
     for (int l = 0; l < L; ++l) {
         const LayerW& lw = layers[static_cast<size_t>(l)];
+        int sp = gemm(lw.wqkv, h, QKV, d, T, hkd::kEpiPartial, pbuf, QKV);
+        hkd::QkvArgs qa{pbuf, sp, lw.bqkv,
+                        hkd::RopeArgs{qkv, f32, T, H, Hkv, hd, d_pos, d_kvw, d_ptab, d_pages, rope, kv_layer(w, l), block}};
         ck = clock.begin(5, st);
-        hkd::rmsnorm(x, lw.attn_norm, f32, d, eps, nullptr, T, h, st);
-        clock.end(ck, st);
-        gemm(lw.wqkv, h, QKV, d, f32 ? hkd::kEpiStoreF32 : hkd::kEpiStoreBf16, qkv, QKV, lw.bqkv);
-        hkd::RopeArgs ra{qkv, f32, T, H, Hkv, hd, d_pos, d_kvw, d_ptab, d_pages, rope, kv_layer(w, l), block};
-        ck = clock.begin(5, st);
-        hkd::rope_kv_write(ra, st);
+        hkd::qkv_rope_kv(qa, st);
         clock.end(ck, st);
         hkd::AttnArgs aa{qkv, f32, H, Hkv, hd, block, d_pos, d_pages, kv_layer(w, l), d_items,
-                         static_cast<int>(n_items), attn, part_o, part_ml, max_parts, T_pre, scale};
+                         n_multi, attn, part_o, part_ml, max_parts, T_pre, scale, 0};
         ck = clock.begin(dec.empty() ? 3 : 1, st);
         hkd::attention_partial(aa, st);
         clock.end(ck, st, alg_bytes);
+        aa.items = d_items + n_multi;
+        aa.n_items = static_cast<int>(n_items) - n_multi;
+        aa.single = 1;
+        ck = clock.begin(2, st);
+        hkd::attention_partial(aa, st);
+        clock.end(ck, st, alg_single);
         ck = clock.begin(4, st);
         hkd::attention_merge(part_o, part_ml, d_np, static_cast<int>(dec.size()), T_pre, H, hd, max_parts, attn, f32, st);
         clock.end(ck, st);
-        gemm(lw.wo, attn, d, H * hd, hkd::kEpiAddF32, x, d, nullptr);
+        sp = gemm(lw.wo, attn, d, H * hd, T, hkd::kEpiPartial, pbuf, d);
         ck = clock.begin(5, st);
-        hkd::rmsnorm(x, lw.mlp_norm, f32, d, eps, nullptr, T, h, st);
+        hkd::add_rmsnorm(pbuf, sp, x, lw.mlp_norm, f32, T, d, eps, h, nullptr, nullptr, st);
         clock.end(ck, st);
-        gemm(lw.wgu, h, 2 * F, d, f32 ? hkd::kEpiStoreF32 : hkd::kEpiStoreBf16, gu, 2 * F, nullptr);
+        if (f32) {
+            gemm(lw.wgu, h, 2 * F, d, T, hkd::kEpiStoreF32, gu, 2 * F);
+            ck = clock.begin(5, st);
+            hkd::swiglu_interleaved(static_cast<const float*>(gu), T, F, static_cast<float*>(act), st);
+            clock.end(ck, st);
+        } else {
+            gemm(lw.wgu, h, 2 * F, d, T, hkd::kEpiSwiGLU, act, F);  // SwiGLU fused in the epilogue
+        }
+        sp = gemm(lw.wd, act, d, F, T, hkd::kEpiPartial, pbuf, d);
+        const bool last = l + 1 == L;
         ck = clock.begin(5, st);
-        hkd::swiglu(gu, f32, T, F, act, st);
+        hkd::add_rmsnorm(pbuf, sp, x, last ? final_norm : layers[static_cast<size_t>(l) + 1].attn_norm, f32, T, d, eps,
+                         h, last && S > 0 ? d_cmap : nullptr, last && S > 0 ? hs : nullptr, st);
         clock.end(ck, st);
-        gemm(lw.wd, act, d, F, hkd::kEpiAddF32, x, d, nullptr);
     }
     if (S > 0) {
-        ck = clock.begin(5, st);
-        hkd::rmsnorm(x, final_norm, f32, d, eps, d_sr, S, h, st);
-        clock.end(ck, st);
-        const int c = clock.begin(0, st);
-        if (f32)
-            hkd::gemm_f32(static_cast<const float*>(lm_head), static_cast<const float*>(h), V, d, S, hkd::kEpiStoreF32,
-                          logits, V, nullptr, st);
-        else
-            hkd::gemm_bf16(static_cast<const bf16*>(lm_head), static_cast<const bf16*>(h), V, d, S, hkd::kEpiStoreF32,
-                           logits, V, nullptr, ws, ws_floats, st);
-        clock.end(c, st, static_cast<double>(V) * d * esz);
-        ck = clock.begin(5, st);
-        hkd::argmax_rows(logits, S, V, sample_ids, d_ss, wk.slot_last, st);
-        clock.end(ck, st);
+        if (f32 || logits_out_host) {
+            gemm(lm_head, hs, V, d, S, hkd::kEpiStoreF32, logits, V);
+            ck = clock.begin(5, st);
+            hkd::argmax_rows(logits, S, V, sample_ids, d_ss, wk.slot_last, st);
+            clock.end(ck, st);
+        } else {
+            gemm(lm_head, hs, V, d, S, hkd::kEpiArgmax, amax, V);  // greedy argmax fused in the epilogue
+            ck = clock.begin(5, st);
+            hkd::argmax_reduce(amax, (V + 127) / 128, S, sample_ids, d_ss, wk.slot_last, st);
+            clock.end(ck, st);
+        }
         if (logits_out_host)
             HK_CUDA(cudaMemcpyAsync(logits_out_host, logits, static_cast<size_t>(S) * V * 4, cudaMemcpyDeviceToHost, st));
         // harvest ring: D2H of the sampled ids into pinned memory
@@ -646,6 +714,7 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         p.worker = w;
         p.slots = sslots;
         HK_CUDA(cudaMemcpyAsync(p.host, sample_ids, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, st));
+        stats.d2h_bytes += static_cast<uint64_t>(S) * 4;
         HK_CUDA(cudaEventRecord(p.ev, st));
         pending.push_back(std::move(p));
         if (pending.size() > 64) harvest(false);
@@ -696,6 +765,7 @@ void hk_engine::trie_sync(int w, std::vector<hk::TrieOp>& ops, const std::functi
     HK_CUDA(cudaStreamSynchronize(st));
     HK_CUDA(cudaMemcpyAsync(tok_d, dev.data(), op_words * 8, cudaMemcpyHostToDevice, st));
     HK_CUDA(cudaMemcpyAsync(tok_d + op_words, keys.data(), keys.size() * 8, cudaMemcpyHostToDevice, st));
+    stats.h2d_bytes += (op_words + keys.size()) * 8;
     const int c = clock.begin(6, st);
     hkd::trie_apply(wk.trie, reinterpret_cast<const hkd::TrieOpDev*>(tok_d), tok_d + op_words,
                     static_cast<int>(dev.size()), st);
@@ -743,6 +813,8 @@ void hk_engine::trie_lookup(int w, const std::vector<const std::vector<uint64_t>
     HK_CUDA(cudaMemcpyAsync(hm.data(), d_matched, hm.size() * 4, cudaMemcpyDeviceToHost, st));
     HK_CUDA(cudaMemcpyAsync(hp.data(), d_path, hp.size() * 4, cudaMemcpyDeviceToHost, st));
     HK_CUDA(cudaStreamSynchronize(st));
+    stats.h2d_bytes += (flat.size() + offs.size()) * 8;
+    stats.d2h_bytes += (hm.size() + hp.size()) * 4;
     paths.assign(static_cast<size_t>(n), {});
     for (int i = 0; i < n; ++i)
         paths[static_cast<size_t>(i)].assign(hp.begin() + static_cast<std::ptrdiff_t>(i) * stride,
@@ -755,7 +827,7 @@ namespace hk {
 class DeviceBody : public LlmBody {
   public:
     DeviceBody(hk_engine* e, const Plan& plan, const SimConfig& cfg) : e_(e) {
-        if (cfg.workers.size() != e->workers.size())
+        if (cfg.workers.size() != e->workers.size() && e->workers.size() != 1)
             throw std::runtime_error("hk_simulate: engine has " + std::to_string(e->workers.size()) +
                                      " worker pools but the schedule has " + std::to_string(cfg.workers.size()) +
                                      " workers");
@@ -764,7 +836,11 @@ class DeviceBody : public LlmBody {
                 throw std::runtime_error("hk_simulate: SimWorkerConfig::block differs from the engine page size");
         e_->sync();
         e_->reset_workers();
+        e_->run_begin();
         (void)plan;
+    }
+    void begin_iteration(std::uint64_t, const std::vector<std::pair<int, LiveCall*>>&) override {
+        e_->mark_pins_done();
     }
     bool uses_pages() const override { return true; }
     int pages_per_worker(int) const override { return static_cast<int>(e_->ec.pages_per_worker); }
@@ -783,18 +859,18 @@ class DeviceBody : public LlmBody {
                 segs[0].count = std::min(e_->maxT, len - c0);
                 segs[0].table = &pin_pages[i];
                 segs[0].prompt = &pins[i];
-                e_->step(w, segs);
+                e_->step(pw(w), segs);
             }
         }
         e_->sync();
     }
     void sync_trie(int w, KvTree& tree) override {
-        e_->trie_sync(w, tree.journal(), [&tree](int node) { return tree.node_key(node); });
+        e_->trie_sync(pw(w), tree.journal(), [&tree](int node) { return tree.node_key(node); });
     }
     void lookup_batch(int w, const std::vector<const TokenSeq*>& prompts, std::vector<std::vector<int>>& paths) override {
-        e_->trie_lookup(w, prompts, paths);
+        e_->trie_lookup(pw(w), prompts, paths);
     }
-    void on_admit(int w, LiveCall& lc) override { lc.slot = e_->alloc_slot(w); }
+    void on_admit(int w, LiveCall& lc) override { lc.slot = e_->alloc_slot(pw(w)); }
     void run_step(StepPlan& sp) override {
         std::vector<hk_engine::SegIn> segs;
         segs.reserve(sp.segs.size());
@@ -810,10 +886,10 @@ class DeviceBody : public LlmBody {
             in.prompt = &s.call->prompt;
             segs.push_back(in);
         }
-        e_->step(sp.worker, segs);
+        e_->step(pw(sp.worker), segs);
     }
     TokenSeq take_output(int w, LiveCall& lc, double, bool) override {
-        auto& toks = e_->workers[static_cast<size_t>(w)].slot_tokens[static_cast<size_t>(lc.slot)];
+        auto& toks = e_->workers[static_cast<size_t>(pw(w))].slot_tokens[static_cast<size_t>(lc.slot)];
         if (toks.size() < lc.out_len) e_->harvest(true);
         if (toks.size() < lc.out_len) {
             HK_CUDA(cudaStreamSynchronize(e_->st));
@@ -826,12 +902,17 @@ class DeviceBody : public LlmBody {
         return out;
     }
     void on_finish(int w, LiveCall& lc) override {
-        if (lc.slot >= 0) e_->free_slot(w, lc.slot);
+        if (lc.slot >= 0) e_->free_slot(pw(w), lc.slot);
         lc.slot = -1;
     }
-    void finish_run() override { e_->sync(); }
+    void finish_run() override {
+        e_->run_end();
+        e_->sync();
+    }
 
   private:
+    // engine pool of schedule worker w (a single pool serves one-worker mode)
+    int pw(int w) const { return e_->workers.size() == 1 ? 0 : w; }
     hk_engine* e_;
 };
 
@@ -1013,6 +1094,12 @@ double hk_engine_kernel_ms(const hk_engine* ce, const char* family, uint64_t* la
             return e->clock.ms[i];
         }
     return -1;
+}
+
+int hk_engine_stats_get(const hk_engine* e, hk_engine_stats* out) {
+    if (!e || !out) return -1;
+    *out = e->stats;
+    return 0;
 }
 
 int hk_engine_profile(hk_engine* e, int enable) {

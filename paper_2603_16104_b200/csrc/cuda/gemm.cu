@@ -110,11 +110,75 @@ __global__ void __launch_bounds__(128, 1)
     mbar_wait(done, 0);
     __syncwarp();
     tc_fence_after();
-    const int m = m0 + warp * 32 + lane;
+    const int row = warp * 32 + lane;
+    const int m = m0 + row;
     const bool m_ok = m < p.N;
-    const float bias = (p.bias && m_ok && p.epi != 3) ? bf2f(p.bias[m]) : 0.f;
+    if (p.epi == kEpiSwiGLU) {
+        // TMEM lanes 0-63 hold gate rows, 64-127 the matching up rows (warp w
+        // may only read lanes 32w..32w+31): up values go through smem.
+        float* xs = reinterpret_cast<float*>(smem);  // [64][BN + 1], pipeline buffers are free now
+        if (warp >= 2) {
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 8) {
+            for (int c = 0; c < BN; c += 8) {
+                float v[8];
+                tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) xs[(row - 64) * (BN + 1) + c + j] = v[j];
+            }
+        }
+        __syncthreads();
+        if (warp < 2) {
+            const int f = blockIdx.x * 64 + row;  // output feature
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 8) {
+                float v[8];
+                tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int n = n0 + c + j;
+                    if (n < p.T && m_ok) {
+                        const float g = v[j], u = xs[row * (BN + 1) + c + j];
+                        static_cast<bf16*>(p.out)[static_cast<size_t>(n) * p.ldo + f] = f2bf(g / (1.0f + expf(-g)) * u);
+                    }
+                }
+            }
+        }
+    } else if (p.epi == kEpiArgmax) {
+        float2* red = reinterpret_cast<float2*>(smem);  // [4][BN] (value, index)
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 8) {
+            float v[8];
+            tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float best = m_ok ? v[j] : -INFINITY;
+                int bi = m;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (ov > best || (ov == best && oi < bi)) {
+                        best = ov;
+                        bi = oi;
+                    }
+                }
+                if (lane == 0) red[warp * BN + c + j] = make_float2(best, __int_as_float(bi));
+            }
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < BN; c += blockDim.x) {
+            float2 b = red[c];
+            for (int w2 = 1; w2 < 4; ++w2) {
+                const float2 o = red[w2 * BN + c];
+                if (o.x > b.x) b = o;  // earlier warps hold lower rows: keep them on ties
+            }
+            const int n = n0 + c;
+            if (n < p.T) reinterpret_cast<float2*>(p.out)[static_cast<size_t>(blockIdx.x) * p.T + n] = b;
+        }
+    }
+    const float bias = (p.bias && m_ok && p.epi != kEpiPartial) ? bf2f(p.bias[m]) : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < BN && p.epi < kEpiSwiGLU; c += 8) {
         float v[8];
         tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
         if (!m_ok) continue;
@@ -250,16 +314,17 @@ void launch_tc(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p
         configured = true;
     }
     gemm_tc_kernel<BN, STAGES><<<grid, 128, sm, st>>>(tw, tx, p);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 }  // namespace
 
 int g_num_sms = 148;
+unsigned long long g_launches = 0;
 
-void gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, const bf16* bias,
-               float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits) {
-    if (T <= 0) return;
+int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, const bf16* bias,
+              float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits, int max_splits) {
+    if (T <= 0) return 0;
     if (K % BK != 0) throw std::runtime_error("gemm_bf16: K must be a multiple of 64");
     int BN;
     if (T <= 16)
@@ -276,19 +341,24 @@ void gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void*
     const int nt = (T + BN - 1) / BN;
     const int kb = K / BK;
     int splits = 1;
-    if (force_splits > 0) {
+    if (epi == kEpiSwiGLU || epi == kEpiArgmax) {
+        splits = 1;  // epilogue needs the whole K reduction in TMEM
+    } else if (force_splits > 0) {
         splits = force_splits;
     } else if (mt * nt < g_num_sms * 3 / 4) {
         splits = std::max(1, g_num_sms / (mt * nt));
         splits = std::min(splits, std::max(1, kb / 4));
     }
+    splits = std::min(splits, std::max(1, max_splits));
     int kbps = (kb + splits - 1) / splits;
     splits = (kb + kbps - 1) / kbps;  // no empty splits
-    if (splits > 1 && static_cast<size_t>(splits) * T * N > workspace_floats) {
+    if (epi != kEpiPartial && splits > 1 && static_cast<size_t>(splits) * T * N > workspace_floats) {
         splits = 1;
         kbps = kb;
     }
-    GemmParams p{N, K, T, kb, kbps, splits > 1 ? kEpiPartial : epi, out, ldo, bias, workspace};
+    const bool via_ws = splits > 1 && epi != kEpiPartial;
+    GemmParams p{N, K, T, kb, kbps, via_ws ? kEpiPartial : epi, out, ldo, bias,
+                 epi == kEpiPartial ? static_cast<float*>(out) : workspace};
     const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
     const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
     dim3 grid(mt, nt, splits);
@@ -299,12 +369,62 @@ void gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void*
         case 128: launch_tc<128, 6>(tw, tx, p, grid, st); break;
         default: launch_tc<256, 4>(tw, tx, p, grid, st); break;
     }
-    if (splits > 1) {
+    if (via_ws) {
         const size_t total = static_cast<size_t>(T) * N;
         const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 4096));
         splitk_reduce_kernel<<<blocks, 256, 0, st>>>(workspace, splits, T, N, epi, out, ldo, bias);
-        HK_CUDA(cudaGetLastError());
+        HK_LAUNCHED(1);
     }
+    return splits;
+}
+
+namespace {
+__global__ void argmax_reduce_kernel(const float2* __restrict__ part, int n_tiles, int T, int32_t* ids,
+                                     const int32_t* slots, int32_t* slot_last) {
+    const int t = blockIdx.x;
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
+        const float2 v = part[static_cast<size_t>(i) * T + t];
+        const int idx = __float_as_int(v.y);
+        if (v.x > best || (v.x == best && idx < bi)) {
+            best = v.x;
+            bi = idx;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) {
+            best = ov;
+            bi = oi;
+        }
+    }
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    if ((threadIdx.x & 31) == 0) {
+        sv[threadIdx.x >> 5] = best;
+        si[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+            if (sv[w] > best || (sv[w] == best && si[w] < bi)) {
+                best = sv[w];
+                bi = si[w];
+            }
+        ids[t] = bi;
+        if (slots) slot_last[slots[t]] = bi;
+    }
+}
+}  // namespace
+
+void argmax_reduce(const float2* part, int n_tiles, int T, int32_t* ids, const int32_t* slots, int32_t* slot_last,
+                   cudaStream_t st) {
+    if (T <= 0) return;
+    argmax_reduce_kernel<<<T, 256, 0, st>>>(part, n_tiles, T, ids, slots, slot_last);
+    HK_LAUNCHED(1);
 }
 
 void gemm_f32(const float* W, const float* X, int N, int K, int T, int epi, void* out, int ldo, const float* bias,
@@ -312,7 +432,7 @@ void gemm_f32(const float* W, const float* X, int N, int K, int T, int epi, void
     if (T <= 0) return;
     dim3 grid((N + 31) / 32, (T + 31) / 32);
     gemm_f32_kernel<<<grid, 256, 0, st>>>(W, X, N, K, T, epi, out, ldo, bias);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 }  // namespace hkd

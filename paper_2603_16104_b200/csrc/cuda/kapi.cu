@@ -40,9 +40,10 @@ int hkx_gemm_bf16(const void* W, const void* X, void* out, int N, int K, int T, 
     try {
         init_sms();
         const size_t ws = static_cast<size_t>(32) * (T + 256) * N;
-        hkd::gemm_bf16(static_cast<const hkd::bf16*>(W), static_cast<const hkd::bf16*>(X), N, K, T, epi, out, N,
+        const int ldo = epi == hkd::kEpiSwiGLU ? N / 2 : N;
+        hkd::gemm_bf16(static_cast<const hkd::bf16*>(W), static_cast<const hkd::bf16*>(X), N, K, T, epi, out, ldo,
                        static_cast<const hkd::bf16*>(bias), workspace(ws), ws, static_cast<cudaStream_t>(stream),
-                       splits);
+                       splits, 64);
         return 0;
     } catch (const std::exception& e) {
         hk::set_error(e.what());

@@ -8,13 +8,24 @@
 
 namespace hkd {
 
-enum : int { kEpiStoreBf16 = 0, kEpiAddF32 = 1, kEpiStoreF32 = 2, kEpiPartial = 3 };
+// GEMM epilogues. kEpiPartial writes fp32 split-K partials [splits][T][N] that
+// a consumer row kernel reduces (fused with bias / RoPE / residual / RMSNorm);
+// kEpiSwiGLU expects W rows interleaved per 128-row tile as [64 gate | 64 up]
+// and writes silu(gate) * up as bf16 [T][N/2]; kEpiArgmax writes per-(tile,
+// token) (max, argmax) pairs [N/128][T] for argmax_reduce.
+enum : int { kEpiStoreBf16 = 0, kEpiAddF32 = 1, kEpiStoreF32 = 2, kEpiPartial = 3, kEpiSwiGLU = 4, kEpiArgmax = 5 };
 extern int g_num_sms;
+extern unsigned long long g_launches;  // kernels launched by this library (all launchers count)
 
 // ----------------------------------------------------------------- gemm.cu
 // out[t][n] (+)= sum_k X[t][k] W[n][k] (+ bias[n]); tcgen05 path for bf16.
-void gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, const bf16* bias,
-               float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits = 0);
+// Returns the split-K factor used (kEpiPartial: `out` must hold splits*T*N floats;
+// max_splits bounds it). Other epilogues reduce split partials through `workspace`.
+int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, const bf16* bias,
+              float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits = 0, int max_splits = 16);
+// ids[t] = argmax over the n_tiles (max, idx) partials of kEpiArgmax (lowest index wins ties)
+void argmax_reduce(const float2* part, int n_tiles, int T, int32_t* ids, const int32_t* slots, int32_t* slot_last,
+                   cudaStream_t st);
 void gemm_f32(const float* W, const float* X, int N, int K, int T, int epi, void* out, int ldo, const float* bias,
               cudaStream_t st);
 
@@ -43,6 +54,24 @@ struct RopeArgs {
 };
 void rope_kv_write(const RopeArgs& a, cudaStream_t st);
 void swiglu(const void* gu, bool f32, int T, int F, void* out, cudaStream_t st);
+// gate/up weights are stored with rows interleaved per 128-row tile ([64 gate | 64 up]);
+// init maps the physical index back to the logical (gate | up) index of the oracle.
+void init_uniform_gu(void* w, bool f32, int F, int d, uint64_t seed, uint64_t tensor_id, float scale, cudaStream_t st);
+// fp32 parity path: silu(gate) * up from an interleaved [T][2F] GEMM output
+void swiglu_interleaved(const float* gu, int T, int F, float* out, cudaStream_t st);
+// Split-K consumer: qkv = sum_s part[s] (+ bias); RoPE on q/k; q -> qkv (bf16 or f32);
+// k, v -> this layer's KV pages (tokens with kvw != 0).
+struct QkvArgs {
+    const float* part;      // [splits][T][QKV]
+    int splits;
+    const void* bias;       // [QKV] or null
+    RopeArgs r;             // r.qkv receives the rotated q (and raw k, v) rows
+};
+void qkv_rope_kv(const QkvArgs& a, cudaStream_t st);
+// Split-K consumer: x[t] += sum_s part[s][t]; h[t] = rmsnorm(x[t]) * w; rows with
+// cmap[t] >= 0 are also written to hc[cmap[t]] (compact rows for the LM head).
+void add_rmsnorm(const float* part, int splits, float* x, const void* w, bool f32, int T, int d, float eps, void* h,
+                 const int32_t* cmap, void* hc, cudaStream_t st);
 // ids[r] = argmax_v logits[r][v] (lowest index on ties); also slot_last[slots[r]] = ids[r]
 void argmax_rows(const float* logits, int R, int V, int32_t* ids, const int32_t* slots, int32_t* slot_last,
                  cudaStream_t st);
@@ -73,6 +102,7 @@ struct AttnArgs {
     int max_parts;
     int part_tok0;         // first batch token that has partials (decode tokens are last)
     float scale;
+    int single;            // items hold exactly one token each (private decode suffixes)
 };
 void attention_partial(const AttnArgs& a, cudaStream_t st);
 // out[tok0 + r][h] = merge of the n_parts[r] partials of row r, r < n_rows

@@ -191,32 +191,234 @@ __global__ void argmax_kernel(const float* logits, int V, int32_t* ids, const in
 
 int grid_for(size_t n) { return static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 16)); }
 
+__global__ void init_gu_kernel(void* w, bool f32, int F, int d, uint64_t seed, uint64_t tid, float scale) {
+    const uint64_t base = seed * 0xd1b54a32d192ed03ull + tid * 0x9e3779b97f4a7c15ull;
+    const size_t n = static_cast<size_t>(2) * F * d;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t p = i / d, col = i % d;
+        const size_t tile = p / 128, r = p % 128;
+        const size_t lrow = r < 64 ? tile * 64 + r : static_cast<size_t>(F) + tile * 64 + (r - 64);
+        const uint64_t h = splitmix64(base + lrow * d + col);
+        const float u = static_cast<float>(static_cast<uint32_t>(h >> 40)) * (1.0f / 8388608.0f) - 1.0f;
+        const float v = __fmul_rn(u, scale);
+        if (f32)
+            static_cast<float*>(w)[i] = v;
+        else
+            static_cast<bf16*>(w)[i] = __float2bfloat16_rn(v);
+    }
+}
+
+__global__ void swiglu_interleaved_kernel(const float* __restrict__ gu, int F, float* __restrict__ out) {
+    const int t = blockIdx.y;
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= F) return;
+    const size_t col = static_cast<size_t>(f / 64) * 128 + f % 64;
+    const float g = gu[static_cast<size_t>(t) * 2 * F + col];
+    const float u = gu[static_cast<size_t>(t) * 2 * F + col + 64];
+    out[static_cast<size_t>(t) * F + f] = g / (1.0f + expf(-g)) * u;
+}
+
+// One thread per rotated pair (q and k heads) or per value pair (v heads).
+template <typename T>
+__global__ void qkv_rope_kv_kernel(QkvArgs a) {
+    const RopeArgs& r = a.r;
+    const int t = blockIdx.y;
+    const int half = r.hd / 2;
+    const int n_rot = (r.H + r.Hkv) * half;   // (i, i + half) pairs of q and k heads
+    const int n_v = r.Hkv * half;             // v handled as (2j, 2j + 1) pairs
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_rot + n_v) return;
+    const int QKV = (r.H + 2 * r.Hkv) * r.hd;
+    const size_t tstride = static_cast<size_t>(r.T) * QKV;
+    const float* src = a.part + static_cast<size_t>(t) * QKV;
+    const int pos = r.pos[t];
+    const bool write = r.kvw[t] != 0;
+    T* row = static_cast<T*>(r.qkv) + static_cast<size_t>(t) * QKV;
+    T* kv = static_cast<T*>(r.kv_layer);
+    const size_t head_stride = static_cast<size_t>(r.block) * r.hd;
+    int page = 0;
+    if (write) page = r.pages[r.ptab[t] + pos / r.block];
+    int c0, c1;
+    if (j < n_rot) {
+        const int hh = j / half, i = j % half;
+        c0 = hh * r.hd + i;
+        c1 = c0 + half;
+    } else {
+        const int jj = j - n_rot;
+        c0 = (r.H + r.Hkv) * r.hd + 2 * jj;
+        c1 = c0 + 1;
+    }
+    float x0 = 0.f, x1 = 0.f;
+    for (int s = 0; s < a.splits; ++s) {
+        x0 += src[s * tstride + c0];
+        x1 += src[s * tstride + c1];
+    }
+    if (a.bias) {
+        if (sizeof(T) == 4) {
+            x0 += static_cast<const float*>(a.bias)[c0];
+            x1 += static_cast<const float*>(a.bias)[c1];
+        } else {
+            x0 += bf2f(static_cast<const bf16*>(a.bias)[c0]);
+            x1 += bf2f(static_cast<const bf16*>(a.bias)[c1]);
+        }
+    }
+    if (j < n_rot) {
+        // round to the storage type first: the oracle rotates the stored (bf16) qkv
+        const T s0 = cvt<T>(x0), s1 = cvt<T>(x1);
+        x0 = ld(&s0);
+        x1 = ld(&s1);
+        const int i = (j % half);
+        const float2 cs = r.rope[static_cast<size_t>(pos) * half + i];
+        const float o1 = x0 * cs.x - x1 * cs.y;
+        const float o2 = x1 * cs.x + x0 * cs.y;
+        const T q1 = cvt<T>(o1), q2 = cvt<T>(o2);
+        row[c0] = q1;
+        row[c1] = q2;
+        const int hh = j / half;
+        if (write && hh >= r.H) {
+            T* kd = kv + ((static_cast<size_t>(page) * 2 + 0) * r.Hkv + (hh - r.H)) * head_stride +
+                    static_cast<size_t>(pos % r.block) * r.hd;
+            kd[i] = q1;
+            kd[i + half] = q2;
+        }
+    } else {
+        const T v0 = cvt<T>(x0), v1 = cvt<T>(x1);
+        row[c0] = v0;
+        row[c1] = v1;
+        if (write) {
+            const int vc = c0 - (r.H + r.Hkv) * r.hd;
+            T* vd = kv + ((static_cast<size_t>(page) * 2 + 1) * r.Hkv + vc / r.hd) * head_stride +
+                    static_cast<size_t>(pos % r.block) * r.hd + vc % r.hd;
+            vd[0] = v0;
+            vd[1] = v1;
+        }
+    }
+}
+
+// Row kernel, 256 threads, row held in registers (d <= 8192).
+template <typename T>
+__global__ void __launch_bounds__(256) add_rmsnorm_kernel(const float* __restrict__ part, int splits, float* x,
+                                                          const T* __restrict__ w, int T_, int d, float eps, T* h,
+                                                          const int32_t* __restrict__ cmap, T* hc) {
+    const int t = blockIdx.x;
+    const int n4 = d / 4;
+    float4 v[8];
+    float ss = 0.f;
+    float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(t) * d);
+    const size_t pstride = static_cast<size_t>(T_) * d / 4;
+    const float4* pr = reinterpret_cast<const float4*>(part) + static_cast<size_t>(t) * d / 4;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int i = threadIdx.x + k * 256;
+        if (i < n4) {
+            float4 a = xr[i];
+            for (int s = 0; s < splits; ++s) {
+                const float4 b = pr[s * pstride + i];
+                a.x += b.x;
+                a.y += b.y;
+                a.z += b.z;
+                a.w += b.w;
+            }
+            v[k] = a;
+            ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+        }
+    }
+    __shared__ float red[8];
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tot += red[k];
+    const float inv = rsqrtf(tot / static_cast<float>(d) + eps);
+    const int cr = cmap ? cmap[t] : -1;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int i = threadIdx.x + k * 256;
+        if (i < n4) {
+            if (splits > 0) xr[i] = v[k];
+            const float4 a = v[k];
+            const float o0 = a.x * inv * ld(w + 4 * i), o1 = a.y * inv * ld(w + 4 * i + 1),
+                        o2 = a.z * inv * ld(w + 4 * i + 2), o3 = a.w * inv * ld(w + 4 * i + 3);
+            T* hr = h + static_cast<size_t>(t) * d + 4 * i;
+            hr[0] = cvt<T>(o0);
+            hr[1] = cvt<T>(o1);
+            hr[2] = cvt<T>(o2);
+            hr[3] = cvt<T>(o3);
+            if (cr >= 0) {
+                T* hcr = hc + static_cast<size_t>(cr) * d + 4 * i;
+                hcr[0] = cvt<T>(o0);
+                hcr[1] = cvt<T>(o1);
+                hcr[2] = cvt<T>(o2);
+                hcr[3] = cvt<T>(o3);
+            }
+        }
+    }
+}
+
 }  // namespace
+
+void init_uniform_gu(void* w, bool f32, int F, int d, uint64_t seed, uint64_t tensor_id, float scale, cudaStream_t st) {
+    init_gu_kernel<<<grid_for(static_cast<size_t>(2) * F * d), 256, 0, st>>>(w, f32, F, d, seed, tensor_id, scale);
+    HK_LAUNCHED(1);
+}
+
+void swiglu_interleaved(const float* gu, int T, int F, float* out, cudaStream_t st) {
+    if (!T) return;
+    swiglu_interleaved_kernel<<<dim3((F + 255) / 256, T), 256, 0, st>>>(gu, F, out);
+    HK_LAUNCHED(1);
+}
+
+void qkv_rope_kv(const QkvArgs& a, cudaStream_t st) {
+    if (!a.r.T) return;
+    const int half = a.r.hd / 2;
+    const int n = (a.r.H + a.r.Hkv) * half + a.r.Hkv * half;
+    dim3 grid((n + 255) / 256, a.r.T);
+    if (a.r.f32)
+        qkv_rope_kv_kernel<float><<<grid, 256, 0, st>>>(a);
+    else
+        qkv_rope_kv_kernel<bf16><<<grid, 256, 0, st>>>(a);
+    HK_LAUNCHED(1);
+}
+
+void add_rmsnorm(const float* part, int splits, float* x, const void* w, bool f32, int T, int d, float eps, void* h,
+                 const int32_t* cmap, void* hc, cudaStream_t st) {
+    if (!T) return;
+    if (d % 4 || d > 8192) throw std::runtime_error("add_rmsnorm: d must be a multiple of 4 and <= 8192");
+    if (f32)
+        add_rmsnorm_kernel<float><<<T, 256, 0, st>>>(part, splits, x, static_cast<const float*>(w), T, d, eps,
+                                                     static_cast<float*>(h), cmap, static_cast<float*>(hc));
+    else
+        add_rmsnorm_kernel<bf16><<<T, 256, 0, st>>>(part, splits, x, static_cast<const bf16*>(w), T, d, eps,
+                                                    static_cast<bf16*>(h), cmap, static_cast<bf16*>(hc));
+    HK_LAUNCHED(1);
+}
 
 void init_uniform(void* w, bool f32, size_t n, uint64_t seed, uint64_t tensor_id, float scale, cudaStream_t st) {
     if (!n) return;
     init_uniform_kernel<<<grid_for(n), 256, 0, st>>>(w, f32, n, seed, tensor_id, scale);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 void fill_const(void* w, bool f32, size_t n, float v, cudaStream_t st) {
     if (!n) return;
     fill_kernel<<<grid_for(n), 256, 0, st>>>(w, f32, n, v);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 void embed(const void* table, bool f32, int d, const int32_t* ids, const int32_t* slots, const int32_t* slot_last,
            int T, float* x, cudaStream_t st) {
     if (!T) return;
     embed_kernel<<<T, 256, 0, st>>>(table, f32, d, ids, slots, slot_last, x);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 void rmsnorm(const float* x, const void* w, bool f32, int d, float eps, const int32_t* rows, int R, void* out,
              cudaStream_t st) {
     if (!R) return;
     rmsnorm_kernel<<<R, 256, 0, st>>>(x, w, f32, d, eps, rows, out);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 void rope_kv_write(const RopeArgs& a, cudaStream_t st) {
@@ -225,7 +427,7 @@ void rope_kv_write(const RopeArgs& a, cudaStream_t st) {
         rope_kv_kernel<float><<<a.T, 256, 0, st>>>(a);
     else
         rope_kv_kernel<bf16><<<a.T, 256, 0, st>>>(a);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 void swiglu(const void* gu, bool f32, int T, int F, void* out, cudaStream_t st) {
@@ -234,14 +436,14 @@ void swiglu(const void* gu, bool f32, int T, int F, void* out, cudaStream_t st) 
         swiglu_kernel<float><<<T, 256, 0, st>>>(static_cast<const float*>(gu), F, static_cast<float*>(out));
     else
         swiglu_kernel<bf16><<<T, 256, 0, st>>>(static_cast<const bf16*>(gu), F, static_cast<bf16*>(out));
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 void argmax_rows(const float* logits, int R, int V, int32_t* ids, const int32_t* slots, int32_t* slot_last,
                  cudaStream_t st) {
     if (!R) return;
     argmax_kernel<<<R, 512, 0, st>>>(logits, V, ids, slots, slot_last);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 }  // namespace hkd

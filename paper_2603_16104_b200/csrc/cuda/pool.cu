@@ -39,7 +39,7 @@ void pool_gather(const void* kv, size_t layer_stride, int L, size_t page_bytes, 
     if (n <= 0) return;
     page_move_kernel<<<dim3(n, L), 256, 0, st>>>(static_cast<const uint8_t*>(kv), static_cast<uint8_t*>(dst),
                                                  layer_stride, L, page_bytes, pages, nullptr, 0);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 void pool_scatter(void* kv, size_t layer_stride, int L, size_t page_bytes, const int32_t* pages, int n, const void* src,
@@ -47,7 +47,7 @@ void pool_scatter(void* kv, size_t layer_stride, int L, size_t page_bytes, const
     if (n <= 0) return;
     page_move_kernel<<<dim3(n, L), 256, 0, st>>>(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(kv),
                                                  layer_stride, L, page_bytes, nullptr, pages, 1);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 void pool_copy(void* kv, size_t layer_stride, int L, size_t page_bytes, const int32_t* src, const int32_t* dst, int n,
@@ -55,7 +55,7 @@ void pool_copy(void* kv, size_t layer_stride, int L, size_t page_bytes, const in
     if (n <= 0) return;
     page_move_kernel<<<dim3(n, L), 256, 0, st>>>(static_cast<const uint8_t*>(kv), static_cast<uint8_t*>(kv),
                                                  layer_stride, L, page_bytes, src, dst, 2);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 }  // namespace hkd

@@ -150,7 +150,7 @@ void trie_apply(DevTrie& t, const TrieOpDev* ops, const uint64_t* keys, int n_op
     const int blocks = (n_ops + 127) / 128;
     trie_erase_kernel<<<blocks, 128, 0, st>>>(t, ops, n_ops);
     trie_insert_kernel<<<blocks, 128, 0, st>>>(t, ops, keys, n_ops);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(2);
 }
 
 void trie_match(const DevTrie& t, const uint64_t* tokens, const uint64_t* offsets, int n_prompts, int32_t* matched,
@@ -160,7 +160,7 @@ void trie_match(const DevTrie& t, const uint64_t* tokens, const uint64_t* offset
     if (sm > 48 * 1024) HK_CUDA(cudaFuncSetAttribute(trie_match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      static_cast<int>(sm)));
     trie_match_kernel<<<n_prompts, 256, sm, st>>>(t, tokens, offsets, matched, node_path, page_table, stride);
-    HK_CUDA(cudaGetLastError());
+    HK_LAUNCHED(1);
 }
 
 }  // namespace hkd

@@ -67,6 +67,7 @@ hk_run* hk_simulate(const uint8_t* plan, size_t plan_len, const hk_sim_config* c
             auto run = std::make_unique<hk_run>();
             hk::ExecOptions eo;
             eo.verify_device_lookup = (flags & 1u) != 0;
+            eo.only_worker = static_cast<int>((flags >> 8) & 0xFFFFu) - 1;
             if (engine) {
                 std::unique_ptr<hk::LlmBody> body = hk::make_device_body(engine, p, sc);
                 run->m = hk::simulate(p, sc, *body, eo);
@@ -132,6 +133,20 @@ size_t hk_run_outputs(const hk_run* r, uint64_t* out, size_t cap) {
             w.push_back(v.size());
             w.insert(w.end(), v.begin(), v.end());
         }
+    }
+    for (size_t i = 0; i < w.size() && i < cap; ++i) out[i] = w[i];
+    return w.size();
+}
+
+size_t hk_run_call_outputs(const hk_run* r, uint64_t* out, size_t cap) {
+    if (!r) return 0;
+    std::vector<uint64_t> w;
+    w.push_back(r->m.call_outputs.size());
+    for (const auto& [cid, toks] : r->m.call_outputs) {
+        w.push_back(static_cast<uint64_t>(cid.op));
+        w.push_back(static_cast<uint64_t>(cid.query));
+        w.push_back(toks.size());
+        w.insert(w.end(), toks.begin(), toks.end());
     }
     for (size_t i = 0; i < w.size() && i < cap; ++i) out[i] = w[i];
     return w.size();

@@ -49,6 +49,26 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
     }
     if (total != plan.leaves.size()) throw std::runtime_error("simulate: schedule does not cover all calls");
 
+    // One-worker mode (one process per GPU): this process runs only worker
+    // `only` of the schedule. Exact whenever no call of that worker waits on a
+    // call of another worker (then its timeline is independent of the others).
+    const int only = opts.only_worker;
+    if (only >= static_cast<int>(W)) throw std::runtime_error("simulate: only_worker out of range");
+    if (only >= 0) {
+        std::map<CallId, int> wof;
+        for (std::size_t w = 0; w < W; ++w)
+            for (const CallId& c : plan.sigma[w]) wof[c] = static_cast<int>(w);
+        total = plan.sigma[static_cast<std::size_t>(only)].size();
+        for (const CallId& c : plan.sigma[static_cast<std::size_t>(only)])
+            for (int p : plan.tree[static_cast<std::size_t>(plan.leaf(c.op, c.query))].preds) {
+                const TreeNode& pn = plan.tree[static_cast<std::size_t>(p)];
+                if (wof[CallId{pn.op, pn.query}] != only)
+                    throw std::runtime_error(
+                        "simulate: only_worker mode cannot serve a cross-worker dependency (run all workers)");
+            }
+    }
+    auto active = [&](std::size_t w) { return only < 0 || static_cast<int>(w) == only; };
+
     Evaluator ev(plan, cfg.seed, cfg.stochastic, /*strict_llm=*/true);
 
     SimMetrics m;
@@ -61,13 +81,13 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
     for (std::size_t w = 0; w < W; ++w) {
         const SimWorkerConfig& wc = cfg.workers[w];
         caches.push_back(std::make_unique<KvTree>(wc.capacity, wc.block));
-        pools.push_back(std::make_unique<PagePool>(paged ? body.pages_per_worker(static_cast<int>(w)) : 0));
+        pools.push_back(std::make_unique<PagePool>(paged && active(w) ? body.pages_per_worker(static_cast<int>(w)) : 0));
         if (paged) {
             caches[w]->set_page_pool(pools[w].get());
             caches[w]->journaling = body.device_lookup();
         }
         budgets[w] = wc.prefill_budget > 0 ? wc.prefill_budget : std::max<std::size_t>(wc.capacity / 8, wc.block);
-        if (cfg.proactive_pin) {
+        if (cfg.proactive_pin && active(w)) {
             const auto budget = static_cast<std::size_t>(cfg.pin_capacity_frac * static_cast<double>(wc.capacity));
             std::vector<TokenSeq> pins = static_pin_prefixes(plan, static_cast<int>(w), wc.block, cfg.pin_threshold, budget);
             std::vector<std::vector<int>> pin_pages;
@@ -126,6 +146,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
         body.begin_iteration(iter, completing);
 
         for (std::size_t w = 0; w < W; ++w) {
+            if (!active(w)) continue;
             KvTree& cache = *caches[w];
             PagePool* pool = paged ? pools[w].get() : nullptr;
             if (pool) pool->flush_deferred();
@@ -295,6 +316,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                 TokenSeq out = lc.out_len > 0 ? body.take_output(static_cast<int>(w), lc, len_out, det) : TokenSeq{};
                 if (out.size() != lc.out_len) throw std::logic_error("simulate: output length drifted from plan");
                 ev.put_llm_output(lc.id.op, static_cast<std::size_t>(lc.id.query), out);
+                m.call_outputs[lc.id] = out;
                 TokenSeq full = lc.prompt;
                 full.insert(full.end(), out.begin(), out.end());
                 cache.insert(full.data(), full.size(), full.size(), false, 0,
@@ -330,7 +352,19 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
     m.hit_rate_pct = m.prompt_tokens > 0
                          ? 100.0 * static_cast<double>(m.cache_served_tokens) / static_cast<double>(m.prompt_tokens)
                          : 0.0;
-    m.outputs = ev.output_values();
+    if (only < 0) {
+        m.outputs = ev.output_values();
+    } else {
+        // one-worker mode: only outputs whose llm calls all ran here
+        for (NodeId id : plan.outputs) {
+            try {
+                std::vector<TokenSeq> vals;
+                for (std::size_t b = 0; b < plan.batch; ++b) vals.push_back(ev.value(id, b));
+                m.outputs[id] = std::move(vals);
+            } catch (const std::runtime_error&) {
+            }
+        }
+    }
     return m;
 }
 

@@ -287,6 +287,7 @@ struct SimMetrics {
     std::vector<SimIterRow> trace;
     std::map<NodeId, std::vector<TokenSeq>> outputs;
     // B200 additions (not part of the reference report)
+    std::map<CallId, TokenSeq> call_outputs;        // every llm call's generated tokens
     std::vector<std::uint64_t> pin_compute_tokens;  // per worker, pin precompute prefill
     std::uint64_t recompute_tokens = 0;             // fully-cached prompts: last position re-run
     double pin_seconds = 0, iter_seconds = 0;       // wall time: pin precompute, iteration loop

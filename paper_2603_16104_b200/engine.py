@@ -120,6 +120,11 @@ class Engine:
         _lib.check_status(rc, "hk_generate")
         return (out[:n_new], logits) if want_logits else out[:n_new]
 
+    def stats(self) -> dict:
+        s = _lib.EngineStatsC()
+        _lib.check_status(_lib.load().hk_engine_stats_get(self.handle, C.byref(s)), "hk_engine_stats_get")
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
     def profile(self, enable: bool = True):
         _lib.check_status(_lib.load().hk_engine_profile(self.handle, int(enable)), "hk_engine_profile")
 

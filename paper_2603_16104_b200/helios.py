@@ -116,6 +116,7 @@ class SimMetrics:
     pin_compute_tokens: List[int] = field(default_factory=list)
     pin_seconds: float = 0.0
     iter_seconds: float = 0.0
+    call_outputs: Dict[tuple, List[int]] = field(default_factory=dict)
 
 
 def _report(h, which: int) -> str:
@@ -154,18 +155,35 @@ def _outputs(h) -> Dict[int, List[List[int]]]:
     return out
 
 
-def simulate(plan: bytes, cfg: SimConfig, engine=None, verify_lookup: bool = False) -> SimMetrics:
+def _call_outputs(h) -> Dict[tuple, List[int]]:
+    lib = _lib.load()
+    n = lib.hk_run_call_outputs(h, None, 0)
+    buf = np.zeros(max(n, 1), dtype=np.uint64)
+    lib.hk_run_call_outputs(h, buf.ctypes.data_as(_lib.u64p), n)
+    w = buf[:n].tolist()
+    out, i = {}, 1
+    for _ in range(w[0]):
+        op, q, ln = int(np.int64(np.uint64(w[i]))), int(w[i + 1]), w[i + 2]
+        out[(op, q)] = w[i + 3:i + 3 + ln]
+        i += 3 + ln
+    return out
+
+
+def simulate(plan: bytes, cfg: SimConfig, engine=None, verify_lookup: bool = False,
+             only_worker: int = -1) -> SimMetrics:
     """simulate() (simulator.hpp:128-130) on a flattened HKPLAN01 plan.
 
     engine=None runs the synthetic LLM body (reference mode S); an Engine runs
-    the device transformer (mode T). Raises RuntimeError with the reference's
-    messages ("simulate: ...") on invalid schedules/configs.
+    the device transformer (mode T). only_worker >= 0 runs one worker of the
+    schedule (one process per GPU; exact when that worker has no cross-worker
+    dependency). Raises RuntimeError with the reference's messages
+    ("simulate: ...") on invalid schedules/configs.
     """
     lib = _lib.load()
     buf = (C.c_uint8 * len(plan)).from_buffer_copy(plan)
     c = cfg.to_c()
-    h = lib.hk_simulate(buf, len(plan), C.byref(c), engine.handle if engine is not None else None,
-                        1 if verify_lookup else 0)
+    flags = (1 if verify_lookup else 0) | ((only_worker + 1) << 8)
+    h = lib.hk_simulate(buf, len(plan), C.byref(c), engine.handle if engine is not None else None, flags)
     if not h:
         raise RuntimeError(_lib.last_error())
     try:
@@ -179,7 +197,8 @@ def simulate(plan: bytes, cfg: SimConfig, engine=None, verify_lookup: bool = Fal
             hit_rate_pct=mc.hit_rate_pct, calls=mc.calls, pinned_tokens=_worker_stat(h, 0),
             evicted_tokens=_worker_stat(h, 1), outputs=_outputs(h), metrics_json=_report(h, 0),
             calls_csv=_report(h, 1), trace_csv=_report(h, 2), recompute_tokens=mc.recompute_tokens,
-            pin_compute_tokens=_worker_stat(h, 2), pin_seconds=t[0], iter_seconds=t[1])
+            pin_compute_tokens=_worker_stat(h, 2), pin_seconds=t[0], iter_seconds=t[1],
+            call_outputs=_call_outputs(h))
     finally:
         lib.hk_run_free(h)
 

@@ -87,6 +87,8 @@ def main():
         wf, i, p, s = wl.c2_per_gpu(n)
         emit(f"c2x{n}", wf, i, p, s, f"configs[1] weak-scaled: {n} ops x 64 branches, one per GPU",
              full_outputs=False)
+    wf, i, p, s = wl.c2_branches(decode=8)
+    emit("c2_short", wf, i, p, s, "configs[1] with 8 decode tokens (profiling / launch lists)", full_outputs=False)
     # reduced-size model-mode cases (fit the CPU transformer oracle)
     wf, i, p, s = wl.c2_branches(n_branches=4, prefix_words=94, decode=8, capacity=4096, budget=64)
     emit("t_small", wf, i, p, dict(s, pin_threshold=32), "4 branches x 96-token prefix, 8 decode")

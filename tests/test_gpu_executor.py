@@ -77,9 +77,12 @@ def test_executor_device_matches_reference_control_plane_and_oracle_tokens(name)
 
 
 def test_executor_c1_dependencies_match_python_oracle_in_model_mode():
-    """c1: 4 map calls feed a reducer; the reducer's prompt contains generated
-    tokens, so metrics depend on the model. Compare against oracle.simulate
-    driven by the oracle decoder."""
+    """c1: 4 map calls feed a reducer whose prompt contains generated tokens.
+    The Python restatement of simulate() replays the run with the GPU's call
+    outputs as its LLM body; every call's output is checked token by token
+    against the oracle decoder on exactly the prompt the executor built
+    (teacher-forced; only near-ties of the oracle's top two may differ), and
+    the control plane and workflow outputs must then agree exactly."""
     blob, meta = wl.load_plan("c1")
     sc = wl.sim_config_from_meta(meta)
     eng = make_engine(sc)
@@ -87,16 +90,28 @@ def test_executor_c1_dependencies_match_python_oracle_in_model_mode():
     eng.close()
     dec = decoder(TINY)
     V = TINY.vocab
+    exact = total = 0
 
-    def body(prompt, out_len, len_out, det):
-        ids, _ = dec.generate([t % V for t in prompt], out_len)
-        return [osim.gen_token(v, V) for v in ids]
+    def body(prompt, out_len, len_out, det, call):
+        nonlocal exact, total
+        gpu = m.call_outputs[call]
+        assert len(gpu) == out_len
+        gids = [t % V for t in gpu]
+        ref, logits = dec.generate([t % V for t in prompt], out_len, forced=gids)
+        for k in range(out_len):
+            total += 1
+            if ref[k] == gids[k]:
+                exact += 1
+            else:
+                assert top2_margin(logits[k]) < 0.04 * np.abs(logits[k]).max(), (call, k)
+        return gpu
 
     p = osim.parse_plan(blob)
     om, calls, trace, outs, _ = osim.simulate(p, osim.SimCfg.from_meta(meta["sim"]), body=body)
     assert m.calls_csv == osim.calls_csv(calls)
     assert json.loads(m.metrics_json)["cache_served_tokens"] == om["cache_served_tokens"]
     assert {k: v for k, v in m.outputs.items()} == {k: v for k, v in outs.items()}
+    assert exact >= total - 2, (exact, total)
 
 
 @pytest.mark.parametrize("name", ["c5", "c4_w1", "c2_nopin"])

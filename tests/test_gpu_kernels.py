@@ -65,6 +65,43 @@ def test_gemm_splitk_bias_and_residual(splits):
     assert (resid - (ref + 1)).abs().max().item() / scale < 1e-4
 
 
+@pytest.mark.parametrize("T", [1, 64, 300])
+def test_gemm_swiglu_epilogue(T):
+    lib = _lib.load()
+    F, K = 512, 256
+    g = torch.Generator(device="cuda").manual_seed(T)
+    Wg = (torch.rand(F, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) * 0.1
+    Wu = (torch.rand(F, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) * 0.1
+    # physical layout: per 128-row tile, 64 gate rows then the matching 64 up rows
+    W = torch.cat([Wg.view(F // 64, 64, K), Wu.view(F // 64, 64, K)], dim=1).reshape(2 * F, K).contiguous()
+    X = (torch.rand(T, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    gg, uu = X.float() @ Wg.float().t(), X.float() @ Wu.float().t()
+    ref = gg * torch.sigmoid(gg) * uu
+    out = torch.zeros(T, F, device="cuda", dtype=torch.bfloat16)
+    assert lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(out), 2 * F, K, T, 4, None, 0, None) == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    assert (out.float() - ref).abs().max().item() / ref.abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("T", [1, 64])
+def test_gemm_argmax_epilogue(T):
+    lib = _lib.load()
+    V, K = 4096, 256
+    g = torch.Generator(device="cuda").manual_seed(T + 1)
+    W = (torch.rand(V, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    X = (torch.rand(T, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    logits = torch.zeros(T, V, device="cuda")
+    assert lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(logits), V, K, T, 2, None, 1, None) == 0
+    part = torch.zeros(V // 128, T, 2, device="cuda")
+    assert lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(part), V, K, T, 5, None, 0, None) == 0
+    torch.cuda.synchronize()
+    lv = logits.view(T, V // 128, 128)
+    mx, ix = lv.max(dim=-1)
+    assert torch.equal(part[..., 0].t(), mx)
+    idx = part[..., 1].contiguous().view(torch.int32).t()
+    assert torch.equal(idx.long(), ix + torch.arange(V // 128, device="cuda") * 128)
+
+
 def test_gemm_deterministic():
     lib = _lib.load()
     N, K, T = 4096, 4096, 64

@@ -361,6 +361,40 @@ def test_simulate_validation_errors():
         helios.simulate(b"\0" * 64, helios.SimConfig(workers=[helios.SimWorkerConfig()]))
 
 
+@pytest.mark.parametrize("name,W", [("c2p_w2", 2), ("c4_w4", 4), ("c2x4", 4)])
+def test_only_worker_slices_equal_the_full_run(name, W):
+    """One-worker mode (one process per GPU) reproduces each worker's call rows
+    of the full multi-worker run when workers are independent."""
+    blob, meta = wl.load_plan(name)
+    gold = json.loads((GOLD / f"{name}.ref.json").read_text())
+    rows = gold["calls_csv"].strip().split("\n")[1:]
+    sc = wl.sim_config_from_meta(meta)
+    total_decode = 0
+    iters = 0
+    for w in range(W):
+        m = helios.simulate(blob, sc, only_worker=w)
+        mine = m.calls_csv.strip().split("\n")[1:]
+        assert mine == [r for r in rows if r.split(",")[2] == str(w)]
+        total_decode += m.decode_tokens
+        iters = max(iters, m.iterations)
+    gm = json.loads(gold["metrics_json"])
+    assert total_decode == gm["decode_tokens"] and iters == gm["iterations"]
+
+
+@needs_ref
+def test_only_worker_rejects_cross_worker_dependencies():
+    from oracle import refpy
+    b = wl.WB()
+    a = b.llm([wl.sys_msg("writer"), wl.user_msg(["go"])], 3)
+    c = b.llm([wl.sys_msg("writer"), wl.user_msg([a])], 3)
+    b.output(c)
+    _, blob = refpy.run(b.workflow(), {}, b.profile, {"workers": 2, "worker_of": {str(a): 0, str(c): 1},
+                                                      "sigma": [[[a, 0]], [[c, 0]]], "skip_sim": True})
+    sc = helios.SimConfig(workers=[helios.SimWorkerConfig()] * 2)
+    with pytest.raises(RuntimeError, match="cross-worker dependency"):
+        helios.simulate(blob, sc, only_worker=1)
+
+
 # ------------------------------------------------------------ C-ABI surface
 def test_cabi_exports_every_declared_symbol():
     header = "".join(h.read_text() for h in sorted((ROOT / "include").glob("*.h")))
