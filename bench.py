@@ -209,7 +209,7 @@ def main():
     if not args.no_profile:
         eng.profile(True)
         one_run()
-        for fam in ("gemm", "attn_shared", "attn_prefill", "attn_merge", "small", "trie"):
+        for fam in ("gemm", "attn_shared", "attn_private", "attn_prefill", "attn_merge", "small", "trie"):
             ms, n, b = eng.kernel_ms(fam)
             prof[fam] = {"ms": ms, "launches": n, "bytes": b}
         prof_stats = eng.stats()
@@ -245,12 +245,16 @@ def main():
                             "frac": gemm_ach / hbm if gemm_ach else None,
                             "traffic": None, "peak_source": peak_src,
                             "share_of_step": g["ms"] / (prof_stats["pin_ms"] + prof_stats["iter_ms"])}
-        a = prof["attn_shared"]
-        if a["ms"] > 0:
-            ach = a["bytes"] / (a["ms"] / 1e3) / 1e9
-            line["attention_roofline"] = {"bound": "hbm", "kernel": "attn_mma_kernel (prefix-shared decode)",
-                                          "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                                          "traffic": None, "peak_source": peak_src}
+        # prefix-shared decode attention = shared-prefix items + private-suffix items + merge
+        a_ms = prof["attn_shared"]["ms"] + prof["attn_private"]["ms"] + prof["attn_merge"]["ms"]
+        a_b = prof["attn_shared"]["bytes"] + prof["attn_private"]["bytes"]
+        if a_ms > 0:
+            ach = a_b / (a_ms / 1e3) / 1e9
+            line["attention_roofline"] = {
+                "bound": "hbm", "kernel": "attn_mma_kernel<64,4> shared + attn_mma_kernel<32,3> private + merge",
+                "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                "peak_source": peak_src, "algorithmic_bytes_per_step": a_b / max(1, prof_stats["steps"]) * 0 + a_b,
+                "note": "bytes = shared-prefix KV once per group + private KV + Q/O, per layer, summed over the run"}
         line["kernel_ms_per_step"] = {k: v["ms"] for k, v in prof.items()}
     if not args.no_cpu_baseline:
         from oracle.cpu_sample import decode_step_sample

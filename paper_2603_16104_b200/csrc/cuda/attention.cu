@@ -88,9 +88,11 @@ __device__ __forceinline__ void load_tile(uint32_t sK, uint32_t sV, const bf16* 
     }
 }
 
-template <int TK>
+template <int TK, int STAGES>
 __global__ void __launch_bounds__(256) attn_mma_kernel(AttnArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
+    pdl_trigger();
+    pdl_wait();
     const AttnItem it = a.items[blockIdx.x];
     const int G = a.H / a.Hkv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -107,8 +109,12 @@ __global__ void __launch_bounds__(256) attn_mma_kernel(AttnArgs a) {
     const uint32_t sbase = smem_u32(smem);  // [stage][K|V] tiles
 
     const int n_tiles = it.kend > it.kbeg ? (it.kend - it.kbeg + TK - 1) / TK : 0;
-    if (n_tiles > 0) {
-        load_tile<TK>(sbase, sbase + TILE, kv, pages, it.kbeg, it.kend, head_off, page_stride, kv_half);
+    // STAGES-deep cp.async ring; one commit group per tile slot (possibly empty)
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < n_tiles)
+            load_tile<TK>(sbase + s * 2 * TILE, sbase + s * 2 * TILE + TILE, kv, pages, it.kbeg + s * TK, it.kend,
+                          head_off, page_stride, kv_half);
         cp_async_commit();
     }
 
@@ -140,16 +146,15 @@ __global__ void __launch_bounds__(256) attn_mma_kernel(AttnArgs a) {
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
     for (int ti = 0; ti < n_tiles; ++ti) {
-        const uint32_t sK = sbase + (ti & 1) * 2 * TILE;
+        const uint32_t sK = sbase + (ti % STAGES) * 2 * TILE;
         const uint32_t sV = sK + TILE;
-        if (ti + 1 < n_tiles) {
-            const uint32_t nK = sbase + ((ti + 1) & 1) * 2 * TILE;
-            load_tile<TK>(nK, nK + TILE, kv, pages, it.kbeg + (ti + 1) * TK, it.kend, head_off, page_stride, kv_half);
-            cp_async_commit();
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
+        const int nt = ti + STAGES - 1;
+        if (nt < n_tiles) {
+            const uint32_t nK = sbase + (nt % STAGES) * 2 * TILE;
+            load_tile<TK>(nK, nK + TILE, kv, pages, it.kbeg + nt * TK, it.kend, head_off, page_stride, kv_half);
         }
+        cp_async_commit();
+        cp_async_wait<STAGES - 1>();
         __syncthreads();
         const int kt0 = it.kbeg + ti * TK;
 
@@ -326,6 +331,8 @@ __global__ void attn_simt_f32_kernel(AttnArgs a) {
 __global__ void attn_merge_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
                                   const int32_t* __restrict__ n_parts, int n_rows, int tok0, int H, int max_parts,
                                   void* out, bool f32) {
+    pdl_trigger();
+    pdl_wait();
     const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (wid >= n_rows * H) return;
@@ -359,15 +366,15 @@ __global__ void attn_merge_kernel(const float* __restrict__ part_o, const float2
     }
 }
 
-template <int TK>
+template <int TK, int STAGES>
 void launch_mma(const AttnArgs& a, int warps, cudaStream_t st) {
-    constexpr int smem = 4 * TK * HD * 2;  // 2 stages x (K + V)
+    constexpr int smem = STAGES * 2 * TK * HD * 2;  // STAGES x (K + V)
     static bool configured = false;
     if (!configured) {
-        HK_CUDA(cudaFuncSetAttribute(attn_mma_kernel<TK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        HK_CUDA(cudaFuncSetAttribute(attn_mma_kernel<TK, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         configured = true;
     }
-    attn_mma_kernel<TK><<<a.n_items, warps * 32, smem, st>>>(a);
+    launch_pdl(attn_mma_kernel<TK, STAGES>, dim3(a.n_items), dim3(warps * 32), smem, st, a);
 }
 
 }  // namespace
@@ -381,9 +388,9 @@ void attention_partial(const AttnArgs& a, cudaStream_t st) {
         if (a.block != BLK) throw std::runtime_error("attention: KV page size must be 16 tokens");
         if (G > 16) throw std::runtime_error("attention: GQA group > 16 unsupported");
         if (a.single)
-            launch_mma<32>(a, (G + 15) / 16, st);
+            launch_mma<32, 3>(a, (G + 15) / 16, st);  // 48 KB: 4 CTAs/SM
         else
-            launch_mma<64>(a, G, st);
+            launch_mma<64, 4>(a, G, st);              // 128 KB: deep ring for long shared ranges
     }
     HK_LAUNCHED(1);
 }
@@ -393,8 +400,8 @@ void attention_merge(const float* part_o, const float2* part_ml, const int32_t* 
     if (n_rows == 0) return;
     if (hd != HD) throw std::runtime_error("attention: head_dim must be 128");
     const int warps = n_rows * H;
-    attn_merge_kernel<<<(warps + 7) / 8, 256, 0, st>>>(part_o, part_ml, n_parts, n_rows, tok0, H, max_parts, out,
-                                                       f32);
+    launch_pdl(attn_merge_kernel, dim3((warps + 7) / 8), dim3(256), 0, st, part_o, part_ml, n_parts, n_rows, tok0, H,
+               max_parts, out, f32);
     HK_LAUNCHED(1);
 }
 

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <functional>
 #include <numeric>
+#include <map>
 #include <unordered_map>
 
 #include "common.cuh"
@@ -155,6 +156,22 @@ struct hk_engine {
     static constexpr int kMetaRing = 4;
     Meta meta[kMetaRing];
     int meta_next = 0;
+    int32_t* meta_dev = nullptr;
+    size_t meta_dev_cap = 0;
+
+    // CUDA graphs of repeated step shapes (decode iterations): key = step signature
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        unsigned long long launches = 0;
+    };
+    std::map<std::vector<int64_t>, GraphEntry> graphs;
+    std::map<std::vector<int64_t>, int> graph_seen;
+    bool use_graphs = true;
+    void drop_graphs() {
+        for (auto& [k, g] : graphs) cudaGraphExecDestroy(g.exec);
+        graphs.clear();
+        graph_seen.clear();
+    }
     // trie staging
     uint64_t* tok_d = nullptr;
     size_t tok_cap = 0;
@@ -267,6 +284,8 @@ hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m
     if (c.block_tokens == 0 || c.pages_per_worker == 0 || c.n_workers == 0)
         throw std::runtime_error("engine: bad engine config");
     HK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    use_graphs = std::getenv("HK_NO_GRAPHS") == nullptr;
+    hkd::g_pdl = std::getenv("HK_NO_PDL") == nullptr;
     init_weights();
 
     // rope table (cos, sin) computed in double, stored fp32 — shared with the oracle
@@ -349,11 +368,12 @@ hk_engine::~hk_engine() {
                     static_cast<void*>(part_ml), static_cast<void*>(tok_d), static_cast<void*>(match_d),
                     static_cast<void*>(pbuf), hs, static_cast<void*>(amax)})
         cudaFree(p);
+    drop_graphs();
     for (Meta& mt : meta) {
-        cudaFree(mt.d);
         if (mt.h) cudaFreeHost(mt.h);
         if (mt.done) cudaEventDestroy(mt.done);
     }
+    cudaFree(meta_dev);
     for (int32_t* b : host_bufs) cudaFreeHost(b);
     cudaStreamDestroy(st);
 }
@@ -577,14 +597,21 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     if (mt.done) HK_CUDA(cudaEventSynchronize(mt.done));  // this slot's previous step has consumed it
     else HK_CUDA(cudaEventCreateWithFlags(&mt.done, cudaEventDisableTiming));
     if (words > mt.cap) {
-        cudaFree(mt.d);
         if (mt.h) cudaFreeHost(mt.h);
         mt.cap = words * 2;
-        mt.d = dalloc<int32_t>(mt.cap);
         HK_CUDA(cudaMallocHost(&mt.h, mt.cap * sizeof(int32_t)));
     }
+    // One device metadata buffer for every step (stream order protects it), so
+    // a captured step graph can be replayed with fresh metadata.
+    if (words > meta_dev_cap) {
+        HK_CUDA(cudaStreamSynchronize(st));
+        cudaFree(meta_dev);
+        meta_dev_cap = words * 2;
+        meta_dev = dalloc<int32_t>(meta_dev_cap);
+        drop_graphs();
+    }
     int32_t* meta_h = mt.h;
-    int32_t* meta_d = mt.d;
+    int32_t* meta_d = meta_dev;
     size_t o = 0;
     auto put = [&](const int32_t* src, size_t n) {
         std::memcpy(meta_h + o, src, n * 4);
@@ -593,11 +620,13 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         o = (o + 3) & ~size_t(3);  // 16B alignment for items
         return at;
     };
+    // layout: every section before `pages` depends only on the step's shape, so a
+    // repeated shape (decode) keeps identical device pointers (CUDA graph replay)
     const size_t o_ids = put(ids.data(), T), o_pos = put(pos.data(), T), o_slots = put(slots.data(), T),
-                 o_kvw = put(kvw.data(), T), o_ptab = put(ptab.data(), T), o_pages = put(pages.data(), pages.size()),
+                 o_kvw = put(kvw.data(), T), o_ptab = put(ptab.data(), T),
                  o_np = put(nparts.data(), nparts.size()), o_sr = put(srows.data(), S), o_ss = put(sslots.data(), S),
                  o_items = put(reinterpret_cast<const int32_t*>(items.data()), n_items * sizeof(hkd::AttnItem) / 4),
-                 o_cmap = put(cmap.data(), cmap.size());
+                 o_cmap = put(cmap.data(), cmap.size()), o_pages = put(pages.data(), pages.size());
     HK_CUDA(cudaMemcpyAsync(meta_d, meta_h, o * 4, cudaMemcpyHostToDevice, st));
     stats.h2d_bytes += o * 4;
     stats.steps += 1;
@@ -621,6 +650,8 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
 
     const float eps = mc.rms_eps;
     const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
+    // the step's kernel sequence (eager, or recorded once into a CUDA graph)
+    auto enqueue = [&]() {
     int ck = clock.begin(5, st);
     hkd::embed(embed, f32, d, d_ids, d_slots, wk.slot_last, T, x, st);
     hkd::add_rmsnorm(nullptr, 0, x, layers[0].attn_norm, f32, T, d, eps, h, nullptr, nullptr, st);
@@ -693,6 +724,38 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
             hkd::argmax_reduce(amax, (V + 127) / 128, S, sample_ids, d_ss, wk.slot_last, st);
             clock.end(ck, st);
         }
+    }
+    };  // enqueue
+
+    const bool graphable = use_graphs && !clock.enabled && !logits_out_host && !f32;
+    if (graphable) {
+        // everything the recorded kernels depend on besides metadata contents
+        const std::vector<int64_t> sig{w, T, S, T_pre, n_multi, static_cast<int64_t>(n_items),
+                                       static_cast<int64_t>(dec.size()), static_cast<int64_t>(o_pages)};
+        auto it = graphs.find(sig);
+        if (it != graphs.end()) {
+            HK_CUDA(cudaGraphLaunch(it->second.exec, st));
+            hkd::g_launches += it->second.launches;
+        } else if (graph_seen[sig]++ >= 1) {
+            // second occurrence of this shape: record it once, replay from now on
+            const unsigned long long l0 = hkd::g_launches;
+            cudaGraph_t g;
+            HK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            enqueue();
+            HK_CUDA(cudaStreamEndCapture(st, &g));
+            GraphEntry ge;
+            HK_CUDA(cudaGraphInstantiate(&ge.exec, g, 0));
+            HK_CUDA(cudaGraphDestroy(g));
+            ge.launches = hkd::g_launches - l0;
+            HK_CUDA(cudaGraphLaunch(ge.exec, st));
+            graphs[sig] = ge;
+        } else {
+            enqueue();
+        }
+    } else {
+        enqueue();
+    }
+    if (S > 0) {
         if (logits_out_host)
             HK_CUDA(cudaMemcpyAsync(logits_out_host, logits, static_cast<size_t>(S) * V * 4, cudaMemcpyDeviceToHost, st));
         // harvest ring: D2H of the sampled ids into pinned memory

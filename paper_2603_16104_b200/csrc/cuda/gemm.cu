@@ -11,11 +11,16 @@
 // thread issues tcgen05.mma into a TMEM accumulator; all four warps drain TMEM
 // with tcgen05.ld in the epilogue. Split-K (grid.z) covers skinny decode
 // GEMMs; partials are reduced deterministically by splitk_reduce.
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace hkd {
 
@@ -32,6 +37,7 @@ struct GemmParams {
     int ldo;
     const bf16* bias;
     float* partial;
+    int cluster;  // 1: the grid.z split-K CTAs form a cluster and reduce through DSMEM
 };
 
 template <int BN, int STAGES>
@@ -73,11 +79,21 @@ __global__ void __launch_bounds__(128, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    pdl_trigger();  // let the next kernel of the chain get scheduled (it prefetches its own weights)
     if (warp == 0) {
         if (lane == 0) {
             const uint64_t pol_w = policy_evict_first();
             const uint64_t pol_x = policy_evict_last();
-            for (int i = 0; i < nkb; ++i) {
+            // Weights do not depend on the previous kernel: start streaming the
+            // first stages before waiting for the activations (PDL overlap).
+            const int pre = min(STAGES, nkb);
+            for (int i = 0; i < pre; ++i) {
+                mbar_expect_tx(&full[i], A_BYTES + B_BYTES);
+                tma_load_2d_hint(sA + i * A_BYTES, &tmW, &full[i], (kb0 + i) * BK, m0, pol_w);
+            }
+            pdl_wait();
+            for (int i = 0; i < pre; ++i) tma_load_2d_hint(sB + i * B_BYTES, &tmX, &full[i], (kb0 + i) * BK, n0, pol_x);
+            for (int i = pre; i < nkb; ++i) {
                 const int s = i % STAGES;
                 mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
                 mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
@@ -110,10 +126,75 @@ __global__ void __launch_bounds__(128, 1)
     mbar_wait(done, 0);
     __syncwarp();
     tc_fence_after();
+    pdl_wait();  // (already satisfied) predecessor writes are visible to the epilogue
     const int row = warp * 32 + lane;
     const int m = m0 + row;
     const bool m_ok = m < p.N;
-    if (p.epi == kEpiSwiGLU) {
+    if (p.cluster) {
+        // Split-K reduction inside the cluster: every CTA parks its fp32 tile
+        // (column-major [BN][128]) in its own smem; CTA rank r then sums rows
+        // [r*128/s, (r+1)*128/s) over all s peers through DSMEM in rank order
+        // (deterministic) and applies the epilogue once. No HBM partials.
+        float* tile = reinterpret_cast<float*>(smem);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 8) {
+            float v[8];
+            tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) tile[(c + j) * BM + row] = v[j];
+        }
+        cluster_sync_all();
+        const int s = static_cast<int>(gridDim.z);
+        const int rank = static_cast<int>(cluster_ctarank());
+        const int per = ((BM + s - 1) / s + 3) & ~3;  // rows per rank, multiple of 4 (float4)
+        const int r0 = min(BM, rank * per), r1 = min(BM, r0 + per);
+        const int nq = (r1 - r0) / 4;                  // float4 row groups
+        const float4* peer[8];
+        cg::cluster_group cl = cg::this_cluster();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) peer[q] = reinterpret_cast<const float4*>(cl.map_shared_rank(tile, q < s ? q : 0));
+        for (int idx = threadIdx.x; idx < nq * BN; idx += blockDim.x) {
+            const int rr = r0 + 4 * (idx % nq), c = idx / nq;
+            const int off4 = (c * BM + rr) / 4;
+            float4 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < s) v[q] = peer[q][off4];  // all peers' loads in flight together
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < s) {  // fixed rank order: deterministic sum
+                    acc[0] += v[q].x;
+                    acc[1] += v[q].y;
+                    acc[2] += v[q].z;
+                    acc[3] += v[q].w;
+                }
+            const int n = n0 + c;
+            if (n >= p.T) continue;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int mm = m0 + rr + e;
+                if (mm >= p.N) continue;
+                float r = acc[e];
+                if (p.bias && p.epi != kEpiPartial) r += bf2f(p.bias[mm]);
+                switch (p.epi) {
+                    case kEpiStoreBf16:
+                        static_cast<bf16*>(p.out)[static_cast<size_t>(n) * p.ldo + mm] = f2bf(r);
+                        break;
+                    case kEpiAddF32:
+                        static_cast<float*>(p.out)[static_cast<size_t>(n) * p.ldo + mm] += r;
+                        break;
+                    case kEpiStoreF32:
+                        static_cast<float*>(p.out)[static_cast<size_t>(n) * p.ldo + mm] = r;
+                        break;
+                    default:
+                        p.partial[static_cast<size_t>(n) * p.N + mm] = r;
+                        break;
+                }
+            }
+        }
+        cluster_sync_all();  // peers keep their smem until every rank has read it
+    } else if (p.epi == kEpiSwiGLU) {
         // TMEM lanes 0-63 hold gate rows, 64-127 the matching up rows (warp w
         // may only read lanes 32w..32w+31): up values go through smem.
         float* xs = reinterpret_cast<float*>(smem);  // [64][BN + 1], pipeline buffers are free now
@@ -178,7 +259,7 @@ __global__ void __launch_bounds__(128, 1)
     }
     const float bias = (p.bias && m_ok && p.epi != kEpiPartial) ? bf2f(p.bias[m]) : 0.f;
 #pragma unroll 1
-    for (int c = 0; c < BN && p.epi < kEpiSwiGLU; c += 8) {
+    for (int c = 0; c < BN && p.epi < kEpiSwiGLU && !p.cluster; c += 8) {
         float v[8];
         tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
         if (!m_ok) continue;
@@ -313,7 +394,24 @@ void launch_tc(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p
                                      static_cast<int>(sm)));
         configured = true;
     }
-    gemm_tc_kernel<BN, STAGES><<<grid, 128, sm, st>>>(tw, tx, p);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (p.cluster) {
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = 1;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = grid.z;
+        cfg.numAttrs = 2;
+    }
+    HK_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES>, tw, tx, p));
     HK_LAUNCHED(1);
 }
 
@@ -321,6 +419,7 @@ void launch_tc(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p
 
 int g_num_sms = 148;
 unsigned long long g_launches = 0;
+bool g_pdl = true;
 
 int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, const bf16* bias,
               float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits, int max_splits) {
@@ -345,30 +444,39 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
         splits = 1;  // epilogue needs the whole K reduction in TMEM
     } else if (force_splits > 0) {
         splits = force_splits;
-    } else if (mt * nt < g_num_sms * 3 / 4) {
-        splits = std::max(1, g_num_sms / (mt * nt));
+    } else {
+        // skinny (decode) GEMMs: split K across a thread-block cluster so that
+        // ~2 CTAs per SM stream weights; reduced through DSMEM (<= 8 per cluster)
+        const int slots = BN <= 64 ? 2 * g_num_sms : g_num_sms;
+        if (mt * nt * 2 <= slots) splits = std::min(8, slots / (mt * nt));
         splits = std::min(splits, std::max(1, kb / 4));
     }
     splits = std::min(splits, std::max(1, max_splits));
     int kbps = (kb + splits - 1) / splits;
     splits = (kb + kbps - 1) / kbps;  // no empty splits
-    if (epi != kEpiPartial && splits > 1 && static_cast<size_t>(splits) * T * N > workspace_floats) {
+    // DSMEM cluster reduction is kept behind a switch: measured slower on B200
+    // than L2-resident fp32 partials reduced by the consumer row kernel
+    // (profiles/r1_gemm_sweep.txt), so partials are the default.
+    static const bool use_cluster = std::getenv("HK_GEMM_CLUSTER") != nullptr;
+    const bool cluster = splits > 1 && splits <= 8 && use_cluster;
+    if (!cluster && epi != kEpiPartial && splits > 1 && static_cast<size_t>(splits) * T * N > workspace_floats) {
         splits = 1;
         kbps = kb;
     }
-    const bool via_ws = splits > 1 && epi != kEpiPartial;
+    const bool via_ws = splits > 1 && !cluster && epi != kEpiPartial;
     GemmParams p{N, K, T, kb, kbps, via_ws ? kEpiPartial : epi, out, ldo, bias,
-                 epi == kEpiPartial ? static_cast<float*>(out) : workspace};
+                 epi == kEpiPartial ? static_cast<float*>(out) : workspace, cluster ? 1 : 0};
     const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
     const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
     dim3 grid(mt, nt, splits);
     switch (BN) {
-        case 16: launch_tc<16, 8>(tw, tx, p, grid, st); break;
-        case 32: launch_tc<32, 8>(tw, tx, p, grid, st); break;
-        case 64: launch_tc<64, 8>(tw, tx, p, grid, st); break;
-        case 128: launch_tc<128, 6>(tw, tx, p, grid, st); break;
+        case 16: launch_tc<16, 4>(tw, tx, p, grid, st); break;
+        case 32: launch_tc<32, 4>(tw, tx, p, grid, st); break;
+        case 64: launch_tc<64, 4>(tw, tx, p, grid, st); break;
+        case 128: launch_tc<128, 4>(tw, tx, p, grid, st); break;
         default: launch_tc<256, 4>(tw, tx, p, grid, st); break;
     }
+    if (cluster) splits = 1;  // the result is already reduced
     if (via_ws) {
         const size_t total = static_cast<size_t>(T) * N;
         const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 4096));
@@ -381,6 +489,8 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
 namespace {
 __global__ void argmax_reduce_kernel(const float2* __restrict__ part, int n_tiles, int T, int32_t* ids,
                                      const int32_t* slots, int32_t* slot_last) {
+    pdl_trigger();
+    pdl_wait();
     const int t = blockIdx.x;
     float best = -INFINITY;
     int bi = 0x7fffffff;
@@ -423,7 +533,7 @@ __global__ void argmax_reduce_kernel(const float2* __restrict__ part, int n_tile
 void argmax_reduce(const float2* part, int n_tiles, int T, int32_t* ids, const int32_t* slots, int32_t* slot_last,
                    cudaStream_t st) {
     if (T <= 0) return;
-    argmax_reduce_kernel<<<T, 256, 0, st>>>(part, n_tiles, T, ids, slots, slot_last);
+    launch_pdl(argmax_reduce_kernel, dim3(T), dim3(256), 0, st, part, n_tiles, T, ids, slots, slot_last);
     HK_LAUNCHED(1);
 }
 

@@ -222,6 +222,8 @@ __global__ void swiglu_interleaved_kernel(const float* __restrict__ gu, int F, f
 // One thread per rotated pair (q and k heads) or per value pair (v heads).
 template <typename T>
 __global__ void qkv_rope_kv_kernel(QkvArgs a) {
+    pdl_trigger();
+    pdl_wait();
     const RopeArgs& r = a.r;
     const int t = blockIdx.y;
     const int half = r.hd / 2;
@@ -301,6 +303,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) add_rmsnorm_kernel(const float* __restrict__ part, int splits, float* x,
                                                           const T* __restrict__ w, int T_, int d, float eps, T* h,
                                                           const int32_t* __restrict__ cmap, T* hc) {
+    pdl_trigger();
+    pdl_wait();
     const int t = blockIdx.x;
     const int n4 = d / 4;
     float4 v[8];
@@ -376,9 +380,9 @@ void qkv_rope_kv(const QkvArgs& a, cudaStream_t st) {
     const int n = (a.r.H + a.r.Hkv) * half + a.r.Hkv * half;
     dim3 grid((n + 255) / 256, a.r.T);
     if (a.r.f32)
-        qkv_rope_kv_kernel<float><<<grid, 256, 0, st>>>(a);
+        launch_pdl(qkv_rope_kv_kernel<float>, grid, dim3(256), 0, st, a);
     else
-        qkv_rope_kv_kernel<bf16><<<grid, 256, 0, st>>>(a);
+        launch_pdl(qkv_rope_kv_kernel<bf16>, grid, dim3(256), 0, st, a);
     HK_LAUNCHED(1);
 }
 
@@ -387,11 +391,11 @@ void add_rmsnorm(const float* part, int splits, float* x, const void* w, bool f3
     if (!T) return;
     if (d % 4 || d > 8192) throw std::runtime_error("add_rmsnorm: d must be a multiple of 4 and <= 8192");
     if (f32)
-        add_rmsnorm_kernel<float><<<T, 256, 0, st>>>(part, splits, x, static_cast<const float*>(w), T, d, eps,
-                                                     static_cast<float*>(h), cmap, static_cast<float*>(hc));
+        launch_pdl(add_rmsnorm_kernel<float>, dim3(T), dim3(256), 0, st, part, splits, x, static_cast<const float*>(w),
+                   T, d, eps, static_cast<float*>(h), cmap, static_cast<float*>(hc));
     else
-        add_rmsnorm_kernel<bf16><<<T, 256, 0, st>>>(part, splits, x, static_cast<const bf16*>(w), T, d, eps,
-                                                    static_cast<bf16*>(h), cmap, static_cast<bf16*>(hc));
+        launch_pdl(add_rmsnorm_kernel<bf16>, dim3(T), dim3(256), 0, st, part, splits, x, static_cast<const bf16*>(w), T,
+                   d, eps, static_cast<bf16*>(h), cmap, static_cast<bf16*>(hc));
     HK_LAUNCHED(1);
 }
 

@@ -128,6 +128,30 @@ def test_executor_device_trie_and_evictions_at_config_scale(name):
     assert m.calls_csv == gold["calls_csv"]
 
 
+def test_graphs_and_pdl_do_not_change_results():
+    """CUDA-graph replay + programmatic dependent launch vs plain eager launches:
+    identical control plane and identical generated tokens (same kernels)."""
+    import subprocess
+    import sys
+    code = ("import json,sys; sys.path.insert(0,'.');"
+            "from paper_2603_16104_b200 import helios, workloads as wl;"
+            "from paper_2603_16104_b200.engine import TINY, Engine, EngineConfig, pages_for;"
+            "blob, meta = wl.load_plan('c5'); sc = wl.sim_config_from_meta(meta);"
+            "e = Engine(TINY, EngineConfig(pages_per_worker=pages_for(sc, 600, 1200), max_calls=600,"
+            " max_step_tokens=8704, max_ctx_tokens=12288));"
+            "m = helios.simulate(blob, sc, engine=e);"
+            "print(json.dumps({'m': m.metrics_json, 'o': {str(k): v for k, v in m.call_outputs.items()}}))")
+    outs = []
+    for env in ({}, {"HK_NO_GRAPHS": "1", "HK_NO_PDL": "1"}):
+        import os
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                           env={**os.environ, **env}, cwd=str(Path(__file__).resolve().parents[1]), timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().split("\n")[-1]))
+    assert outs[0]["m"] == outs[1]["m"]
+    assert outs[0]["o"] == outs[1]["o"]
+
+
 def test_executor_without_device_trie_matches_too():
     blob, meta = wl.load_plan("t_press")
     gold = json.loads((GOLD / "t_press.ref.json").read_text())
