@@ -473,7 +473,22 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     order.insert(order.end(), dec.begin(), dec.end());
 
     int T = 0;
-    for (int i : order) T += segs[i].count;
+    const int n_pages = static_cast<int>(ec.pages_per_worker);
+    for (int i : order) {
+        const SegIn& s = segs[i];
+        T += s.count;
+        // every page the step touches must exist: a bad table would silently
+        // read or overwrite another call's KV
+        const size_t need = static_cast<size_t>((s.start + s.count + block - 1) / block);
+        if (s.table->size() < need)
+            throw std::runtime_error("engine: block table shorter than the segment (" + std::to_string(s.table->size()) +
+                                     " pages for " + std::to_string(s.start + s.count) + " tokens)");
+        for (size_t k = 0; k < need; ++k)
+            if ((*s.table)[k] < 0 || (*s.table)[k] >= n_pages)
+                throw std::runtime_error("engine: page id out of range: " + std::to_string((*s.table)[k]));
+        if (s.slot >= static_cast<int>(ec.max_calls) || (!s.from_prompt && s.slot < 0))
+            throw std::runtime_error("engine: bad call slot");
+    }
     if (T == 0) return;
     if (T > maxT) throw std::runtime_error("engine: step exceeds max_step_tokens");
     const int T_pre = T - static_cast<int>(dec.size());
@@ -904,6 +919,7 @@ class DeviceBody : public LlmBody {
     }
     void begin_iteration(std::uint64_t, const std::vector<std::pair<int, LiveCall*>>&) override {
         e_->mark_pins_done();
+        for (std::size_t w = 0; w < finished_slots_.size(); ++w) release_slots(static_cast<int>(w));
     }
     bool uses_pages() const override { return true; }
     int pages_per_worker(int) const override { return static_cast<int>(e_->ec.pages_per_worker); }
@@ -950,6 +966,7 @@ class DeviceBody : public LlmBody {
             segs.push_back(in);
         }
         e_->step(pw(sp.worker), segs);
+        release_slots(sp.worker);
     }
     TokenSeq take_output(int w, LiveCall& lc, double, bool) override {
         auto& toks = e_->workers[static_cast<size_t>(pw(w))].slot_tokens[static_cast<size_t>(lc.slot)];
@@ -965,8 +982,12 @@ class DeviceBody : public LlmBody {
         return out;
     }
     void on_finish(int w, LiveCall& lc) override {
-        if (lc.slot >= 0) e_->free_slot(pw(w), lc.slot);
-        lc.slot = -1;
+        // The call's last decode token (it writes the KV of the final output
+        // token, read back by the completion insert) is still in this
+        // worker-iteration's step: keep its slot until that step is issued.
+        if (lc.slot < 0) return;
+        if (finished_slots_.size() <= static_cast<std::size_t>(w)) finished_slots_.resize(static_cast<std::size_t>(w) + 1);
+        finished_slots_[static_cast<std::size_t>(w)].push_back(lc.slot);
     }
     void finish_run() override {
         e_->run_end();
@@ -976,7 +997,13 @@ class DeviceBody : public LlmBody {
   private:
     // engine pool of schedule worker w (a single pool serves one-worker mode)
     int pw(int w) const { return e_->workers.size() == 1 ? 0 : w; }
+    void release_slots(int w) {
+        if (static_cast<std::size_t>(w) >= finished_slots_.size()) return;
+        for (int s : finished_slots_[static_cast<std::size_t>(w)]) e_->free_slot(pw(w), s);
+        finished_slots_[static_cast<std::size_t>(w)].clear();
+    }
     hk_engine* e_;
+    std::vector<std::vector<int>> finished_slots_;
 };
 
 std::unique_ptr<LlmBody> make_device_body(hk_engine* e, const Plan& plan, const SimConfig& cfg) {
