@@ -25,6 +25,26 @@ int hkx_gemm_bf16(const void* W, const void* X, void* out, int N, int K, int T, 
  * the mean milliseconds per launch (or a negative value on error). */
 double hkx_gemm_bench(const void* W, const void* X, void* out, int N, int K, int T, int epi, int splits, int iters);
 
+/* K3b decode attention of one layer (device pointers; bf16):
+ *   qkv [n_rows][(H + 2 Hkv) * 128], kv [n_pages][2][Hkv][16][128], out [n_rows][H][128].
+ * Row r attends keys [0, pos[r]] through the page table tables[offs[r] .. offs[r+1])
+ * (host arrays). Rows come in n_groups consecutive groups of group_rows[g]
+ * rows whose tables share group_shared_pages[g] leading pages (0 = none): the
+ * shared pages run on the tcgen05 kernel once per group, the rest per row.
+ * Replaces the attention that the reference's decode step implies
+ * (simulator.cpp:347-355). iters > 0 also times that many back-to-back calls:
+ * returns ms per call (0 when iters == 0) or a negative value on error. */
+double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_rows, int H, int Hkv,
+                            const int32_t* tables, const int32_t* offs, const int32_t* pos, const int32_t* group_rows,
+                            const int32_t* group_shared_pages, int n_groups, void* out, int iters);
+/* Debug: record per-CTA phase timestamps (%globaltimer, ns) of later
+ * hkx_decode_attention calls into device_buf ([shared CTAs + private CTAs][8] u64);
+ * NULL turns it off. */
+int hkx_decode_attention_trace(void* device_buf);
+/* Algorithmic bytes of that call: shared KV once per group + private KV + q and o. */
+double hkx_decode_attention_bytes(int n_rows, int H, int Hkv, const int32_t* offs, const int32_t* pos,
+                                  const int32_t* group_rows, const int32_t* group_shared_pages, int n_groups);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,774 @@
+// K3b: prefix-shared paged decode attention (bf16), the attention of every
+// decode token of one (iteration, worker) step of the reference's simulate()
+// loop (simulator.cpp:347-374: one token per running call per iteration).
+//
+// Decode rows that share a block-table prefix (branches of one shared prompt,
+// e.g. the 2,048-token pinned system prompt of configs[1]) form a group. Per
+// layer and kv head the group's rows are (token, q-head) pairs — G = H / Hkv
+// of them per token — so 128/G tokens fill one 128-row tcgen05 tile:
+//
+//   shared item  (attn_shared_tc_kernel): S = Q K^T and O = P V on the tensor
+//                cores for 128 rows x a range of shared pages. K/V pages are
+//                staged by TMA (128B swizzle) straight from the paged pool,
+//                Q is written swizzled by the CTA, S and O live in TMEM, the
+//                softmax warps read S with tcgen05.ld (one thread per row) and
+//                write P (bf16) back to shared memory as the A operand of PV;
+//                V is consumed MN-major, as it lies in the page. The shared KV
+//                is read once for all rows of the tile instead of once per row.
+//   private item (attn_private_kernel): one token x one kv head over its own
+//                pages (prompt suffix + generated tokens): a GEMV-shaped flash
+//                loop on the CUDA cores, whole 4 KB K and V page halves staged
+//                by 1D bulk async copies (cp.async.bulk) into an 8-deep
+//                mbarrier ring, 8 lanes x 16 dims per key, 8-lane shuffles.
+//
+// The shared items that split one tile's pages form a thread-block cluster:
+// they exchange row maxima and reduce their O tiles through distributed shared
+// memory, so a tile leaves ONE flash partial (m, l, unnormalised o; log2
+// domain) per row however many SMs streamed its pages. Private items leave
+// one partial each. A per-(decode row, kv head) arrival counter picks the last
+// contributor, which merges the row's partials and writes the bf16 attention
+// output — there is no separate merge launch. The private kernel runs first and lets
+// the shared kernel launch as soon as every private CTA has started (PDL);
+// the shared kernel waits for the private grid only before exiting, so the
+// next kernel's griddepcontrol.wait covers both.
+#include <algorithm>
+#include <cfloat>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace hkd {
+
+namespace {
+
+constexpr int HD = 128;
+constexpr int PG = 16;        // tokens per KV page
+constexpr int KC = 128;       // keys per tcgen05 chunk (8 pages)
+constexpr int ROWS = 128;     // MMA rows of a shared item
+
+// -------------------------------------------------------------------- merge
+// Merge of (decode row, head) partials: an 8-lane group per pair, lane owns
+// 16 dims; a warp merges 4 pairs at once. All part loads of a lane are
+// independent, so a merge costs about two L2 round trips.
+__device__ __forceinline__ void merge_group(const DecodeAttnArgs& a, int row, int head, bool active, int sub) {
+    const unsigned full = 0xffffffffu;
+    const int np = active ? a.n_parts[row] : 0;
+    const size_t base = (static_cast<size_t>(active ? row : 0) * a.H + head) * a.max_parts;
+    float2 ml[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int k = sub + 8 * j;
+        ml[j] = k < np ? __ldcg(&a.part_ml[base + k]) : make_float2(-INFINITY, 0.f);
+    }
+    float M = fmaxf(fmaxf(ml[0].x, ml[1].x), fmaxf(ml[2].x, ml[3].x));
+    M = fmaxf(M, __shfl_xor_sync(full, M, 1));
+    M = fmaxf(M, __shfl_xor_sync(full, M, 2));
+    M = fmaxf(M, __shfl_xor_sync(full, M, 4));
+    float w[4], L = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        w[j] = sub + 8 * j < np ? exp2f(ml[j].x - M) : 0.f;
+        L += w[j] * ml[j].y;
+    }
+    L += __shfl_xor_sync(full, L, 1);
+    L += __shfl_xor_sync(full, L, 2);
+    L += __shfl_xor_sync(full, L, 4);
+    float acc[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+    const int lane = threadIdx.x & 31;
+    const int g0 = lane & ~7;
+    // 4 parts per round trip: all 16 loads issued before any use
+    for (int k0 = 0; k0 < 32; k0 += 4) {
+        if (!__any_sync(full, k0 < np)) break;
+        const float wsel = k0 < 8 ? w[0] : (k0 < 16 ? w[1] : (k0 < 24 ? w[2] : w[3]));
+        float4 v[4][4];
+        float wk[4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            const int k = k0 + kk;
+            wk[kk] = __shfl_sync(full, wsel, g0 + (k & 7));
+            const float4* src = reinterpret_cast<const float4*>(a.part_o + (base + (k < np ? k : 0)) * HD + sub * 16);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[kk][e] = __ldcg(src + e);
+            if (k >= np) wk[kk] = 0.f;
+        }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                acc[4 * e] += wk[kk] * v[kk][e].x;
+                acc[4 * e + 1] += wk[kk] * v[kk][e].y;
+                acc[4 * e + 2] += wk[kk] * v[kk][e].z;
+                acc[4 * e + 3] += wk[kk] * v[kk][e].w;
+            }
+    }
+    if (!active) return;
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    bf16* o = a.out + (static_cast<size_t>(a.dec_tok0 + row) * a.H + head) * HD + sub * 16;
+    uint4 w0, w1;
+    __nv_bfloat162 t[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) t[e] = __floats2bfloat162_rn(acc[2 * e] * inv, acc[2 * e + 1] * inv);
+    w0 = *reinterpret_cast<uint4*>(&t[0]);
+    w1 = *reinterpret_cast<uint4*>(&t[4]);
+    reinterpret_cast<uint4*>(o)[0] = w0;
+    reinterpret_cast<uint4*>(o)[1] = w1;
+}
+
+// Merge the n (row, head) pairs pair(i) = (row_i, head_i), i < n, with one warp.
+template <typename PairFn>
+__device__ __forceinline__ void merge_pairs(const DecodeAttnArgs& a, int n, PairFn pair) {
+    const int lane = threadIdx.x & 31, grp = lane >> 3, sub = lane & 7;
+    for (int i0 = 0; i0 < n; i0 += 4) {
+        const int i = i0 + grp;
+        int row = 0, head = 0;
+        if (i < n) pair(i, row, head);
+        merge_group(a, row, head, i < n, sub);
+    }
+}
+
+// Arrival on a (row, kv head) counter: release orders this thread's partial
+// stores (after a warp/CTA barrier, those of its peers too, by cumulativity)
+// before the increment; acquire makes the other contributors' partials
+// visible to the thread that arrives last.
+__device__ __forceinline__ int arrive_acq_rel(int32_t* ctr) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+    return old;
+}
+
+__device__ __forceinline__ void stamp(const DecodeAttnArgs& a, int cta, int k) {
+    if (a.trace && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[static_cast<size_t>(cta) * 16 + k] = t;
+        if (k == 0 || k == 5) a.trace[static_cast<size_t>(cta) * 16 + 14 + (k == 5)] = clock64();
+    }
+}
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// ------------------------------------------------------- shared (tcgen05)
+// Warp-specialised, one CTA per SM (320 threads):
+//   warp 9  (TMA)     page ids -> smem, then K/V chunks of 8 pages into a
+//                     2-stage ring (TMA 2D, 128B swizzle, box 64 x 16);
+//   warp 8  (MMA)     one thread issues S(c) = Q K(c)^T into one of two TMEM
+//                     S buffers, then O += P(c-1) V(c-1) — QK of the next
+//                     chunk overlaps the softmax of the current one;
+//   warps 0-7 (softmax) two threads per row (TMEM lane quarter = warp % 4,
+//                     column half = warp / 4): scale, row max (exchanged
+//                     through smem), lazy O rescale, exp2, P (bf16) into the
+//                     A-operand tile, then the epilogue and arrival counters.
+// smem (1024-aligned): sQ [2][128][64] | 2 x (sK [2][128][64] | sV) | sP [2][128][64] | barriers | exchange
+constexpr int SQ_BYTES = ROWS * HD * 2;   // 32 KB
+constexpr int SKV_BYTES = KC * HD * 2;    // 32 KB (K or V of one chunk)
+constexpr int SH_THREADS = 320;
+constexpr int SH_MAX_PAGES = 512;         // pages of one shared item
+constexpr int SH_SMEM = 1024 + SQ_BYTES + 2 * 2 * SKV_BYTES + ROWS * KC * 2 + 256 + 5 * ROWS * 4 + (ROWS + 4) * 4 +
+                        SH_MAX_PAGES * 4;
+
+__device__ __forceinline__ uint32_t sw128(int row, int chunk16) {  // byte offset inside a [rows][64] SW128 block
+    return static_cast<uint32_t>(row * 128 + ((chunk16 ^ (row & 7)) << 4));
+}
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <int G>
+__global__ void __launch_bounds__(SH_THREADS, 1) attn_shared_tc_kernel(const __grid_constant__ CUtensorMap tm_kv,
+                                                                       DecodeAttnArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // stay in the shared address space (pointer arithmetic on the array) so
+    // plain stores compile to STS
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sQ = sm;
+    uint8_t* sKV = sm + SQ_BYTES;  // stage b: K at b*2*SKV_BYTES, V at +SKV_BYTES
+    uint8_t* sP = sKV + 4 * SKV_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + ROWS * KC * 2);
+    uint64_t* kv_full = bars;       // [2] chunk landed (TMA tx)
+    uint64_t* kv_empty = bars + 2;  // [2] chunk consumed (PV commit)
+    uint64_t* s_full = bars + 4;    // [2] S buffer written (MMA commit)
+    uint64_t* s_free = bars + 6;    // [2] S buffer read (256 softmax threads)
+    uint64_t* p_full = bars + 8;    // P written (256 softmax threads)
+    uint64_t* o_done = bars + 9;    // PV complete (MMA commit)
+    uint64_t* q_full = bars + 10;   // Q tile written (256 softmax threads)
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 12);
+
+    float* red = reinterpret_cast<float*>(sm + SQ_BYTES + 4 * SKV_BYTES + ROWS * KC * 2 + 256);  // [2][128] x 2
+    int* flags = reinterpret_cast<int*>(red + 5 * ROWS);  // [ROWS] tokens this CTA merges, [ROWS] count
+    int* spg = flags + ROWS + 4;                            // page ids of this item
+
+    stamp(a, blockIdx.x, 0);
+    const ShItem it = a.sh[blockIdx.x];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nrows = it.ntok * G;
+    const int nch = (it.npages + 7) / 8;
+
+    if (tid == 0) {
+        tma_prefetch_desc(&tm_kv);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&kv_full[b], 1);
+            mbar_init(&kv_empty[b], 1);
+            mbar_init(&s_full[b], 1);
+            mbar_init(&s_free[b], 256);
+        }
+        mbar_init(p_full, 256);
+        mbar_init(o_done, 1);
+        mbar_init(q_full, 256);
+        fence_barrier_init();
+    }
+    if (warp == 8) tmem_alloc(tslot, 512);  // S0 [0,128) | S1 [128,256) | O [256,384)
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    stamp(a, blockIdx.x, 1);
+
+    if (warp == 9) {
+        // ---- TMA producer. Shared pages were written by earlier steps, so their
+        // loads need not wait for this step's producers.
+        for (int i = lane; i < it.npages; i += 32) spg[i] = a.pages[it.ptab + it.page0 + i];
+        __syncwarp();
+        if (lane == 0) {
+            const int rows_per_head = a.Hkv * PG;  // pool-map rows between K and V of a page
+            for (int c = 0; c < nch; ++c) {
+                const int b = c & 1;
+                if (c >= 2) mbar_wait(&kv_empty[b], ((c >> 1) - 1) & 1);
+                const int np = min(8, it.npages - c * 8);
+                uint8_t* sK = sKV + b * 2 * SKV_BYTES;
+                uint8_t* sV = sK + SKV_BYTES;
+                mbar_expect_tx(&kv_full[b], static_cast<uint32_t>(np) * 4 * 2048);
+                for (int i = 0; i < np; ++i) {
+                    const int rk = a.layer_row0 + (spg[c * 8 + i] * 2 * a.Hkv + it.kvh) * PG;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        tma_load_2d(sK + h * SKV_BYTES / 2 + i * 2048, &tm_kv, &kv_full[b], h * 64, rk);
+                        tma_load_2d(sV + h * SKV_BYTES / 2 + i * 2048, &tm_kv, &kv_full[b], h * 64, rk + rows_per_head);
+                    }
+                }
+                if (c == 0) stamp(a, blockIdx.x, 6);
+            }
+        }
+        pdl_wait();
+        pdl_trigger();
+    } else if (warp == 8) {
+        // ---- MMA issuer
+        pdl_wait();
+        pdl_trigger();
+        if (lane == 0) {
+            const uint32_t q0 = smem_u32(sQ), p0 = smem_u32(sP);
+            auto issue_pv = [&](int j) {
+                mbar_wait(p_full, j & 1);
+                tc_fence_after();
+                const int np = min(8, it.npages - j * 8);
+                const uint32_t v0 = smem_u32(sKV + (j & 1) * 2 * SKV_BYTES + SKV_BYTES);
+                const uint32_t idesc = umma_idesc_bf16(ROWS, HD) | (1u << 16);  // B = V, MN-major
+                for (int kk = 0; kk < np; ++kk)
+                    umma_bf16(tmem + 256, umma_desc_sw128(p0 + (kk >> 2) * (ROWS * 128) + (kk & 3) * 32),
+                              umma_desc_sw128_lbo(v0 + kk * 2048, SKV_BYTES / 2, 1024), idesc,
+                              (j > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(o_done);
+                umma_commit(&kv_empty[j & 1]);
+            };
+            mbar_wait(q_full, 0);
+            for (int c = 0; c < nch; ++c) {
+                const int b = c & 1;
+                mbar_wait(&kv_full[b], (c >> 1) & 1);
+                if (c >= 2) mbar_wait(&s_free[b], ((c >> 1) - 1) & 1);
+                tc_fence_after();
+                const int nk = min(8, it.npages - c * 8) * PG;
+                const uint32_t idesc = umma_idesc_bf16(ROWS, nk);
+                const uint32_t k0 = smem_u32(sKV + b * 2 * SKV_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * (SKV_BYTES / 2) + (kk & 3) * 32;
+                    umma_bf16(tmem + b * 128, umma_desc_sw128(q0 + (kk >> 2) * (SQ_BYTES / 2) + (kk & 3) * 32),
+                              umma_desc_sw128(k0 + off), idesc, kk > 0 ? 1u : 0u);
+                }
+                umma_commit(&s_full[b]);
+                if (c >= 1) issue_pv(c - 1);
+            }
+            issue_pv(nch - 1);
+        }
+        __syncwarp();
+    } else {
+        // ---- softmax warps: thread = (row, column half)
+        const int row = (warp & 3) * 32 + lane;
+        const int half = warp >> 2;
+        const uint32_t t_lane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        pdl_wait();  // q comes from the qkv/RoPE kernel
+        pdl_trigger();
+        {
+            // Q tile rows (token r / G, head kvh*G + r % G); rows >= nrows are zero.
+            uint4 qv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int idx = tid + i * 256, r = idx >> 4, ch = idx & 15;
+                qv[i] = make_uint4(0u, 0u, 0u, 0u);
+                if (r < nrows)
+                    qv[i] = __ldg(reinterpret_cast<const uint4*>(
+                        a.qkv + static_cast<size_t>(a.dec_tok0 + it.row0 + r / G) * a.QKV + (it.kvh * G + r % G) * HD +
+                        ch * 8));
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int idx = tid + i * 256, r = idx >> 4, ch = idx & 15;
+                *reinterpret_cast<uint4*>(sQ + (ch >> 3) * (SQ_BYTES / 2) + sw128(r, ch & 7)) = qv[i];
+            }
+            fence_proxy_async();
+            mbar_arrive(q_full);
+        }
+        stamp(a, blockIdx.x, 2);
+        float m_run = -INFINITY, l_half = 0.f;
+        float* red_mx = red;             // [2][128] row maxima halves, then [128] m_run at 2*ROWS
+        float* red_l = red + 3 * ROWS;   // [2][128]
+        for (int c = 0; c < nch; ++c) {
+            const int b = c & 1;
+            const int nk = min(8, it.npages - c * 8) * PG;
+            mbar_wait(&s_full[b], (c >> 1) & 1);
+            tc_fence_after();
+            if (c == 0) stamp(a, blockIdx.x, 7);
+            float s[64];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int col0 = half * 64 + j * 32;
+                float v[32];
+                if (col0 < nk) {
+                    tmem_ld32(t_lane + b * 128 + col0, v);
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) s[j * 32 + e] = col0 + e < nk ? v[e] * a.sl2 : -INFINITY;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) s[j * 32 + e] = -INFINITY;
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&s_free[b]);  // this thread is done with S buffer b
+            float mx = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 64; ++j) mx = fmaxf(mx, s[j]);
+            red_mx[half * ROWS + row] = mx;
+            named_bar(1, 256);
+            mx = fmaxf(red_mx[row], red_mx[ROWS + row]);
+            // PV(c-1) must be done before O is rescaled or P rewritten
+            if (c > 0) {
+                mbar_wait(o_done, (c - 1) & 1);
+                tc_fence_after();
+            }
+            // lazy rescale (exact: O and l always refer to m_run; p <= 2^8 between
+            // rescales). tcgen05.ld/st are warp-collective: a warp rescales together.
+            const bool need = mx > m_run + 8.f;
+            if (__any_sync(0xffffffffu, need)) {
+                const float al = need ? ex2(m_run - mx) : 1.f;
+                if (c > 0) {
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        float v[32];
+                        const uint32_t ta = t_lane + 256 + half * 64 + j * 32;
+                        tmem_ld32(ta, v);
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) v[e] *= al;
+                        tmem_st32(ta, v);
+                    }
+                    tmem_wait_st();
+                }
+                if (need) {
+                    l_half *= al;
+                    m_run = mx;
+                }
+            }
+#pragma unroll
+            for (int j8 = 0; j8 < 8; ++j8) {
+                float p[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    p[e] = ex2(s[j8 * 8 + e] - m_run);
+                    l_half += p[e];
+                }
+                uint4 w;
+                w.x = pack2(p[0], p[1]);
+                w.y = pack2(p[2], p[3]);
+                w.z = pack2(p[4], p[5]);
+                w.w = pack2(p[6], p[7]);
+                *reinterpret_cast<uint4*>(sP + half * (ROWS * 128) + sw128(row, j8)) = w;
+            }
+            fence_proxy_async();
+            tc_fence_before();
+            mbar_arrive(p_full);
+            if (c == 0) stamp(a, blockIdx.x, 8);
+        }
+        mbar_wait(o_done, (nch - 1) & 1);
+        tc_fence_after();
+        stamp(a, blockIdx.x, 3);
+        if (half == 0) red_mx[2 * ROWS + row] = m_run;
+        // ---- partial rows, staged through smem (the K/V stages are free) so that
+        // each warp stores whole 512-byte rows (coalesced)
+        constexpr int SO = HD + 4;  // padded fp32 row stride: conflict-free float4 stores
+        float* sO = reinterpret_cast<float*>(sKV);
+        red_l[half * ROWS + row] = l_half;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            float v[32];
+            tmem_ld32(t_lane + 256 + half * 64 + j * 32, v);
+            float4* dst = reinterpret_cast<float4*>(sO + row * SO + half * 64 + j * 32);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+        }
+        named_bar(1, 256);
+        for (int r = warp; r < nrows; r += 8) {
+            const size_t pi = (static_cast<size_t>(it.row0 + r / G) * a.H + it.kvh * G + r % G) * a.max_parts + it.rank;
+            reinterpret_cast<float4*>(a.part_o + pi * HD)[lane] = reinterpret_cast<const float4*>(sO + r * SO)[lane];
+            if (lane == 0) a.part_ml[pi] = make_float2(red_mx[2 * ROWS + r], red_l[r] + red_l[ROWS + r]);
+        }
+        stamp(a, blockIdx.x, 4);
+        // ---- arrival counters: the last contributor of a (token, kv head) merges it
+        int* mlist = flags;  // tokens to merge, compacted
+        if (tid == 0) flags[ROWS] = 0;
+        named_bar(1, 256);
+        if (tid < it.ntok) {
+            const int r = it.row0 + tid;
+            if (arrive_acq_rel(&a.counters[r * a.Hkv + it.kvh]) == a.n_parts[r] - 1) mlist[atomicAdd(&flags[ROWS], 1)] = tid;
+        }
+        named_bar(1, 256);
+        const int nm = flags[ROWS] * G;  // (token, head) pairs to merge, spread over the 8 warps
+        const int per = (nm + 7) / 8;
+        merge_pairs(a, max(0, min(per, nm - warp * per)), [&](int i, int& r, int& h) {
+            const int q = warp * per + i;
+            r = it.row0 + mlist[q / G];
+            h = it.kvh * G + q % G;
+        });
+        named_bar(1, 256);
+        if (tid < flags[ROWS]) a.counters[(it.row0 + mlist[tid]) * a.Hkv + it.kvh] = 0;
+        stamp(a, blockIdx.x, 5);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ------------------------------------------------------ private (tensor cores)
+// One warp per item (a token's own pages for one kv head). MMA rows are the G
+// q-heads of the token (rows >= G are zero padding): per 16-key page,
+// S = Q K^T is 8 x 2 mma.sync m16n8k16 and O += P V is 16 more, operands read
+// with ldmatrix from TMA-swizzled page tiles (conflict-free). The warp feeds
+// itself: lane 0 keeps PV_ST pages (4 TMA boxes each) in flight in the warp's
+// own ring and refills a stage as soon as the warp has read it.
+constexpr int PV_WARPS = 4;
+constexpr int PV_ST = 3;
+constexpr int PV_SMEM = 1024 + PV_WARPS * PV_ST * 8192 + PV_WARPS * PV_ST * 8 + 64;
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// byte offset of (row, 16-byte chunk c of 16) in a page tile made of two TMA
+// boxes [16 rows][64 elems] with 128B swizzle (box = c / 8)
+__device__ __forceinline__ uint32_t tile_off(int row, int c) {
+    return static_cast<uint32_t>((c >> 3) * 2048 + row * 128 + (((c & 7) ^ (row & 7)) << 4));
+}
+
+template <int G>
+__global__ void __launch_bounds__(PV_WARPS * 32, 2) attn_private_kernel(const __grid_constant__ CUtensorMap tm_kv,
+                                                                        DecodeAttnArgs a) {
+    static_assert(G <= 8, "private kernel: G q-heads must fit rows 0-7 of the MMA tile");
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + PV_WARPS * PV_ST * 8192);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int ii = blockIdx.x * PV_WARPS + warp;
+    if (lane == 0) {
+        for (int s = 0; s < PV_ST; ++s) mbar_init(&full[warp * PV_ST + s], 1);
+        fence_barrier_init();
+        tma_prefetch_desc(&tm_kv);
+    }
+    __syncwarp();
+    stamp(a, a.n_sh + blockIdx.x, 0);
+    // q and this token's own K/V come from the qkv/RoPE kernel: when a shared
+    // grid runs first it has waited for that kernel before letting us launch.
+    if (a.n_sh == 0) pdl_wait();
+    pdl_trigger();  // the next kernel (O projection) may start prefetching its weights
+    stamp(a, a.n_sh + blockIdx.x, 1);
+    if (ii >= a.n_pv) {
+        pdl_wait();
+        return;
+    }
+    const PvItem it = a.pv[ii];
+    const int p0 = it.kbeg / PG;
+    const int np = (it.kend - it.kbeg + PG - 1) / PG;
+    uint8_t* ring = sm + warp * PV_ST * 8192;
+    const uint32_t ring_s = smem_u32(ring);
+    const int rows_per_head = a.Hkv * PG;
+    // page ids of the item (np <= 32 for this kernel's key splits), one per lane
+    const int my_page = lane < np ? a.pages[it.ptab + p0 + lane] : 0;
+    auto issue = [&](int i, int page) {  // lane 0 only: K (2 boxes) + V (2 boxes)
+        const int s = i % PV_ST;
+        uint64_t* bar = &full[warp * PV_ST + s];
+        uint8_t* dst = ring + s * 8192;
+        const int rk = a.layer_row0 + (page * 2 * a.Hkv + it.kvh) * PG;
+        mbar_expect_tx(bar, 8192);
+        tma_load_2d(dst, &tm_kv, bar, 0, rk);
+        tma_load_2d(dst + 2048, &tm_kv, bar, 64, rk);
+        tma_load_2d(dst + 4096, &tm_kv, bar, 0, rk + rows_per_head);
+        tma_load_2d(dst + 6144, &tm_kv, bar, 64, rk + rows_per_head);
+    };
+#pragma unroll
+    for (int i = 0; i < PV_ST; ++i) {
+        const int pg = __shfl_sync(0xffffffffu, my_page, i);
+        if (lane == 0 && i < np) issue(i, pg);
+    }
+    // Q as the A operand (rows gid < G hold q heads kvh*G + gid; rows >= 8 are zero)
+    uint32_t qa[8][2];
+    {
+        const bf16* qp = a.qkv + static_cast<size_t>(a.dec_tok0 + it.row) * a.QKV + (it.kvh * G + gid) * HD + 2 * tig;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            qa[ks][0] = gid < G ? *reinterpret_cast<const uint32_t*>(qp + ks * 16) : 0u;
+            qa[ks][1] = gid < G ? *reinterpret_cast<const uint32_t*>(qp + ks * 16 + 8) : 0u;
+        }
+    }
+    float o[16][4];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;  // row gid (rows gid + 8 are padding)
+    // ldmatrix lane roles: matrix mi = lane / 8, row within it rr = lane % 8
+    const int mi = lane >> 3, rr = lane & 7;
+    for (int i = 0; i < np; ++i) {
+        const int s = i % PV_ST;
+        mbar_wait(&full[warp * PV_ST + s], (i / PV_ST) & 1);
+        if (i == 0 && warp == 0) stamp(a, a.n_sh + blockIdx.x, 3);
+        const uint32_t kt = ring_s + s * 8192, vt = kt + 4096;
+        // S = Q K^T: two n-tiles of 8 keys
+        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            uint32_t b0, b1, b2, b3;  // (keys 0-7 | 8-15) x (dims lo | hi of the k-step)
+            ldsm_x4(kt + tile_off((mi >> 1) * 8 + rr, 2 * ks + (mi & 1)), b0, b1, b2, b3);
+            const uint32_t af[4] = {qa[ks][0], 0u, qa[ks][1], 0u};
+            mma16816(sc[0], af, b0, b1);
+            mma16816(sc[1], af, b2, b3);
+        }
+        // online softmax on row gid (values sc[j][0..1]; [2..3] are padding rows)
+        const int kb = it.kbeg + i * PG;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const bool valid = kb + j * 8 + 2 * tig + e < it.kend;
+                sc[j][e] = valid ? sc[j][e] * a.sl2 : -INFINITY;
+                mx = fmaxf(mx, sc[j][e]);
+            }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        if (mx > m_run) {  // (quad-uniform)
+            const float al = ex2(m_run - mx);
+            l_run *= al;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                o[j][0] *= al;
+                o[j][1] *= al;
+            }
+            m_run = mx;
+        }
+        float p[2][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                p[j][e] = ex2(sc[j][e] - m_run);
+                l_run += p[j][e];
+            }
+        const uint32_t pa[4] = {pack2(p[0][0], p[0][1]), 0u, pack2(p[1][0], p[1][1]), 0u};
+        // O += P V: V tile [key][dim], B operand via ldmatrix.trans, two dim n-tiles per load
+#pragma unroll
+        for (int dp = 0; dp < 8; ++dp) {
+            uint32_t b0, b1, b2, b3;  // (keys 0-7 | 8-15) x (dims 16dp.. | 16dp+8..)
+            ldsm_x4_t(vt + tile_off((mi & 1) * 8 + rr, 2 * dp + (mi >> 1)), b0, b1, b2, b3);
+            mma16816(o[2 * dp], pa, b0, b1);
+            mma16816(o[2 * dp + 1], pa, b2, b3);
+        }
+        // every lane has read stage s (the shuffle syncs the warp): refill it
+        const int pg = __shfl_sync(0xffffffffu, my_page, (i + PV_ST) & 31);
+        if (lane == 0 && i + PV_ST < np) issue(i + PV_ST, pg);
+    }
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    if (warp == 0) stamp(a, a.n_sh + blockIdx.x, 2);
+    const bool vrow = gid < G;
+    if (it.part < 0) {
+        if (vrow) {
+            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+            bf16* op = a.out + (static_cast<size_t>(a.dec_tok0 + it.row) * a.H + it.kvh * G + gid) * HD + 2 * tig;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) *reinterpret_cast<uint32_t*>(op + j * 8) = pack2(o[j][0] * inv, o[j][1] * inv);
+        }
+        pdl_wait();
+        return;
+    }
+    if (vrow) {
+        const size_t pi = (static_cast<size_t>(it.row) * a.H + it.kvh * G + gid) * a.max_parts + it.part;
+        float* po = a.part_o + pi * HD + 2 * tig;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) *reinterpret_cast<float2*>(po + j * 8) = make_float2(o[j][0], o[j][1]);
+        if (tig == 0) a.part_ml[pi] = make_float2(m_run, l_run);
+    }
+    if (warp == 0) stamp(a, a.n_sh + blockIdx.x, 4);
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = arrive_acq_rel(&a.counters[it.row * a.Hkv + it.kvh]) == a.n_parts[it.row] - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (warp == 0) stamp(a, a.n_sh + blockIdx.x, 5);
+    if (last) {
+        __syncwarp();
+        merge_pairs(a, G, [&](int q, int& r, int& h) {
+            r = it.row;
+            h = it.kvh * G + q;
+        });
+        if (lane == 0) a.counters[it.row * a.Hkv + it.kvh] = 0;
+    }
+    if (warp == 0) stamp(a, a.n_sh + blockIdx.x, 6);
+    pdl_wait();  // complete only after the shared grid: the next kernel's wait covers both
+}
+
+template <int G>
+void launch_g(const DecodeAttnArgs& a, const CUtensorMap& tm, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        HK_CUDA(cudaFuncSetAttribute(attn_shared_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, SH_SMEM));
+        HK_CUDA(cudaFuncSetAttribute(attn_private_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, PV_SMEM));
+        configured = true;
+    }
+    if (a.n_sh > 0) {
+        launch_pdl(attn_shared_tc_kernel<G>, dim3(a.n_sh), dim3(SH_THREADS), SH_SMEM, st, tm, a);
+        HK_LAUNCHED(1);
+    }
+    if (a.n_pv > 0) {
+        launch_pdl(attn_private_kernel<G>, dim3((a.n_pv + PV_WARPS - 1) / PV_WARPS), dim3(PV_WARPS * 32), PV_SMEM,
+                   st, tm, a);
+        HK_LAUNCHED(1);
+    }
+}
+
+}  // namespace
+
+void decode_attention(const DecodeAttnArgs& a, const CUtensorMap& tm_kv, cudaStream_t st) {
+    if (a.n_sh > 0 && a.n_pv == 0) throw std::runtime_error("decode_attention: shared items need private items");
+    switch (a.H / a.Hkv) {
+        case 1: launch_g<1>(a, tm_kv, st); break;
+        case 2: launch_g<2>(a, tm_kv, st); break;
+        case 4: launch_g<4>(a, tm_kv, st); break;
+        case 5: launch_g<5>(a, tm_kv, st); break;
+        default: throw std::runtime_error("decode_attention: unsupported GQA group size");
+    }
+}
+
+// Host planning: every shared group is tiled into (128/G rows) x kv heads;
+// each tile is streamed by a cluster of S CTAs (S uniform per launch, about
+// one CTA per SM overall, <= 8 portable) that split its 8-page chunks. Every
+// row then gets private items over its own pages, split at kPrivKeys keys.
+void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vector<DecodeGroupIn>& groups, int H,
+                           int Hkv, int max_parts, int num_sms, DecodePlan& plan) {
+    const int G = H / Hkv;
+    const int rb = ROWS / G;
+    const double kv_tok = 2.0 * HD * 2;  // K + V bytes of one key of one kv head
+    plan.sh.clear();
+    plan.pv.clear();
+    plan.n_parts.assign(rows.size(), 0);
+    plan.shared_bytes = plan.private_bytes = 0;
+    int tiles = 0;
+    for (const auto& g : groups)
+        if (g.shared_pages > 0 && g.members > 1) tiles += (g.members + rb - 1) / rb * Hkv;
+    plan.sh_cluster = 1;
+    // private key split: about 8 private warps per SM over the whole step
+    double priv_keys = 0;
+    for (const auto& g : groups) {
+        const int k0 = (g.shared_pages > 0 && g.members > 1) ? g.shared_pages * PG : 0;
+        for (int m = 0; m < g.members; ++m) priv_keys += rows[static_cast<size_t>(g.row0 + m)].pos + 1 - k0;
+    }
+    int kp_base = static_cast<int>(priv_keys * Hkv / (8.0 * num_sms));
+    kp_base = std::max(128, std::min(512, (kp_base + PG - 1) / PG * PG));
+    if (std::getenv("HK_ATTN_PRIV_KEYS")) kp_base = std::atoi(std::getenv("HK_ATTN_PRIV_KEYS"));
+    for (const auto& g : groups) {
+        const bool shared = g.shared_pages > 0 && g.members > 1;
+        const int shared_pages = shared ? g.shared_pages : 0;
+        int splits = 0;
+        if (shared) {
+            // about one shared CTA per SM over all tiles; the private kernel fills
+            // the remaining SMs and every SM a finished shared CTA frees
+            const int nch = (shared_pages + 7) / 8;
+            static const int env_splits = std::getenv("HK_ATTN_SPLITS") ? std::atoi(std::getenv("HK_ATTN_SPLITS")) : 0;
+            splits = std::max(1, std::min({nch, env_splits > 0 ? env_splits : (num_sms + tiles - 1) / tiles,
+                                           max_parts / 2}));
+            int cpc = (nch + splits - 1) / splits;
+            cpc = std::min(cpc, SH_MAX_PAGES / 8);
+            splits = (nch + cpc - 1) / cpc;
+            for (int r0 = 0; r0 < g.members; r0 += rb)
+                for (int h = 0; h < Hkv; ++h)
+                    for (int k = 0; k < splits; ++k) {
+                        ShItem it{};
+                        it.row0 = g.row0 + r0;
+                        it.ntok = std::min(rb, g.members - r0);
+                        it.kvh = h;
+                        it.ptab = rows[static_cast<size_t>(g.row0)].ptab;
+                        it.page0 = k * cpc * 8;
+                        it.npages = std::min(cpc * 8, shared_pages - it.page0);
+                        it.rank = k;  // partial index
+                        plan.sh.push_back(it);
+                    }
+            plan.shared_bytes += static_cast<double>(shared_pages) * PG * Hkv * kv_tok;
+        }
+        for (int m = 0; m < g.members; ++m) {
+            const int r = g.row0 + m;
+            const DecodeRowIn& in = rows[static_cast<size_t>(r)];
+            const int k0 = shared_pages * PG, k1 = in.pos + 1;
+            if (k1 <= k0) throw std::runtime_error("decode_attention: shared range covers the decode token");
+            const int first = splits;  // the shared items contribute partials 0 .. splits - 1
+            int kp = std::max(kp_base, (k1 - k0 + (max_parts - first) - 1) / (max_parts - first));
+            kp = (kp + PG - 1) / PG * PG;
+            if (kp > 32 * PG) throw std::runtime_error("decode_attention: private range too long for max_parts");
+            const int npv = (k1 - k0 + kp - 1) / kp;
+            const int parts = first + npv;
+            if (parts > max_parts) throw std::runtime_error("decode_attention: too many partials for a row");
+            plan.n_parts[static_cast<size_t>(r)] = parts;
+            for (int i = 0; i < npv; ++i)
+                for (int h = 0; h < Hkv; ++h) {
+                    PvItem it{};
+                    it.row = r;
+                    it.kvh = h;
+                    it.ptab = in.ptab;
+                    it.kbeg = k0 + i * kp;
+                    it.kend = std::min(k1, it.kbeg + kp);
+                    it.part = parts == 1 ? -1 : first + i;
+                    plan.pv.push_back(it);
+                }
+            plan.private_bytes += static_cast<double>(k1 - k0) * Hkv * kv_tok;
+            plan.private_bytes += 2.0 * H * HD * 2;  // q in, o out
+        }
+    }
+}
+
+}  // namespace hkd

@@ -122,6 +122,8 @@ struct hk_engine {
         void* kv = nullptr;           // [L][P][2][Hkv][block][hd]
         size_t layer_stride = 0;      // bytes
         int32_t* slot_last = nullptr; // [max_calls]
+        int32_t* counters = nullptr;  // [max decode rows][Hkv] decode-attention arrival counters
+        CUtensorMap tm_kv{};          // the pool as [L*P*2*Hkv*block][hd] bf16 rows (TMA, box 64 x 16)
         hkd::DevTrie trie;
         int trie_tombs = 0;
         std::vector<int> free_slots;
@@ -308,6 +310,11 @@ hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m
         wk.layer_stride = page_bytes_layer * c.pages_per_worker;
         wk.kv = dalloc<uint8_t>(wk.layer_stride * L);
         HK_CUDA(cudaMemsetAsync(wk.kv, 0, wk.layer_stride * L, st));
+        if (!f32)
+            wk.tm_kv = hkd::make_tmap_2d_bf16(wk.kv, static_cast<uint64_t>(L) * c.pages_per_worker * 2 * Hkv * c.block_tokens,
+                                              static_cast<uint64_t>(hd), 64, c.block_tokens);
+        wk.counters = dalloc<int32_t>(static_cast<size_t>(c.max_calls * c.n_workers + 16) * Hkv);
+        HK_CUDA(cudaMemsetAsync(wk.counters, 0, static_cast<size_t>(c.max_calls * c.n_workers + 16) * Hkv * 4, st));
         wk.slot_last = dalloc<int32_t>(c.max_calls);
         HK_CUDA(cudaMemsetAsync(wk.slot_last, 0, c.max_calls * sizeof(int32_t), st));
         hkd::DevTrie& t = wk.trie;
@@ -356,6 +363,7 @@ hk_engine::~hk_engine() {
     for (auto& wk : workers) {
         cudaFree(wk.kv);
         cudaFree(wk.slot_last);
+        cudaFree(wk.counters);
         cudaFree(wk.trie.parent);
         cudaFree(wk.trie.page);
         cudaFree(wk.trie.phash);
@@ -532,9 +540,11 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         }
         t += s.count;
     }
-    // decode groups: maximal runs (in sorted order) sharing >= 1 full page
-    const int KS = 512;   // key split for shared ranges
-    const int KP = 1024;  // key split for private ranges
+    // decode groups: maximal runs (in sorted order) sharing >= 4 full pages
+    const int KS = 512;   // key split for shared ranges (fp32 path)
+    const int KP = 1024;  // key split for private ranges (fp32 path)
+    std::vector<hkd::DecodeRowIn> drows;
+    std::vector<hkd::DecodeGroupIn> dgroups;
     size_t gi = 0;
     while (gi < dec.size()) {
         size_t gj = gi + 1;
@@ -553,7 +563,8 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         const int shared_pages = members > 1 ? lcp : 0;
         const int shared_keys = shared_pages * block;
         const int tg0 = t;
-        // per-member rows + private items
+        dgroups.push_back(hkd::DecodeGroupIn{tg0 - T_pre, members, shared_pages});
+        // per-member rows (+ private items of the fp32 path)
         for (size_t q = gi; q < gj; ++q) {
             SegIn& s = segs[dec[q]];
             const int off = static_cast<int>(pages.size());
@@ -563,16 +574,19 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
             slots[t] = s.slot;
             kvw[t] = 1;
             ptab[t] = off;
+            drows.push_back(hkd::DecodeRowIn{off, s.start});
             const int r = t - T_pre;
-            int part = shared_keys > 0 ? (shared_keys + KS - 1) / KS : 0;
-            for (int k0 = shared_keys; k0 < s.start + 1; k0 += KP) {
-                const int k1 = std::min(k0 + KP, s.start + 1);
-                for (int kh = 0; kh < Hkv; ++kh) items_single.push_back(hkd::AttnItem{t, 1, kh, off, k0, k1, 0, part});
-                n_pv_items += Hkv;
-                ++part;
+            if (f32) {
+                int part = shared_keys > 0 ? (shared_keys + KS - 1) / KS : 0;
+                for (int k0 = shared_keys; k0 < s.start + 1; k0 += KP) {
+                    const int k1 = std::min(k0 + KP, s.start + 1);
+                    for (int kh = 0; kh < Hkv; ++kh) items_single.push_back(hkd::AttnItem{t, 1, kh, off, k0, k1, 0, part});
+                    n_pv_items += Hkv;
+                    ++part;
+                }
+                if (part > max_parts) throw std::runtime_error("engine: too many attention partials");
+                nparts[static_cast<size_t>(r)] = part;
             }
-            if (part > max_parts) throw std::runtime_error("engine: too many attention partials");
-            nparts[static_cast<size_t>(r)] = part;
             alg_single += (s.start + 1 - shared_keys) * kv_tok_bytes + 2.0 * H * hd * esz;
             if (s.sample) {
                 srows.push_back(t);
@@ -580,7 +594,7 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
             }
             ++t;
         }
-        if (shared_keys > 0) {
+        if (shared_keys > 0 && f32) {
             const int off0 = ptab[tg0];
             for (int r0 = tg0; r0 < t; r0 += 16) {
                 const int n = std::min(16, t - r0);
@@ -590,9 +604,14 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
                         items.push_back(hkd::AttnItem{r0, n, kh, off0, k0, std::min(k0 + KS, shared_keys), 0, part});
                 n_sh_items += Hkv * ((shared_keys + KS - 1) / KS);
             }
-            alg_bytes += shared_keys * kv_tok_bytes;
         }
+        if (shared_keys > 0) alg_bytes += shared_keys * kv_tok_bytes;
         gi = gj;
+    }
+    hkd::DecodePlan dplan;
+    if (!f32 && !dec.empty()) {
+        hkd::plan_decode_attention(drows, dgroups, H, Hkv, max_parts, hkd::g_num_sms, dplan);
+        nparts = dplan.n_parts;
     }
     const int S = static_cast<int>(srows.size());
     if (S > maxS) throw std::runtime_error("engine: too many sampled rows in one step");
@@ -606,7 +625,8 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     std::vector<int32_t> cmap(static_cast<size_t>(T), -1);  // batch row -> LM-head row
     for (int k = 0; k < S; ++k) cmap[static_cast<size_t>(srows[static_cast<size_t>(k)])] = k;
     const size_t words = 6 * static_cast<size_t>(T) + pages.size() + nparts.size() + 2 * static_cast<size_t>(S) +
-                         n_items * (sizeof(hkd::AttnItem) / 4) + 64;
+                         n_items * (sizeof(hkd::AttnItem) / 4) + dplan.sh.size() * (sizeof(hkd::ShItem) / 4) +
+                         dplan.pv.size() * (sizeof(hkd::PvItem) / 4) + 64;
     Meta& mt = meta[meta_next];
     meta_next = (meta_next + 1) % kMetaRing;
     if (mt.done) HK_CUDA(cudaEventSynchronize(mt.done));  // this slot's previous step has consumed it
@@ -641,7 +661,10 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
                  o_kvw = put(kvw.data(), T), o_ptab = put(ptab.data(), T),
                  o_np = put(nparts.data(), nparts.size()), o_sr = put(srows.data(), S), o_ss = put(sslots.data(), S),
                  o_items = put(reinterpret_cast<const int32_t*>(items.data()), n_items * sizeof(hkd::AttnItem) / 4),
-                 o_cmap = put(cmap.data(), cmap.size()), o_pages = put(pages.data(), pages.size());
+                 o_cmap = put(cmap.data(), cmap.size()),
+                 o_sh = put(reinterpret_cast<const int32_t*>(dplan.sh.data()), dplan.sh.size() * sizeof(hkd::ShItem) / 4),
+                 o_pv = put(reinterpret_cast<const int32_t*>(dplan.pv.data()), dplan.pv.size() * sizeof(hkd::PvItem) / 4),
+                 o_pages = put(pages.data(), pages.size());
     HK_CUDA(cudaMemcpyAsync(meta_d, meta_h, o * 4, cudaMemcpyHostToDevice, st));
     stats.h2d_bytes += o * 4;
     stats.steps += 1;
@@ -658,6 +681,8 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     const int32_t* d_cmap = meta_d + o_cmap;
     (void)o_sr;
     const hkd::AttnItem* d_items = reinterpret_cast<const hkd::AttnItem*>(meta_d + o_items);
+    const hkd::ShItem* d_sh = reinterpret_cast<const hkd::ShItem*>(meta_d + o_sh);
+    const hkd::PvItem* d_pv = reinterpret_cast<const hkd::PvItem*>(meta_d + o_pv);
     // items are packed pre | (per group: private..., shared...) — launch them as one grid
     (void)n_pre_items;
     (void)n_sh_items;
@@ -696,18 +721,39 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         clock.end(ck, st);
         hkd::AttnArgs aa{qkv, f32, H, Hkv, hd, block, d_pos, d_pages, kv_layer(w, l), d_items,
                          n_multi, attn, part_o, part_ml, max_parts, T_pre, scale, 0};
-        ck = clock.begin(dec.empty() ? 3 : 1, st);
-        hkd::attention_partial(aa, st);
-        clock.end(ck, st, alg_bytes);
-        aa.items = d_items + n_multi;
-        aa.n_items = static_cast<int>(n_items) - n_multi;
-        aa.single = 1;
-        ck = clock.begin(2, st);
-        hkd::attention_partial(aa, st);
-        clock.end(ck, st, alg_single);
-        ck = clock.begin(4, st);
-        hkd::attention_merge(part_o, part_ml, d_np, static_cast<int>(dec.size()), T_pre, H, hd, max_parts, attn, f32, st);
-        clock.end(ck, st);
+        if (f32) {
+            ck = clock.begin(dec.empty() ? 3 : 1, st);
+            hkd::attention_partial(aa, st);
+            clock.end(ck, st, alg_bytes);
+            aa.items = d_items + n_multi;
+            aa.n_items = static_cast<int>(n_items) - n_multi;
+            aa.single = 1;
+            ck = clock.begin(2, st);
+            hkd::attention_partial(aa, st);
+            clock.end(ck, st, alg_single);
+            ck = clock.begin(4, st);
+            hkd::attention_merge(part_o, part_ml, d_np, static_cast<int>(dec.size()), T_pre, H, hd, max_parts, attn,
+                                 f32, st);
+            clock.end(ck, st);
+        } else {
+            if (n_multi > 0) {  // prefill chunks (causal, written directly)
+                ck = clock.begin(3, st);
+                hkd::attention_partial(aa, st);
+                clock.end(ck, st, alg_bytes - dplan.shared_bytes);
+            }
+            if (!dplan.pv.empty()) {
+                hkd::DecodeAttnArgs da{static_cast<const bf16*>(qkv), H, Hkv, QKV,
+                                       static_cast<const bf16*>(kv_layer(w, l)),
+                                       static_cast<int>(static_cast<size_t>(l) * ec.pages_per_worker * 2 * Hkv * block),
+                                       d_pages, d_sh, static_cast<int>(dplan.sh.size()), dplan.sh_cluster, d_pv,
+                                       static_cast<int>(dplan.pv.size()), part_o, part_ml, max_parts, d_np,
+                                       wk.counters, T_pre, static_cast<bf16*>(attn), scale * 1.4426950408889634f, nullptr};
+                // one event bracket: the two grids overlap (private, then shared under PDL)
+                ck = clock.begin(1, st);
+                hkd::decode_attention(da, wk.tm_kv, st);
+                clock.end(ck, st, dplan.shared_bytes + dplan.private_bytes, 2);
+            }
+        }
         sp = gemm(lw.wo, attn, d, H * hd, T, hkd::kEpiPartial, pbuf, d);
         ck = clock.begin(5, st);
         hkd::add_rmsnorm(pbuf, sp, x, lw.mlp_norm, f32, T, d, eps, h, nullptr, nullptr, st);

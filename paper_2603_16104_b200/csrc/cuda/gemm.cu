@@ -368,10 +368,16 @@ EncodeTiledFn encode_fn() {
 }
 
 CUtensorMap make_map_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    return make_tmap_2d_bf16(base, rows, cols, BK, box_rows);
+}
+
+}  // namespace
+
+CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {cols, rows};
     const cuuint64_t strides[1] = {cols * 2};
-    const cuuint32_t box[2] = {BK, box_rows};
+    const cuuint32_t box[2] = {box_cols, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -379,6 +385,8 @@ CUtensorMap make_map_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return m;
 }
+
+namespace {
 
 template <int BN, int STAGES>
 constexpr size_t smem_bytes() {

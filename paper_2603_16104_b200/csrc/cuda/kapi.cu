@@ -1,5 +1,6 @@
 // Kernel-level C-ABI (include/helium_b200_kernels.h).
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "helium_b200_kernels.h"
@@ -10,6 +11,7 @@ void set_error(const std::string& s);
 }
 
 namespace {
+unsigned long long* g_trace = nullptr;  // hkx_decode_attention_trace target (device)
 float* g_ws = nullptr;
 size_t g_ws_floats = 0;
 
@@ -77,6 +79,106 @@ double hkx_gemm_bench(const void* W, const void* X, void* out, int N, int K, int
         hk::set_error(e.what());
         return -1;
     }
+}
+
+double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_rows, int H, int Hkv,
+                            const int32_t* tables, const int32_t* offs, const int32_t* pos, const int32_t* group_rows,
+                            const int32_t* group_shared_pages, int n_groups, void* out, int iters) {
+    void* bufs[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    try {
+        init_sms();
+        constexpr int kMaxParts = 32;
+        std::vector<hkd::DecodeRowIn> rows(static_cast<size_t>(n_rows));
+        for (int r = 0; r < n_rows; ++r) {
+            rows[static_cast<size_t>(r)] = hkd::DecodeRowIn{offs[r], pos[r]};
+            if ((pos[r] + 16) / 16 > offs[r + 1] - offs[r]) throw std::runtime_error("hkx_decode_attention: short table");
+            for (int k = offs[r]; k < offs[r + 1]; ++k)
+                if (tables[k] < 0 || tables[k] >= n_pages) throw std::runtime_error("hkx_decode_attention: bad page");
+        }
+        std::vector<hkd::DecodeGroupIn> groups;
+        int r0 = 0;
+        for (int g = 0; g < n_groups; ++g) {
+            groups.push_back(hkd::DecodeGroupIn{r0, group_rows[g], group_shared_pages[g]});
+            r0 += group_rows[g];
+        }
+        if (r0 != n_rows) throw std::runtime_error("hkx_decode_attention: groups do not cover the rows");
+        hkd::DecodePlan plan;
+        hkd::plan_decode_attention(rows, groups, H, Hkv, kMaxParts, hkd::g_num_sms, plan);
+        const size_t n_tab = static_cast<size_t>(offs[n_rows]);
+        const size_t b_tab = n_tab * 4, b_sh = plan.sh.size() * sizeof(hkd::ShItem),
+                     b_pv = plan.pv.size() * sizeof(hkd::PvItem), b_np = plan.n_parts.size() * 4;
+        HK_CUDA(cudaMalloc(&bufs[0], b_tab + b_sh + b_pv + b_np + 64));
+        uint8_t* m = static_cast<uint8_t*>(bufs[0]);
+        HK_CUDA(cudaMemcpy(m, tables, b_tab, cudaMemcpyHostToDevice));
+        const size_t o_sh = (b_tab + 15) / 16 * 16, o_pv = o_sh + b_sh, o_np = o_pv + b_pv;
+        if (b_sh) HK_CUDA(cudaMemcpy(m + o_sh, plan.sh.data(), b_sh, cudaMemcpyHostToDevice));
+        if (b_pv) HK_CUDA(cudaMemcpy(m + o_pv, plan.pv.data(), b_pv, cudaMemcpyHostToDevice));
+        HK_CUDA(cudaMemcpy(m + o_np, plan.n_parts.data(), b_np, cudaMemcpyHostToDevice));
+        const size_t n_part = static_cast<size_t>(n_rows) * H * kMaxParts;
+        HK_CUDA(cudaMalloc(&bufs[1], n_part * 128 * 4));
+        HK_CUDA(cudaMalloc(&bufs[2], n_part * 8));
+        HK_CUDA(cudaMalloc(&bufs[3], static_cast<size_t>(n_rows) * Hkv * 4));
+        HK_CUDA(cudaMemset(bufs[3], 0, static_cast<size_t>(n_rows) * Hkv * 4));
+        const CUtensorMap tm = hkd::make_tmap_2d_bf16(kv, static_cast<uint64_t>(n_pages) * 2 * Hkv * 16, 128, 64, 16);
+        hkd::DecodeAttnArgs a{static_cast<const hkd::bf16*>(qkv), H, Hkv, (H + 2 * Hkv) * 128,
+                              static_cast<const hkd::bf16*>(kv), 0, reinterpret_cast<const int32_t*>(m),
+                              reinterpret_cast<const hkd::ShItem*>(m + o_sh), static_cast<int>(plan.sh.size()), plan.sh_cluster,
+                              reinterpret_cast<const hkd::PvItem*>(m + o_pv), static_cast<int>(plan.pv.size()),
+                              static_cast<float*>(bufs[1]), static_cast<float2*>(bufs[2]), kMaxParts,
+                              reinterpret_cast<const int32_t*>(m + o_np), static_cast<int32_t*>(bufs[3]), 0,
+                              static_cast<hkd::bf16*>(out), 1.4426950408889634f / sqrtf(128.f), g_trace};
+        hkd::decode_attention(a, tm, nullptr);
+        HK_CUDA(cudaDeviceSynchronize());
+        double ms = 0;
+        if (iters > 0) {
+            cudaEvent_t e0, e1;
+            HK_CUDA(cudaEventCreate(&e0));
+            HK_CUDA(cudaEventCreate(&e1));
+            HK_CUDA(cudaEventRecord(e0));
+            for (int i = 0; i < iters; ++i) hkd::decode_attention(a, tm, nullptr);
+            HK_CUDA(cudaEventRecord(e1));
+            HK_CUDA(cudaEventSynchronize(e1));
+            float t = 0;
+            HK_CUDA(cudaEventElapsedTime(&t, e0, e1));
+            ms = t / iters;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
+        for (void* b : bufs) cudaFree(b);
+        return ms;
+    } catch (const std::exception& e) {
+        for (void* b : bufs) cudaFree(b);
+        hk::set_error(e.what());
+        return -1;
+    }
+}
+
+/* Phase timestamps (%globaltimer ns) of the next hkx_decode_attention calls:
+ * [n_sh + n_pv CTAs][8] into a device buffer of `words` u64 (NULL = off). */
+int hkx_decode_attention_trace(void* device_buf) {
+    g_trace = static_cast<unsigned long long*>(device_buf);
+    return 0;
+}
+
+/* algorithmic bytes of the same call (shared KV once per group + private KV + q/o) */
+double hkx_decode_attention_bytes(int n_rows, int H, int Hkv, const int32_t* offs, const int32_t* pos,
+                                  const int32_t* group_rows, const int32_t* group_shared_pages, int n_groups) {
+    std::vector<hkd::DecodeRowIn> rows(static_cast<size_t>(n_rows));
+    for (int r = 0; r < n_rows; ++r) rows[static_cast<size_t>(r)] = hkd::DecodeRowIn{offs[r], pos[r]};
+    std::vector<hkd::DecodeGroupIn> groups;
+    int r0 = 0;
+    for (int g = 0; g < n_groups; ++g) {
+        groups.push_back(hkd::DecodeGroupIn{r0, group_rows[g], group_shared_pages[g]});
+        r0 += group_rows[g];
+    }
+    hkd::DecodePlan plan;
+    try {
+        hkd::plan_decode_attention(rows, groups, H, Hkv, 32, 148, plan);
+    } catch (const std::exception& e) {
+        hk::set_error(e.what());
+        return -1;
+    }
+    return plan.shared_bytes + plan.private_bytes;
 }
 
 }  // extern "C"

@@ -3,6 +3,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 #include "common.cuh"
 
@@ -26,6 +27,8 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
 // ids[t] = argmax over the n_tiles (max, idx) partials of kEpiArgmax (lowest index wins ties)
 void argmax_reduce(const float2* part, int n_tiles, int T, int32_t* ids, const int32_t* slots, int32_t* slot_last,
                    cudaStream_t st);
+// 2D bf16 tensor map [rows][cols] (row stride cols*2 B), box {box_cols, box_rows}, 128B swizzle
+CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows);
 void gemm_f32(const float* W, const float* X, int N, int K, int T, int epi, void* out, int ldo, const float* bias,
               cudaStream_t st);
 
@@ -108,6 +111,79 @@ void attention_partial(const AttnArgs& a, cudaStream_t st);
 // out[tok0 + r][h] = merge of the n_parts[r] partials of row r, r < n_rows
 void attention_merge(const float* part_o, const float2* part_ml, const int32_t* n_parts, int n_rows, int tok0, int H,
                      int hd, int max_parts, void* out, bool f32, cudaStream_t st);
+
+// --------------------------------------------------------- decode_attn.cu
+// K3b (bf16): decode attention of one ragged step, one launch pair per layer.
+//   * shared items (tcgen05): 128 MMA rows = (token, q-head) pairs of up to
+//     128/G decode tokens sharing a block-table prefix x one kv head x a range
+//     of whole shared pages; the shared KV is read once for all those rows;
+//   * private items (CUDA cores): one decode token x one kv head x its own
+//     pages (suffix + generated tokens).
+// The shared items of one (rows, kv head) tile form a thread-block cluster
+// that combines its page ranges through DSMEM into one flash partial (m, l,
+// unnormalised o); private items leave one partial each. The last contributor
+// of a (token, kv head) merges its partials (a per-(row, kv head) arrival
+// counter) and writes the bf16 output, so no separate merge launch exists.
+struct ShItem {
+    int row0;    // first decode row
+    int ntok;    // decode rows covered (<= 128 / G)
+    int kvh;
+    int ptab;    // block table (arena offset) of the group's first member
+    int page0;   // first shared page (index into the table)
+    int npages;  // shared pages covered by this item (may be 0)
+    int rank;    // rank in the cluster of items covering the same rows (all pages of the group)
+    int pad;
+};
+struct PvItem {
+    int row;     // decode row
+    int kvh;
+    int ptab;
+    int kbeg;    // key range [kbeg, kend), kbeg page aligned
+    int kend;
+    int part;    // partial index, -1 = sole contributor: write the output directly
+    int pad0, pad1;
+};
+struct DecodeAttnArgs {
+    const bf16* qkv;        // [T][QKV]
+    int H, Hkv, QKV;
+    const bf16* kv_layer;   // this layer's pool [P][2][Hkv][16][128]
+    int layer_row0;         // first row of this layer in the pool tensor map
+    const int32_t* pages;   // page arena
+    const ShItem* sh;
+    int n_sh;
+    int sh_cluster;         // CTAs per shared cluster (items of one tile are consecutive)
+    const PvItem* pv;
+    int n_pv;
+    float* part_o;          // [rows][H][max_parts][128]
+    float2* part_ml;        // [rows][H][max_parts] (m, l), log2 units
+    int max_parts;
+    const int32_t* n_parts; // [rows] partials per (row, kv head)
+    int32_t* counters;      // [rows][Hkv], zero between launches
+    int dec_tok0;           // batch token of decode row 0
+    bf16* out;              // [T][H][128]
+    float sl2;              // softmax scale * log2(e)
+    unsigned long long* trace;  // optional [n_sh + n_pv][8] %globaltimer stamps per CTA phase (null = off)
+};
+// Host planning of one step's decode rows. Rows of a group are consecutive
+// and share `shared_pages` leading pages of their block tables.
+struct DecodeRowIn {
+    int ptab;  // block table offset in the arena
+    int pos;   // position of the decode token (keys [0, pos] are attended)
+};
+struct DecodeGroupIn {
+    int row0, members, shared_pages;
+};
+struct DecodePlan {
+    std::vector<ShItem> sh;
+    std::vector<PvItem> pv;
+    std::vector<int32_t> n_parts;
+    int sh_cluster = 1;
+    double shared_bytes = 0, private_bytes = 0;  // algorithmic KV bytes (+ Q/O) per layer
+};
+void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vector<DecodeGroupIn>& groups, int H,
+                           int Hkv, int max_parts, int num_sms, DecodePlan& plan);
+// tm_kv: the worker's whole pool as a [L*P*2*Hkv*16][128] bf16 tensor map, box {64, 16}.
+void decode_attention(const DecodeAttnArgs& a, const CUtensorMap& tm_kv, cudaStream_t st);
 
 // ------------------------------------------------------------------ pool.cu
 // K1: page-granular moves of whole KV pages (all layers) inside one pool.

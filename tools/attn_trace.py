@@ -1,0 +1,61 @@
+"""Per-CTA phase timeline of the decode attention kernels (debug: %globaltimer stamps)."""
+import ctypes as C
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tests"))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2603_16104_b200 import _lib  # noqa: E402
+from test_gpu_decode_attn import make_case, run  # noqa: E402
+
+
+def warm_gpu(seconds=0.5):
+    """Bring SM clocks up before timing short kernels."""
+    import time
+    import torch
+    x = torch.randn(4096, 4096, device="cuda", dtype=torch.bfloat16)
+    t = time.time()
+    while time.time() - t < seconds:
+        for _ in range(20):
+            x = (x @ x).clamp_(-1, 1)
+        torch.cuda.synchronize()
+
+
+warm_gpu()
+
+k = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+case = make_case(32, 8, [(64, 128, [16 + k] * 64)], seed=1)
+run(case, iters=3)  # warm
+buf = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
+_lib.load().hkx_decode_attention_trace(C.c_void_p(buf.data_ptr()))
+run(case)
+_lib.load().hkx_decode_attention_trace(None)
+t = buf.view(-1, 16).cpu().numpy().astype(np.float64)
+n_sh = int((t[:, 0] > 0).sum()) - int((t[:, 0] > 0).sum() - 0)  # placeholder
+n_sh = int(sys.argv[2]) if len(sys.argv) > 2 else 128
+sh = t[:n_sh]
+pv = t[n_sh:][t[n_sh:, 0] > 0]
+t0 = min(sh[:, 0].min(), pv[:, 0].min())
+us = lambda x: (x - t0) / 1e3
+print(f"k={k}: private CTAs {len(pv)}: start {us(pv[:,0]).min():.1f}..{us(pv[:,0]).max():.1f} us, "
+      f"warp-0 item done {us(pv[:,2]).min():.1f}..{us(pv[:,2]).max():.1f} (mean item {((pv[:,2]-pv[:,1])/1e3).mean():.2f} us)")
+pvo = [(1, "pdl/trigger"), (3, "page0 landed"), (2, "pages done"), (4, "partial out"), (5, "atomic"), (6, "merged")]
+for (i0, n0), (i1, n1) in zip(pvo[:-1], pvo[1:]):
+    d = (pv[:, i1] - pv[:, i0]) / 1e3
+    print(f"  private {n0:>12s} -> {n1:<12s} mean {d.mean():6.2f} us  max {d.max():6.2f}")
+print(f"shared CTAs {n_sh}: start {us(sh[:,0]).min():.1f}..{us(sh[:,0]).max():.1f} us")
+# stamp order within a shared CTA
+order = [(0, "start"), (1, "tmem+bars"), (2, "q in smem"), (7, "S0 ready"), (8, "P0 written"), (3, "O done"),
+         (4, "partial out"), (5, "merge")]
+prev = None
+for idx, name in order:
+    if prev is not None:
+        d = (sh[:, idx] - sh[:, prev[0]]) / 1e3
+        print(f"  {prev[1]:>14s} -> {name:<14s} mean {d.mean():7.2f} us  max {d.max():7.2f}")
+    prev = (idx, name)
+mhz = (sh[:, 15] - sh[:, 14]) / (sh[:, 5] - sh[:, 0]) * 1e3
+print(f"  SM clock inside shared CTAs: {mhz.mean():.0f} MHz")
+print(f"  end of last shared CTA {us(sh[:,5]).max():.1f} us; end of last private {us(pv[:,2]).max():.1f}")
