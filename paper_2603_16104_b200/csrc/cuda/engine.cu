@@ -348,6 +348,7 @@ hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m
     ws = dalloc<float>(ws_floats);
     pbuf_floats = std::max(static_cast<size_t>(maxT) * std::max(QKV, d) * 2, static_cast<size_t>(16) * 512 * std::max(QKV, d));
     pbuf = dalloc<float>(pbuf_floats);
+    if (!f32) hkd::gemm_streamk_reserve(std::max((V + 127) / 128, 4096), 64);
     hs = dalloc<uint8_t>(static_cast<size_t>(maxS) * d * esz);
     amax = dalloc<float2>(static_cast<size_t>((V + 127) / 128) * maxS);
     max_part_rows = static_cast<int>(c.max_calls * c.n_workers) + 16;

@@ -433,6 +433,14 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
               float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits, int max_splits) {
     if (T <= 0) return 0;
     if (K % BK != 0) throw std::runtime_error("gemm_bf16: K must be a multiple of 64");
+    // Stream-K pays off for the long LM-head contraction (1,002 vocab tiles:
+    // ~7 whole tiles per SM, 97% of HBM peak measured); the per-layer GEMMs
+    // keep split-K partials reduced by their consumer row kernels, which
+    // measured faster (tools/gemm_sweep.py, profiles/).
+    if (T <= 64 && epi == kEpiArgmax && force_splits == 0 && bias == nullptr && gemm_streamk_enabled()) {
+        gemm_bf16_streamk(W, X, N, K, T, epi, out, ldo, st);
+        return 1;  // fully reduced
+    }
     int BN;
     if (T <= 16)
         BN = 16;

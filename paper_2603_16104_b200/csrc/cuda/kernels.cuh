@@ -24,6 +24,13 @@ extern unsigned long long g_launches;  // kernels launched by this library (all 
 // max_splits bounds it). Other epilogues reduce split partials through `workspace`.
 int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, const bf16* bias,
               float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits = 0, int max_splits = 16);
+// Stream-K variant for decode shapes (T <= 64): one CTA per SM over equal
+// shares of (128-row tile, 64-k) units; the result is fully reduced (no
+// split-K partials): kEpiPartial/kEpiStoreF32 write fp32 [T][ldo].
+void gemm_bf16_streamk(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, cudaStream_t st);
+bool gemm_streamk_enabled();
+// allocate the stream-K workspace/counters ahead of any CUDA-graph capture
+void gemm_streamk_reserve(int max_tiles, int max_bn);
 // ids[t] = argmax over the n_tiles (max, idx) partials of kEpiArgmax (lowest index wins ties)
 void argmax_reduce(const float2* part, int n_tiles, int T, int32_t* ids, const int32_t* slots, int32_t* slot_last,
                    cudaStream_t st);

@@ -97,9 +97,19 @@ def test_gemm_argmax_epilogue(T):
     torch.cuda.synchronize()
     lv = logits.view(T, V // 128, 128)
     mx, ix = lv.max(dim=-1)
-    assert torch.equal(part[..., 0].t(), mx)
+    # the stream-K LM-head path may sum a vocab tile's k-segments in another
+    # (fixed, deterministic) order than the single-accumulator reference
+    assert torch.allclose(part[..., 0].t(), mx, rtol=1e-5, atol=1e-5)
     idx = part[..., 1].contiguous().view(torch.int32).t()
-    assert torch.equal(idx.long(), ix + torch.arange(V // 128, device="cuda") * 128)
+    top2 = lv.topk(2, dim=-1).values
+    clear = (top2[..., 0] - top2[..., 1]) > 1e-3
+    ref = ix + torch.arange(V // 128, device="cuda") * 128
+    assert torch.equal(idx.long()[clear], ref[clear])
+    # and the path is deterministic run to run
+    part2 = torch.zeros_like(part)
+    assert lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(part2), V, K, T, 5, None, 0, None) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(part, part2)
 
 
 def test_gemm_deterministic():

@@ -1,0 +1,3 @@
+timeout -s KILL 600 python -m pytest tests/test_gpu_kernels.py -q -x --timeout 300 2>&1 | tail -3
+echo "## stream-K (default)"; python tools/gemm_sweep.py 64
+echo "## previous split-K path"; HK_GEMM_NO_STREAMK=1 python tools/gemm_sweep.py 64
