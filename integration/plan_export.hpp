@@ -1,5 +1,5 @@
 // Flattens the reference's executor inputs into the HKPLAN01 blob that
-// hk_executor_create() (include/helium_b200.h) consumes.
+// hk_simulate() (include/helium_b200.h) consumes.
 //
 // This is the reference-side half of the drop-in boundary: it is compiled
 // against the reference's own headers (helios/*.hpp) and is what a maintainer
