@@ -1,5 +1,6 @@
 // K5: row-wise ops of the decoder (embedding gather, RMSNorm, RoPE + paged KV
 // write, SwiGLU, greedy argmax) and the counter-based weight init.
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -252,9 +253,19 @@ __global__ void qkv_rope_kv_kernel(QkvArgs a) {
         c1 = c0 + 1;
     }
     float x0 = 0.f, x1 = 0.f;
-    for (int s = 0; s < a.splits; ++s) {
-        x0 += src[s * tstride + c0];
-        x1 += src[s * tstride + c1];
+    for (int s0 = 0; s0 < a.splits; s0 += 8) {
+        float p0[8], p1[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            const bool ok = s0 + s < a.splits;
+            p0[s] = ok ? __ldcg(src + (s0 + s) * tstride + c0) : 0.f;
+            p1[s] = ok ? __ldcg(src + (s0 + s) * tstride + c1) : 0.f;
+        }
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {  // fixed split order: deterministic
+            x0 += p0[s];
+            x1 += p1[s];
+        }
     }
     if (a.bias) {
         if (sizeof(T) == 4) {
@@ -298,7 +309,11 @@ __global__ void qkv_rope_kv_kernel(QkvArgs a) {
     }
 }
 
-// Row kernel, 256 threads, row held in registers (d <= 8192).
+// Row kernel spread over a thread-block cluster: the RS CTAs of cluster
+// (token t) each own d / RS consecutive features (one float4 per thread),
+// load the residual and every split-K partial with all loads in flight, and
+// exchange their partial sums of squares through distributed shared memory.
+constexpr int kRowSplit = 8;
 template <typename T>
 __global__ void __launch_bounds__(256) add_rmsnorm_kernel(const float* __restrict__ part, int splits, float* x,
                                                           const T* __restrict__ w, int T_, int d, float eps, T* h,
@@ -307,58 +322,65 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(const float* __restric
     pdl_wait();
     const int t = blockIdx.x;
     const int n4 = d / 4;
-    float4 v[8];
-    float ss = 0.f;
+    const int i = blockIdx.y * blockDim.x + threadIdx.x;  // float4 index within the row
+    const bool ok = i < n4;
     float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(t) * d);
     const size_t pstride = static_cast<size_t>(T_) * d / 4;
     const float4* pr = reinterpret_cast<const float4*>(part) + static_cast<size_t>(t) * d / 4;
+    float4 v = ok ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < splits; s0 += 8) {
+        float4 b[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int i = threadIdx.x + k * 256;
-        if (i < n4) {
-            float4 a = xr[i];
-            for (int s = 0; s < splits; ++s) {
-                const float4 b = pr[s * pstride + i];
-                a.x += b.x;
-                a.y += b.y;
-                a.z += b.z;
-                a.w += b.w;
-            }
-            v[k] = a;
-            ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+        for (int s = 0; s < 8; ++s)
+            b[s] = (ok && s0 + s < splits) ? __ldcg(pr + (s0 + s) * pstride + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {  // fixed split order: deterministic
+            v.x += b[s].x;
+            v.y += b[s].y;
+            v.z += b[s].z;
+            v.w += b[s].w;
         }
     }
+    float ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
     __shared__ float red[8];
+    __shared__ float cta_sum;
     ss = warp_sum(ss);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
     __syncthreads();
+    if (threadIdx.x == 0) {
+        float a = 0.f;
+        for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) a += red[k];
+        cta_sum = a;
+    }
+    cluster_sync_all();
     float tot = 0.f;
+    {
+        float pv[kRowSplit];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) tot += red[k];
+        for (int q = 0; q < kRowSplit; ++q) pv[q] = ld_dsmem_f32(mapa_shared(smem_u32(&cta_sum), q));
+#pragma unroll
+        for (int q = 0; q < kRowSplit; ++q) tot += pv[q];  // rank order: every CTA gets the same total
+    }
     const float inv = rsqrtf(tot / static_cast<float>(d) + eps);
     const int cr = cmap ? cmap[t] : -1;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int i = threadIdx.x + k * 256;
-        if (i < n4) {
-            if (splits > 0) xr[i] = v[k];
-            const float4 a = v[k];
-            const float o0 = a.x * inv * ld(w + 4 * i), o1 = a.y * inv * ld(w + 4 * i + 1),
-                        o2 = a.z * inv * ld(w + 4 * i + 2), o3 = a.w * inv * ld(w + 4 * i + 3);
-            T* hr = h + static_cast<size_t>(t) * d + 4 * i;
-            hr[0] = cvt<T>(o0);
-            hr[1] = cvt<T>(o1);
-            hr[2] = cvt<T>(o2);
-            hr[3] = cvt<T>(o3);
-            if (cr >= 0) {
-                T* hcr = hc + static_cast<size_t>(cr) * d + 4 * i;
-                hcr[0] = cvt<T>(o0);
-                hcr[1] = cvt<T>(o1);
-                hcr[2] = cvt<T>(o2);
-                hcr[3] = cvt<T>(o3);
-            }
+    if (ok) {
+        if (splits > 0) xr[i] = v;
+        const float o0 = v.x * inv * ld(w + 4 * i), o1 = v.y * inv * ld(w + 4 * i + 1),
+                    o2 = v.z * inv * ld(w + 4 * i + 2), o3 = v.w * inv * ld(w + 4 * i + 3);
+        T* hr = h + static_cast<size_t>(t) * d + 4 * i;
+        if constexpr (sizeof(T) == 2) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(o0, o1), hi = __floats2bfloat162_rn(o2, o3);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&lo);
+            pk.y = *reinterpret_cast<uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(hr) = pk;
+            if (cr >= 0) *reinterpret_cast<uint2*>(hc + static_cast<size_t>(cr) * d + 4 * i) = pk;
+        } else {
+            *reinterpret_cast<float4*>(hr) = make_float4(o0, o1, o2, o3);
+            if (cr >= 0) *reinterpret_cast<float4*>(hc + static_cast<size_t>(cr) * d + 4 * i) = make_float4(o0, o1, o2, o3);
         }
     }
+    cluster_sync_all();  // peers read cta_sum: keep it alive until everyone has
 }
 
 }  // namespace
@@ -389,13 +411,29 @@ void qkv_rope_kv(const QkvArgs& a, cudaStream_t st) {
 void add_rmsnorm(const float* part, int splits, float* x, const void* w, bool f32, int T, int d, float eps, void* h,
                  const int32_t* cmap, void* hc, cudaStream_t st) {
     if (!T) return;
-    if (d % 4 || d > 8192) throw std::runtime_error("add_rmsnorm: d must be a multiple of 4 and <= 8192");
+    if (d % 4 || d > 8192 * 4) throw std::runtime_error("add_rmsnorm: d must be a multiple of 4");
+    const int per = (d / 4 + kRowSplit - 1) / kRowSplit;          // float4 per CTA
+    const int threads = std::max(32, (per + 31) / 32 * 32);
+    if (threads > 256) throw std::runtime_error("add_rmsnorm: d too large");
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(T, kRowSplit);
+    cfg.blockDim = dim3(threads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 1;
+    attr[1].val.clusterDim.y = kRowSplit;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
     if (f32)
-        launch_pdl(add_rmsnorm_kernel<float>, dim3(T), dim3(256), 0, st, part, splits, x, static_cast<const float*>(w),
-                   T, d, eps, static_cast<float*>(h), cmap, static_cast<float*>(hc));
+        HK_CUDA(cudaLaunchKernelEx(&cfg, add_rmsnorm_kernel<float>, part, splits, x, static_cast<const float*>(w), T, d,
+                                   eps, static_cast<float*>(h), cmap, static_cast<float*>(hc)));
     else
-        launch_pdl(add_rmsnorm_kernel<bf16>, dim3(T), dim3(256), 0, st, part, splits, x, static_cast<const bf16*>(w), T,
-                   d, eps, static_cast<bf16*>(h), cmap, static_cast<bf16*>(hc));
+        HK_CUDA(cudaLaunchKernelEx(&cfg, add_rmsnorm_kernel<bf16>, part, splits, x, static_cast<const bf16*>(w), T, d,
+                                   eps, static_cast<bf16*>(h), cmap, static_cast<bf16*>(hc)));
     HK_LAUNCHED(1);
 }
 
