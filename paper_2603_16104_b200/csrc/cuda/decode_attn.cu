@@ -33,6 +33,7 @@
 // next kernel's griddepcontrol.wait covers both.
 #include <algorithm>
 #include <cfloat>
+#include <cmath>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -182,12 +183,7 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 template <int G>
-__global__ void __launch_bounds__(SH_THREADS, 1) attn_shared_tc_kernel(const __grid_constant__ CUtensorMap tm_kv,
-                                                                       DecodeAttnArgs a) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // stay in the shared address space (pointer arithmetic on the array) so
-    // plain stores compile to STS
-    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+__device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const DecodeAttnArgs& a, uint8_t* sm) {
     uint8_t* sQ = sm;
     uint8_t* sKV = sm + SQ_BYTES;  // stage b: K at b*2*SKV_BYTES, V at +SKV_BYTES
     uint8_t* sP = sKV + 4 * SKV_BYTES;
@@ -428,24 +424,6 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_shared_tc_kernel(const __g
             if (lane == 0) a.part_ml[pi] = make_float2(red_mx[2 * ROWS + r], red_l[r] + red_l[ROWS + r]);
         }
         stamp(a, blockIdx.x, 4);
-        // ---- arrival counters: the last contributor of a (token, kv head) merges it
-        int* mlist = flags;  // tokens to merge, compacted
-        if (tid == 0) flags[ROWS] = 0;
-        named_bar(1, 256);
-        if (tid < it.ntok) {
-            const int r = it.row0 + tid;
-            if (arrive_acq_rel(&a.counters[r * a.Hkv + it.kvh]) == a.n_parts[r] - 1) mlist[atomicAdd(&flags[ROWS], 1)] = tid;
-        }
-        named_bar(1, 256);
-        const int nm = flags[ROWS] * G;  // (token, head) pairs to merge, spread over the 8 warps
-        const int per = (nm + 7) / 8;
-        merge_pairs(a, max(0, min(per, nm - warp * per)), [&](int i, int& r, int& h) {
-            const int q = warp * per + i;
-            r = it.row0 + mlist[q / G];
-            h = it.kvh * G + q % G;
-        });
-        named_bar(1, 256);
-        if (tid < flags[ROWS]) a.counters[(it.row0 + mlist[tid]) * a.Hkv + it.kvh] = 0;
         stamp(a, blockIdx.x, 5);
     }
     tc_fence_before();
@@ -463,9 +441,7 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_shared_tc_kernel(const __g
 // with ldmatrix from TMA-swizzled page tiles (conflict-free). The warp feeds
 // itself: lane 0 keeps PV_ST pages (4 TMA boxes each) in flight in the warp's
 // own ring and refills a stage as soon as the warp has read it.
-constexpr int PV_WARPS = 4;
-constexpr int PV_ST = 3;
-constexpr int PV_SMEM = 1024 + PV_WARPS * PV_ST * 8192 + PV_WARPS * PV_ST * 8 + 64;
+constexpr int PV_ST = 3;  // pages in flight per private warp
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -490,43 +466,24 @@ __device__ __forceinline__ uint32_t tile_off(int row, int c) {
     return static_cast<uint32_t>((c >> 3) * 2048 + row * 128 + (((c & 7) ^ (row & 7)) << 4));
 }
 
+// One private item with the calling warp. ring / full: the warp's PV_ST
+// stages (8 KB each) and their mbarriers; pc counts the pages this warp has
+// already pushed through the ring (mbarrier phase bookkeeping).
 template <int G>
-__global__ void __launch_bounds__(PV_WARPS * 32, 2) attn_private_kernel(const __grid_constant__ CUtensorMap tm_kv,
-                                                                        DecodeAttnArgs a) {
-    static_assert(G <= 8, "private kernel: G q-heads must fit rows 0-7 of the MMA tile");
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + PV_WARPS * PV_ST * 8192);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+__device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const DecodeAttnArgs& a, const PvItem& it,
+                                             uint8_t* ring, uint64_t* full, int& pc) {
+    static_assert(G <= 8, "private item: G q-heads must fit rows 0-7 of the MMA tile");
+    const int lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
-    const int ii = blockIdx.x * PV_WARPS + warp;
-    if (lane == 0) {
-        for (int s = 0; s < PV_ST; ++s) mbar_init(&full[warp * PV_ST + s], 1);
-        fence_barrier_init();
-        tma_prefetch_desc(&tm_kv);
-    }
-    __syncwarp();
-    stamp(a, a.n_sh + blockIdx.x, 0);
-    // q and this token's own K/V come from the qkv/RoPE kernel: when a shared
-    // grid runs first it has waited for that kernel before letting us launch.
-    if (a.n_sh == 0) pdl_wait();
-    pdl_trigger();  // the next kernel (O projection) may start prefetching its weights
-    stamp(a, a.n_sh + blockIdx.x, 1);
-    if (ii >= a.n_pv) {
-        pdl_wait();
-        return;
-    }
-    const PvItem it = a.pv[ii];
     const int p0 = it.kbeg / PG;
     const int np = (it.kend - it.kbeg + PG - 1) / PG;
-    uint8_t* ring = sm + warp * PV_ST * 8192;
     const uint32_t ring_s = smem_u32(ring);
     const int rows_per_head = a.Hkv * PG;
     // page ids of the item (np <= 32 for this kernel's key splits), one per lane
     const int my_page = lane < np ? a.pages[it.ptab + p0 + lane] : 0;
     auto issue = [&](int i, int page) {  // lane 0 only: K (2 boxes) + V (2 boxes)
-        const int s = i % PV_ST;
-        uint64_t* bar = &full[warp * PV_ST + s];
+        const int s = (pc + i) % PV_ST;
+        uint64_t* bar = &full[s];
         uint8_t* dst = ring + s * 8192;
         const int rk = a.layer_row0 + (page * 2 * a.Hkv + it.kvh) * PG;
         mbar_expect_tx(bar, 8192);
@@ -557,9 +514,8 @@ __global__ void __launch_bounds__(PV_WARPS * 32, 2) attn_private_kernel(const __
     // ldmatrix lane roles: matrix mi = lane / 8, row within it rr = lane % 8
     const int mi = lane >> 3, rr = lane & 7;
     for (int i = 0; i < np; ++i) {
-        const int s = i % PV_ST;
-        mbar_wait(&full[warp * PV_ST + s], (i / PV_ST) & 1);
-        if (i == 0 && warp == 0) stamp(a, a.n_sh + blockIdx.x, 3);
+        const int s = (pc + i) % PV_ST;
+        mbar_wait(&full[s], ((pc + i) / PV_ST) & 1);
         const uint32_t kt = ring_s + s * 8192, vt = kt + 4096;
         // S = Q K^T: two n-tiles of 8 keys
         float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -615,9 +571,9 @@ __global__ void __launch_bounds__(PV_WARPS * 32, 2) attn_private_kernel(const __
         const int pg = __shfl_sync(0xffffffffu, my_page, (i + PV_ST) & 31);
         if (lane == 0 && i + PV_ST < np) issue(i + PV_ST, pg);
     }
+    pc += np;
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
-    if (warp == 0) stamp(a, a.n_sh + blockIdx.x, 2);
     const bool vrow = gid < G;
     if (it.part < 0) {
         if (vrow) {
@@ -626,7 +582,6 @@ __global__ void __launch_bounds__(PV_WARPS * 32, 2) attn_private_kernel(const __
 #pragma unroll
             for (int j = 0; j < 16; ++j) *reinterpret_cast<uint32_t*>(op + j * 8) = pack2(o[j][0] * inv, o[j][1] * inv);
         }
-        pdl_wait();
         return;
     }
     if (vrow) {
@@ -636,39 +591,177 @@ __global__ void __launch_bounds__(PV_WARPS * 32, 2) attn_private_kernel(const __
         for (int j = 0; j < 16; ++j) *reinterpret_cast<float2*>(po + j * 8) = make_float2(o[j][0], o[j][1]);
         if (tig == 0) a.part_ml[pi] = make_float2(m_run, l_run);
     }
-    if (warp == 0) stamp(a, a.n_sh + blockIdx.x, 4);
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) last = arrive_acq_rel(&a.counters[it.row * a.Hkv + it.kvh]) == a.n_parts[it.row] - 1;
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (warp == 0) stamp(a, a.n_sh + blockIdx.x, 5);
-    if (last) {
-        __syncwarp();
-        merge_pairs(a, G, [&](int q, int& r, int& h) {
-            r = it.row;
-            h = it.kvh * G + q;
-        });
-        if (lane == 0) a.counters[it.row * a.Hkv + it.kvh] = 0;
+}
+
+// out[row][head] = merge of the row's n_parts partials. A 16-lane group per
+// (row, head), lane owns 8 dims; the part count, every (m, l) and every part's
+// 8 dims of a batch of 8 parts are loaded at once (one memory round trip);
+// unused slots are masked, never multiplied (they may hold stale bits).
+// All 32 lanes of the warp must call it (two pairs per warp).
+__device__ __forceinline__ void merge16(const DecodeAttnArgs& a, int pair, int n_pairs) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31, sub = lane & 15;
+    const bool active = pair < n_pairs;
+    const int row = active ? pair / a.H : 0, head = active ? pair % a.H : 0;
+    const int np = active ? a.n_parts[row] : 0;
+    const size_t base = (static_cast<size_t>(row) * a.H + head) * a.max_parts;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float M = -INFINITY, L = 0.f;
+    for (int k0 = 0; k0 < a.max_parts; k0 += 8) {
+        if (!__any_sync(full, k0 < np)) break;
+        const float2 ml = sub < 8 ? __ldcg(&a.part_ml[base + k0 + sub]) : make_float2(-INFINITY, 0.f);
+        float4 v[8][2];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float4* src = reinterpret_cast<const float4*>(a.part_o + (base + k0 + k) * HD) + sub * 2;
+            v[k][0] = __ldcg(src);
+            v[k][1] = __ldcg(src + 1);
+        }
+        const bool mine = sub < 8 && k0 + sub < np;
+        float mx = mine ? ml.x : -INFINITY;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(full, mx, o));
+        const float Mn = fmaxf(M, mx);
+        const float sc = M == -INFINITY ? 0.f : exp2f(M - Mn);  // rescale the previous batches
+        const float w = mine ? exp2f(ml.x - Mn) : 0.f;
+        float lw = mine ? w * ml.y : 0.f;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) lw += __shfl_xor_sync(full, lw, o);
+        L = L * sc + lw;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] *= sc;
+        const int g0 = lane & 16;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float wk = __shfl_sync(full, w, g0 + k);
+            if (k0 + k < np) {
+                acc[0] += wk * v[k][0].x;
+                acc[1] += wk * v[k][0].y;
+                acc[2] += wk * v[k][0].z;
+                acc[3] += wk * v[k][0].w;
+                acc[4] += wk * v[k][1].x;
+                acc[5] += wk * v[k][1].y;
+                acc[6] += wk * v[k][1].z;
+                acc[7] += wk * v[k][1].w;
+            }
+        }
+        M = Mn;
     }
-    if (warp == 0) stamp(a, a.n_sh + blockIdx.x, 6);
-    pdl_wait();  // complete only after the shared grid: the next kernel's wait covers both
+    if (!active || np <= 1) return;
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    uint4 w4;
+    w4.x = pack2(acc[0] * inv, acc[1] * inv);
+    w4.y = pack2(acc[2] * inv, acc[3] * inv);
+    w4.z = pack2(acc[4] * inv, acc[5] * inv);
+    w4.w = pack2(acc[6] * inv, acc[7] * inv);
+    *reinterpret_cast<uint4*>(a.out + (static_cast<size_t>(a.dec_tok0 + row) * a.H + head) * HD + sub * 8) = w4;
+}
+
+// Fallback merge launch (when the attention grid exceeds one CTA per SM).
+__global__ void __launch_bounds__(256) attn_merge_rows_kernel(DecodeAttnArgs a, int n_pairs) {
+    pdl_trigger();
+    pdl_wait();
+    merge16(a, (blockIdx.x * blockDim.x + threadIdx.x) >> 4, n_pairs);
+}
+
+// ------------------------------------------------------------ the kernel
+// One CTA per SM (persistent). CTA b < n_sh first streams shared item b on
+// the tensor cores (all 10 warps); then warps 0-7 of every CTA pull private
+// items from a global queue until it is empty, each with its own TMA ring in
+// the (now free) shared memory. No SM waits for another's phase.
+constexpr int DA_PV_WARPS = 8;
+constexpr int DA_SMEM = SH_SMEM + 256;
+
+template <int G>
+__global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid_constant__ CUtensorMap tm_kv,
+                                                                    DecodeAttnArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // stay in the shared address space (pointer arithmetic on the array) so
+    // plain stores compile to STS
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    pdl_trigger();  // the next kernel (O projection) may launch; it waits for us before reading
+    if (blockIdx.x < a.n_sh) {
+        shared_phase<G>(tm_kv, a, sm);
+    } else {
+        stamp(a, blockIdx.x, 0);
+        pdl_wait();  // q and this step's own K/V come from the qkv/RoPE kernel
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp >= DA_PV_WARPS) return;
+    uint8_t* ring = sm + warp * PV_ST * 8192;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + SH_SMEM - 1024) + warp * PV_ST;
+    if (lane == 0) {
+        for (int s = 0; s < PV_ST; ++s) mbar_init(&full[s], 1);
+        fence_barrier_init();
+    }
+    __syncwarp();
+    int pc = 0;
+    for (;;) {
+        int idx = 0;
+        if (lane == 0) idx = atomicAdd(a.pv_next, 1);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx >= a.n_pv) break;
+        private_item<G>(tm_kv, a, a.pv[idx], ring, full, pc);
+    }
+    if (warp == 0) stamp(a, blockIdx.x, 12);
+    if (!a.merge_in_kernel) {
+        // the last warp out rewinds the queue for the next launch
+        if (lane == 0 && atomicAdd(a.pv_done, 1) == static_cast<int>(gridDim.x) * DA_PV_WARPS - 1) {
+            *a.pv_next = 0;
+            *a.pv_done = 0;
+        }
+        return;
+    }
+    // Grid-wide arrival: every CTA of this grid is resident (one per SM, and
+    // the launch guarantees grid <= SMs), so spinning cannot deadlock. After
+    // it, all partials exist: the rows are merged by every SM in parallel.
+    named_bar(2, DA_PV_WARPS * 32);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        __threadfence();
+        atomicAdd(a.grid_arrive, 1);
+        int seen;
+        do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(a.grid_arrive) : "memory");
+            if (seen < static_cast<int>(gridDim.x)) __nanosleep(64);
+        } while (seen < static_cast<int>(gridDim.x));
+    }
+    named_bar(2, DA_PV_WARPS * 32);
+    if (warp == 0) stamp(a, blockIdx.x, 13);
+    const int n_pairs = a.n_rows * a.H;
+    for (int pb = blockIdx.x * (DA_PV_WARPS * 2); pb < n_pairs; pb += gridDim.x * (DA_PV_WARPS * 2))
+        merge16(a, pb + (tid >> 4), n_pairs);
+    named_bar(2, DA_PV_WARPS * 32);
+    // the last CTA out rewinds the queue and the barrier for the next launch
+    if (tid == 0 && atomicAdd(a.pv_done, 1) == static_cast<int>(gridDim.x) - 1) {
+        *a.pv_next = 0;
+        *a.pv_done = 0;
+        *a.grid_arrive = 0;
+    }
 }
 
 template <int G>
 void launch_g(const DecodeAttnArgs& a, const CUtensorMap& tm, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
-        HK_CUDA(cudaFuncSetAttribute(attn_shared_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, SH_SMEM));
-        HK_CUDA(cudaFuncSetAttribute(attn_private_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, PV_SMEM));
+        HK_CUDA(cudaFuncSetAttribute(attn_decode_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, DA_SMEM));
         configured = true;
     }
-    if (a.n_sh > 0) {
-        launch_pdl(attn_shared_tc_kernel<G>, dim3(a.n_sh), dim3(SH_THREADS), SH_SMEM, st, tm, a);
-        HK_LAUNCHED(1);
-    }
-    if (a.n_pv > 0) {
-        launch_pdl(attn_private_kernel<G>, dim3((a.n_pv + PV_WARPS - 1) / PV_WARPS), dim3(PV_WARPS * 32), PV_SMEM,
-                   st, tm, a);
+    // every SM: shared items first, the rest of the grid starts on the private queue at once
+    const int grid = std::max(a.n_sh, a.n_pv > 0 ? g_num_sms : 1);
+    DecodeAttnArgs k = a;
+    k.merge_in_kernel = a.any_merge && grid <= g_num_sms ? 1 : 0;
+    launch_pdl(attn_decode_kernel<G>, dim3(grid), dim3(SH_THREADS), DA_SMEM, st, tm, k);
+    HK_LAUNCHED(1);
+    static const bool no_merge = std::getenv("HK_ATTN_DEBUG_NO_MERGE") != nullptr;  // timing experiments only
+    if (a.n_rows > 0 && a.any_merge && !no_merge && !k.merge_in_kernel) {
+        const int pairs = a.n_rows * a.H;  // 16 lanes each
+        static const bool merge_plain = std::getenv("HK_ATTN_MERGE_NO_PDL") != nullptr;
+        if (merge_plain)
+            attn_merge_rows_kernel<<<(pairs * 16 + 255) / 256, 256, 0, st>>>(a, pairs);
+        else
+            launch_pdl(attn_merge_rows_kernel, dim3((pairs * 16 + 255) / 256), dim3(256), 0, st, a, pairs);
         HK_LAUNCHED(1);
     }
 }
@@ -712,17 +805,38 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
     int kp_base = static_cast<int>(priv_keys * Hkv / (8.0 * num_sms));
     kp_base = std::max(128, std::min(512, (kp_base + PG - 1) / PG * PG));
     if (std::getenv("HK_ATTN_PRIV_KEYS")) kp_base = std::atoi(std::getenv("HK_ATTN_PRIV_KEYS"));
+    // Shared split count S from a small cost model (us, SM-us; measured on
+    // B200, tools/attn_bench.py): a shared CTA costs ~5 us + ~1.3 us per 8-page
+    // chunk; private pages cost ~0.2 SM-us each (~40 GB/s per SM). SMs without
+    // a shared item start on the private queue at once and the shared CTAs
+    // join when done, so the step ends at max(t_shared, total SM-time / SMs).
+    int best_s = 1;
+    {
+        int max_nch = 0;
+        for (const auto& g : groups)
+            if (g.shared_pages > 0 && g.members > 1) max_nch = std::max(max_nch, (g.shared_pages + 7) / 8);
+        const double pv_sm_us = priv_keys * Hkv * kv_tok / 40e3;
+        double best_t = 1e30;
+        for (int S = 1; S <= std::min(8, std::max(1, max_nch)); ++S) {
+            const int n_sh = tiles * S;
+            const double waves = std::ceil(static_cast<double>(n_sh) / num_sms);
+            const double t_sh = waves * (5.0 + std::ceil(static_cast<double>(max_nch) / S) * 1.3);
+            const double t = std::max(t_sh, (pv_sm_us + n_sh * t_sh / waves) / num_sms);
+            if (t < best_t - 0.05) {
+                best_t = t;
+                best_s = S;
+            }
+        }
+        static const int env_splits = std::getenv("HK_ATTN_SPLITS") ? std::atoi(std::getenv("HK_ATTN_SPLITS")) : 0;
+        if (env_splits > 0) best_s = env_splits;
+    }
     for (const auto& g : groups) {
         const bool shared = g.shared_pages > 0 && g.members > 1;
         const int shared_pages = shared ? g.shared_pages : 0;
         int splits = 0;
         if (shared) {
-            // about one shared CTA per SM over all tiles; the private kernel fills
-            // the remaining SMs and every SM a finished shared CTA frees
             const int nch = (shared_pages + 7) / 8;
-            static const int env_splits = std::getenv("HK_ATTN_SPLITS") ? std::atoi(std::getenv("HK_ATTN_SPLITS")) : 0;
-            splits = std::max(1, std::min({nch, env_splits > 0 ? env_splits : (num_sms + tiles - 1) / tiles,
-                                           max_parts / 2}));
+            splits = std::max(1, std::min({nch, best_s, max_parts / 2}));
             int cpc = (nch + splits - 1) / splits;
             cpc = std::min(cpc, SH_MAX_PAGES / 8);
             splits = (nch + cpc - 1) / cpc;

@@ -117,32 +117,50 @@ double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_
         const size_t n_part = static_cast<size_t>(n_rows) * H * kMaxParts;
         HK_CUDA(cudaMalloc(&bufs[1], n_part * 128 * 4));
         HK_CUDA(cudaMalloc(&bufs[2], n_part * 8));
-        HK_CUDA(cudaMalloc(&bufs[3], static_cast<size_t>(n_rows) * Hkv * 4));
-        HK_CUDA(cudaMemset(bufs[3], 0, static_cast<size_t>(n_rows) * Hkv * 4));
+        HK_CUDA(cudaMalloc(&bufs[3], (static_cast<size_t>(n_rows) * Hkv + 4) * 4));
+        HK_CUDA(cudaMemset(bufs[3], 0, (static_cast<size_t>(n_rows) * Hkv + 4) * 4));
+        int32_t* ctr = static_cast<int32_t*>(bufs[3]);
         const CUtensorMap tm = hkd::make_tmap_2d_bf16(kv, static_cast<uint64_t>(n_pages) * 2 * Hkv * 16, 128, 64, 16);
         hkd::DecodeAttnArgs a{static_cast<const hkd::bf16*>(qkv), H, Hkv, (H + 2 * Hkv) * 128,
                               static_cast<const hkd::bf16*>(kv), 0, reinterpret_cast<const int32_t*>(m),
                               reinterpret_cast<const hkd::ShItem*>(m + o_sh), static_cast<int>(plan.sh.size()), plan.sh_cluster,
                               reinterpret_cast<const hkd::PvItem*>(m + o_pv), static_cast<int>(plan.pv.size()),
                               static_cast<float*>(bufs[1]), static_cast<float2*>(bufs[2]), kMaxParts,
-                              reinterpret_cast<const int32_t*>(m + o_np), static_cast<int32_t*>(bufs[3]), 0,
+                              reinterpret_cast<const int32_t*>(m + o_np), ctr, n_rows, 1,
+                              ctr + static_cast<size_t>(n_rows) * Hkv,
+                              ctr + static_cast<size_t>(n_rows) * Hkv + 1, ctr + static_cast<size_t>(n_rows) * Hkv + 2,
+                              0, 0,
                               static_cast<hkd::bf16*>(out), 1.4426950408889634f / sqrtf(128.f), g_trace};
         hkd::decode_attention(a, tm, nullptr);
         HK_CUDA(cudaDeviceSynchronize());
         double ms = 0;
         if (iters > 0) {
+            // time graph replays (as the engine runs decode steps), 10 calls per graph
+            cudaStream_t cs;
+            HK_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            cudaGraph_t g;
+            HK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            for (int i = 0; i < 10; ++i) hkd::decode_attention(a, tm, cs);
+            HK_CUDA(cudaStreamEndCapture(cs, &g));
+            cudaGraphExec_t ge;
+            HK_CUDA(cudaGraphInstantiate(&ge, g, 0));
+            HK_CUDA(cudaGraphLaunch(ge, cs));  // warm
             cudaEvent_t e0, e1;
             HK_CUDA(cudaEventCreate(&e0));
             HK_CUDA(cudaEventCreate(&e1));
-            HK_CUDA(cudaEventRecord(e0));
-            for (int i = 0; i < iters; ++i) hkd::decode_attention(a, tm, nullptr);
-            HK_CUDA(cudaEventRecord(e1));
+            const int reps = (iters + 9) / 10;
+            HK_CUDA(cudaEventRecord(e0, cs));
+            for (int i = 0; i < reps; ++i) HK_CUDA(cudaGraphLaunch(ge, cs));
+            HK_CUDA(cudaEventRecord(e1, cs));
             HK_CUDA(cudaEventSynchronize(e1));
             float t = 0;
             HK_CUDA(cudaEventElapsedTime(&t, e0, e1));
-            ms = t / iters;
+            ms = t / (reps * 10);
             cudaEventDestroy(e0);
             cudaEventDestroy(e1);
+            cudaGraphExecDestroy(ge);
+            cudaGraphDestroy(g);
+            cudaStreamDestroy(cs);
         }
         for (void* b : bufs) cudaFree(b);
         return ms;

@@ -126,11 +126,9 @@ void attention_merge(const float* part_o, const float2* part_ml, const int32_t* 
 //     of whole shared pages; the shared KV is read once for all those rows;
 //   * private items (CUDA cores): one decode token x one kv head x its own
 //     pages (suffix + generated tokens).
-// The shared items of one (rows, kv head) tile form a thread-block cluster
-// that combines its page ranges through DSMEM into one flash partial (m, l,
-// unnormalised o); private items leave one partial each. The last contributor
-// of a (token, kv head) merges its partials (a per-(row, kv head) arrival
-// counter) and writes the bf16 output, so no separate merge launch exists.
+// Every item leaves a flash partial (m, l, unnormalised o) per row and head
+// (a row's only item writes the bf16 output directly); a PDL-chained merge
+// kernel combines the partials of rows that have several.
 struct ShItem {
     int row0;    // first decode row
     int ntok;    // decode rows covered (<= 128 / G)
@@ -166,6 +164,12 @@ struct DecodeAttnArgs {
     int max_parts;
     const int32_t* n_parts; // [rows] partials per (row, kv head)
     int32_t* counters;      // [rows][Hkv], zero between launches
+    int n_rows;             // decode rows of the step
+    int any_merge;          // some row has > 1 partial (a merge launch follows)
+    int32_t* pv_next;       // private work queue head (zero between launches)
+    int32_t* pv_done;       // warps / CTAs that left the queue (zero between launches)
+    int32_t* grid_arrive;   // grid-wide arrival before the in-kernel merge (zero between launches)
+    int merge_in_kernel;    // set by the launcher
     int dec_tok0;           // batch token of decode row 0
     bf16* out;              // [T][H][128]
     float sl2;              // softmax scale * log2(e)

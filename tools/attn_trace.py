@@ -34,20 +34,13 @@ _lib.load().hkx_decode_attention_trace(C.c_void_p(buf.data_ptr()))
 run(case)
 _lib.load().hkx_decode_attention_trace(None)
 t = buf.view(-1, 16).cpu().numpy().astype(np.float64)
-n_sh = int((t[:, 0] > 0).sum()) - int((t[:, 0] > 0).sum() - 0)  # placeholder
 n_sh = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 sh = t[:n_sh]
-pv = t[n_sh:][t[n_sh:, 0] > 0]
-t0 = min(sh[:, 0].min(), pv[:, 0].min())
+rest = t[n_sh:][t[n_sh:, 0] > 0]
+t0 = sh[:, 0].min() if len(rest) == 0 else min(sh[:, 0].min(), rest[:, 0].min())
 us = lambda x: (x - t0) / 1e3
-print(f"k={k}: private CTAs {len(pv)}: start {us(pv[:,0]).min():.1f}..{us(pv[:,0]).max():.1f} us, "
-      f"warp-0 item done {us(pv[:,2]).min():.1f}..{us(pv[:,2]).max():.1f} (mean item {((pv[:,2]-pv[:,1])/1e3).mean():.2f} us)")
-pvo = [(1, "pdl/trigger"), (3, "page0 landed"), (2, "pages done"), (4, "partial out"), (5, "atomic"), (6, "merged")]
-for (i0, n0), (i1, n1) in zip(pvo[:-1], pvo[1:]):
-    d = (pv[:, i1] - pv[:, i0]) / 1e3
-    print(f"  private {n0:>12s} -> {n1:<12s} mean {d.mean():6.2f} us  max {d.max():6.2f}")
-print(f"shared CTAs {n_sh}: start {us(sh[:,0]).min():.1f}..{us(sh[:,0]).max():.1f} us")
-# stamp order within a shared CTA
+print(f"k={k}: shared CTAs {n_sh}: start {us(sh[:,0]).min():.1f}..{us(sh[:,0]).max():.1f} us; "
+      f"queue-only CTAs {len(rest)} start {us(rest[:,0]).min() if len(rest) else 0:.1f} us")
 order = [(0, "start"), (1, "tmem+bars"), (2, "q in smem"), (7, "S0 ready"), (8, "P0 written"), (3, "O done"),
          (4, "partial out"), (5, "merge")]
 prev = None
@@ -56,6 +49,7 @@ for idx, name in order:
         d = (sh[:, idx] - sh[:, prev[0]]) / 1e3
         print(f"  {prev[1]:>14s} -> {name:<14s} mean {d.mean():7.2f} us  max {d.max():7.2f}")
     prev = (idx, name)
+print(f"  queue loop ends: shared CTAs {us(sh[:,12]).min():.1f}..{us(sh[:,12]).max():.1f} us, "
+      f"queue-only CTAs {us(rest[:,12]).min() if len(rest) else 0:.1f}..{us(rest[:,12]).max() if len(rest) else 0:.1f} us")
 mhz = (sh[:, 15] - sh[:, 14]) / (sh[:, 5] - sh[:, 0]) * 1e3
-print(f"  SM clock inside shared CTAs: {mhz.mean():.0f} MHz")
-print(f"  end of last shared CTA {us(sh[:,5]).max():.1f} us; end of last private {us(pv[:,2]).max():.1f}")
+print(f"  SM clock inside shared CTAs: {mhz.mean():.0f} MHz; shared phase ends {us(sh[:,5]).min():.1f}..{us(sh[:,5]).max():.1f} us")
