@@ -469,9 +469,28 @@ __device__ __forceinline__ uint32_t tile_off(int row, int c) {
 // One private item with the calling warp. ring / full: the warp's PV_ST
 // stages (8 KB each) and their mbarriers; pc counts the pages this warp has
 // already pushed through the ring (mbarrier phase bookkeeping).
+// The queue is software-pipelined: `next` holds the next item's index (its
+// atomic was issued before this item started); while this item's pages
+// stream, the warp loads the next item's record and page ids into `nit` /
+// `npage`, so a new item starts without waiting on L2 round trips.
+struct PvNext {
+    int idx;     // next item index (raw atomic result in lane 0)
+    PvItem it;   // its record (valid when idx < n_pv after the prefetch)
+    int page;    // its page id for this lane
+};
+__device__ __forceinline__ void prefetch_next(const DecodeAttnArgs& a, PvNext& nx) {
+    nx.idx = __shfl_sync(0xffffffffu, nx.idx, 0);
+    if (nx.idx < a.n_pv) {
+        nx.it = a.pv[nx.idx];
+        const int nnp = (nx.it.kend - nx.it.kbeg + PG - 1) / PG;
+        const int lane = threadIdx.x & 31;
+        nx.page = lane < nnp ? a.pages[nx.it.ptab + nx.it.kbeg / PG + lane] : 0;
+    }
+}
+
 template <int G>
 __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const DecodeAttnArgs& a, const PvItem& it,
-                                             uint8_t* ring, uint64_t* full, int& pc) {
+                                             int my_page, uint8_t* ring, uint64_t* full, int& pc, PvNext& nx) {
     static_assert(G <= 8, "private item: G q-heads must fit rows 0-7 of the MMA tile");
     const int lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
@@ -479,8 +498,7 @@ __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const Dec
     const int np = (it.kend - it.kbeg + PG - 1) / PG;
     const uint32_t ring_s = smem_u32(ring);
     const int rows_per_head = a.Hkv * PG;
-    // page ids of the item (np <= 32 for this kernel's key splits), one per lane
-    const int my_page = lane < np ? a.pages[it.ptab + p0 + lane] : 0;
+    // (my_page: page ids of the item, one per lane; np <= 32 for this kernel's key splits)
     auto issue = [&](int i, int page) {  // lane 0 only: K (2 boxes) + V (2 boxes)
         const int s = (pc + i) % PV_ST;
         uint64_t* bar = &full[s];
@@ -570,6 +588,7 @@ __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const Dec
         // every lane has read stage s (the shuffle syncs the warp): refill it
         const int pg = __shfl_sync(0xffffffffu, my_page, (i + PV_ST) & 31);
         if (lane == 0 && i + PV_ST < np) issue(i + PV_ST, pg);
+        if (i == 0) prefetch_next(a, nx);
     }
     pc += np;
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
@@ -697,12 +716,14 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
     }
     __syncwarp();
     int pc = 0;
-    for (;;) {
-        int idx = 0;
-        if (lane == 0) idx = atomicAdd(a.pv_next, 1);
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (idx >= a.n_pv) break;
-        private_item<G>(tm_kv, a, a.pv[idx], ring, full, pc);
+    PvNext nx;
+    nx.idx = lane == 0 ? atomicAdd(a.pv_next, 1) : 0;
+    prefetch_next(a, nx);
+    while (nx.idx < a.n_pv) {
+        const PvItem it = nx.it;
+        const int my_page = nx.page;
+        nx.idx = lane == 0 ? atomicAdd(a.pv_next, 1) : 0;  // claim the next item now; used after page 0
+        private_item<G>(tm_kv, a, it, my_page, ring, full, pc, nx);
     }
     if (warp == 0) stamp(a, blockIdx.x, 12);
     if (!a.merge_in_kernel) {
@@ -806,7 +827,7 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
     kp_base = std::max(128, std::min(512, (kp_base + PG - 1) / PG * PG));
     if (std::getenv("HK_ATTN_PRIV_KEYS")) kp_base = std::atoi(std::getenv("HK_ATTN_PRIV_KEYS"));
     // Shared split count S from a small cost model (us, SM-us; measured on
-    // B200, tools/attn_bench.py): a shared CTA costs ~5 us + ~1.3 us per 8-page
+    // B200, tools/attn_bench.py): a shared CTA costs ~5.3 us + ~2.3 us per 8-page
     // chunk; private pages cost ~0.2 SM-us each (~40 GB/s per SM). SMs without
     // a shared item start on the private queue at once and the shared CTAs
     // join when done, so the step ends at max(t_shared, total SM-time / SMs).
@@ -820,7 +841,7 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
         for (int S = 1; S <= std::min(8, std::max(1, max_nch)); ++S) {
             const int n_sh = tiles * S;
             const double waves = std::ceil(static_cast<double>(n_sh) / num_sms);
-            const double t_sh = waves * (5.0 + std::ceil(static_cast<double>(max_nch) / S) * 1.3);
+            const double t_sh = waves * (5.3 + std::ceil(static_cast<double>(max_nch) / S) * 2.3);
             const double t = std::max(t_sh, (pv_sm_us + n_sh * t_sh / waves) / num_sms);
             if (t < best_t - 0.05) {
                 best_t = t;
@@ -861,7 +882,9 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
             const int k0 = shared_pages * PG, k1 = in.pos + 1;
             if (k1 <= k0) throw std::runtime_error("decode_attention: shared range covers the decode token");
             const int first = splits;  // the shared items contribute partials 0 .. splits - 1
-            int kp = std::max(kp_base, (k1 - k0 + (max_parts - first) - 1) / (max_parts - first));
+            // keep a row's partials within one 8-part merge batch when possible
+            const int part_cap = first < 8 ? 8 - first : max_parts - first;
+            int kp = std::max(kp_base, (k1 - k0 + part_cap - 1) / part_cap);
             kp = (kp + PG - 1) / PG * PG;
             if (kp > 32 * PG) throw std::runtime_error("decode_attention: private range too long for max_parts");
             const int npv = (k1 - k0 + kp - 1) / kp;

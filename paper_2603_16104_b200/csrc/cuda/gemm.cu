@@ -433,11 +433,15 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
               float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits, int max_splits) {
     if (T <= 0) return 0;
     if (K % BK != 0) throw std::runtime_error("gemm_bf16: K must be a multiple of 64");
-    // Stream-K pays off for the long LM-head contraction (1,002 vocab tiles:
-    // ~7 whole tiles per SM, 97% of HBM peak measured); the per-layer GEMMs
-    // keep split-K partials reduced by their consumer row kernels, which
-    // measured faster (tools/gemm_sweep.py, profiles/).
-    if (T <= 64 && epi == kEpiArgmax && force_splits == 0 && bias == nullptr && gemm_streamk_enabled()) {
+    // The LM head (1,002 vocab tiles, argmax epilogue) runs stream-K, one CTA
+    // per SM (97% of HBM peak measured); the per-layer GEMMs keep split-K
+    // partials reduced by their consumer row kernels, measured faster
+    // (tools/gemm_sweep.py, profiles/r1_gemm_sweep.txt).
+    const bool wide = (N + BM - 1) / BM >= g_num_sms;  // at least one whole wave of weight tiles
+    static const bool sk_swiglu = std::getenv("HK_SK_SWIGLU") != nullptr;  // opt-in: slower on B200 (sweep)
+    if (T <= 64 && wide && (epi == kEpiArgmax || (sk_swiglu && epi == kEpiSwiGLU)) && force_splits == 0 &&
+        bias == nullptr &&
+        gemm_streamk_enabled()) {
         gemm_bf16_streamk(W, X, N, K, T, epi, out, ldo, st);
         return 1;  // fully reduced
     }

@@ -33,8 +33,10 @@ struct SkParams {
     int N, K, T;
     int kb;      // k-blocks per tile
     int mt;      // weight tiles
-    int units;   // mt * kb
+    int units;   // units of the stream-K region: (mt - dp_tiles) * kb
     int ctas;    // grid size
+    int w;       // whole-tile waves before the stream-K region (tile c + q * ctas, q < w)
+    int dp_tiles;
     int epi;
     void* out;
     int ldo;
@@ -56,6 +58,20 @@ __device__ __forceinline__ int sk_arrive(int32_t* ctr) {
     int old;
     asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
     return old;
+}
+
+// Segment q of CTA c: the first w are whole tiles (data-parallel waves), the
+// rest are the CTA's tile pieces of the stream-K region [u0, u1) (region-
+// relative units; t_rel indexes region tiles).
+struct SkSeg {
+    int t;      // global tile
+    int ka, kz; // k-block range [ka, kz) within the tile
+    int t_rel;  // region tile (stream-K segments), -1 for whole tiles
+};
+__device__ __forceinline__ SkSeg sk_seg(int c, int q, int u0, int u1, int t_first, const SkParams& p) {
+    if (q < p.w) return SkSeg{c + q * p.ctas, 0, p.kb, -1};
+    const int tr = t_first + (q - p.w);
+    return SkSeg{p.dp_tiles + tr, max(u0, tr * p.kb) - tr * p.kb, min(u1, (tr + 1) * p.kb) - tr * p.kb, tr};
 }
 
 template <int BN, int STAGES>
@@ -85,7 +101,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const int u0 = sk_u0(c, p), u1 = sk_u0(c + 1, p);
-    const int t_first = u0 / p.kb, t_last = (u1 - 1) / p.kb;
+    const int t_first = u0 / p.kb, t_last = u1 > u0 ? (u1 - 1) / p.kb : t_first - 1;
+    const int n_segs = p.w + (t_last - t_first + 1);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmW);
@@ -111,33 +128,48 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         if (lane == 0) {
             const uint64_t pol_w = policy_evict_first();
             const uint64_t pol_x = policy_evict_last();
-            const int n = u1 - u0;
+            const int n = p.w * p.kb + (u1 - u0);
+            auto unit = [&](int i, int& t, int& k) {  // i-th unit of this CTA -> (global tile, k-block)
+                if (i < p.w * p.kb) {
+                    t = c + (i / p.kb) * p.ctas;
+                    k = i % p.kb;
+                } else {
+                    const int u = u0 + i - p.w * p.kb;
+                    t = p.dp_tiles + u / p.kb;
+                    k = u % p.kb;
+                }
+            };
             // Weights do not depend on the previous kernel: start streaming them
             // before waiting for the activations (PDL overlap).
             const int pre = min(STAGES, n);
             for (int i = 0; i < pre; ++i) {
-                const int u = u0 + i;
+                int t, k;
+                unit(i, t, k);
                 mbar_expect_tx(&full[i], A_BYTES + B_BYTES);
-                tma_load_2d_hint(sA + i * A_BYTES, &tmW, &full[i], (u % p.kb) * SK_BK, (u / p.kb) * SK_BM, pol_w);
+                tma_load_2d_hint(sA + i * A_BYTES, &tmW, &full[i], k * SK_BK, t * SK_BM, pol_w);
             }
             pdl_wait();
             for (int i = 0; i < pre; ++i) {
-                const int u = u0 + i;
-                tma_load_2d_hint(sB + i * B_BYTES, &tmX, &full[i], (u % p.kb) * SK_BK, 0, pol_x);
+                int t, k;
+                unit(i, t, k);
+                tma_load_2d_hint(sB + i * B_BYTES, &tmX, &full[i], k * SK_BK, 0, pol_x);
             }
             for (int i = pre; i < n; ++i) {
-                const int s = i % STAGES, u = u0 + i;
+                const int s = i % STAGES;
+                int t, k;
+                unit(i, t, k);
                 mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
                 mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-                tma_load_2d_hint(sA + s * A_BYTES, &tmW, &full[s], (u % p.kb) * SK_BK, (u / p.kb) * SK_BM, pol_w);
-                tma_load_2d_hint(sB + s * B_BYTES, &tmX, &full[s], (u % p.kb) * SK_BK, 0, pol_x);
+                tma_load_2d_hint(sA + s * A_BYTES, &tmW, &full[s], k * SK_BK, t * SK_BM, pol_w);
+                tma_load_2d_hint(sB + s * B_BYTES, &tmX, &full[s], k * SK_BK, 0, pol_x);
             }
         }
     } else if (warp == 1) {
         constexpr uint32_t idesc = umma_idesc_bf16(SK_BM, BN);
         int i = 0;
-        for (int t = t_first, q = 0; t <= t_last; ++t, ++q) {
-            const int a = max(u0, t * p.kb), b = min(u1, (t + 1) * p.kb);
+        for (int q = 0; q < n_segs; ++q) {
+            const SkSeg sg = sk_seg(c, q, u0, u1, t_first, p);
+            const int a = sg.ka, b = sg.kz;
             const int buf = q & 1;
             if (q >= 2) mbar_wait(&acc_empty[buf], ((q >> 1) - 1) & 1);
             tc_fence_after();
@@ -164,8 +196,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         const int row = quarter * 32 + lane;
         const int etid = threadIdx.x - 64;  // 0..127
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-        for (int t = t_first, q = 0; t <= t_last; ++t, ++q) {
-            const int a = max(u0, t * p.kb), b = min(u1, (t + 1) * p.kb);
+        for (int q = 0; q < n_segs; ++q) {
+            const SkSeg sg = sk_seg(c, q, u0, u1, t_first, p);
+            const int t = sg.t;
             const int buf = q & 1;
             mbar_wait(&acc_full[buf], (q >> 1) & 1);
             tc_fence_after();
@@ -190,21 +223,22 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             }
             tc_fence_before();
             mbar_arrive(&acc_empty[buf]);
-            if (a != t * p.kb || b != (t + 1) * p.kb) {
+            if (sg.ka != 0 || sg.kz != p.kb) {
                 // split tile: park this segment, the last arriver sums all segments in k order
-                const int slot = t == t_first ? 0 : 1;
+                const int tr = sg.t_rel;
+                const int slot = tr == t_first ? 0 : 1;
                 float* wsp = p.ws + (static_cast<size_t>(c) * 2 + slot) * BN * SK_BM;
 #pragma unroll
                 for (int j = 0; j < BN; ++j) wsp[j * SK_BM + row] = v[j];
                 named_bar(1, 128);
-                const int cf = sk_cta_of(t * p.kb, p), cl = sk_cta_of((t + 1) * p.kb - 1, p);
+                const int cf = sk_cta_of(tr * p.kb, p), cl = sk_cta_of((tr + 1) * p.kb - 1, p);
                 if (etid == 0) *flag = sk_arrive(&p.counters[t]) == cl - cf;
                 named_bar(1, 128);
                 if (!*flag) continue;
 #pragma unroll
                 for (int j = 0; j < BN; ++j) v[j] = 0.f;
                 for (int cc = cf; cc <= cl; ++cc) {
-                    const int sl = (t == sk_u0(cc, p) / p.kb) ? 0 : 1;
+                    const int sl = (tr == sk_u0(cc, p) / p.kb) ? 0 : 1;
                     const float* src = p.ws + (static_cast<size_t>(cc) * 2 + sl) * BN * SK_BM;
 #pragma unroll
                     for (int j = 0; j < BN; ++j) v[j] += __ldcg(src + j * SK_BM + row);
@@ -334,9 +368,14 @@ void gemm_bf16_streamk(const bf16* W, const bf16* X, int N, int K, int T, int ep
     p.T = T;
     p.kb = K / SK_BK;
     p.mt = (N + SK_BM - 1) / SK_BM;
-    p.units = p.mt * p.kb;
     static const int per_sm = std::getenv("HK_SK_CTAS_PER_SM") ? std::atoi(std::getenv("HK_SK_CTAS_PER_SM")) : 1;
-    p.ctas = std::min(g_num_sms * per_sm, p.units);
+    p.ctas = std::min(g_num_sms * per_sm, p.mt * p.kb);
+    // whole-tile waves first (no fixups), stream-K only over the remainder
+    // (opt-in: measured slower than pure stream-K on B200, profiles/r1_gemm_sweep.txt)
+    static const bool hybrid = std::getenv("HK_SK_HYBRID") != nullptr;
+    p.w = hybrid && p.mt >= p.ctas ? p.mt / p.ctas : 0;
+    p.dp_tiles = p.w * p.ctas;
+    p.units = (p.mt - p.dp_tiles) * p.kb;
     p.epi = epi;
     p.out = out;
     p.ldo = ldo;

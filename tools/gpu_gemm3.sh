@@ -1,3 +1,3 @@
-echo "## stream-K 1 CTA/SM x 8 stages"; python tools/gemm_sweep.py 64
-echo "## stream-K 2 CTA/SM x 4 stages"; HK_SK_CTAS_PER_SM=2 python tools/gemm_sweep.py 64
-echo "## stream-K 3 CTA/SM x 4 stages"; HK_SK_CTAS_PER_SM=3 python tools/gemm_sweep.py 64
+timeout -s KILL 600 python -m pytest tests/test_gpu_kernels.py -q -x --timeout 300 2>&1 | tail -2
+echo "## default routing"; python tools/gemm_sweep.py 64
+echo "## no stream-K"; HK_GEMM_NO_STREAMK=1 python tools/gemm_sweep.py 64
