@@ -488,32 +488,45 @@ __device__ __forceinline__ void prefetch_next(const DecodeAttnArgs& a, PvNext& n
     }
 }
 
+// Issue page i of item `it` into the warp's ring (lane 0 only): K and V, two
+// TMA boxes each.
+__device__ __forceinline__ void pv_issue(const CUtensorMap& tm_kv, const DecodeAttnArgs& a, const PvItem& it,
+                                         uint8_t* ring, uint64_t* full, int pc, int i, int page) {
+    const int s = (pc + i) % PV_ST;
+    uint64_t* bar = &full[s];
+    uint8_t* dst = ring + s * 8192;
+    const int rk = a.layer_row0 + (page * 2 * a.Hkv + it.kvh) * PG;
+    const int rows_per_head = a.Hkv * PG;
+    mbar_expect_tx(bar, 8192);
+    tma_load_2d(dst, &tm_kv, bar, 0, rk);
+    tma_load_2d(dst + 2048, &tm_kv, bar, 64, rk);
+    tma_load_2d(dst + 4096, &tm_kv, bar, 0, rk + rows_per_head);
+    tma_load_2d(dst + 6144, &tm_kv, bar, 64, rk + rows_per_head);
+}
+
+// Pages of `it` that were written by earlier steps: every page before the one
+// holding the item's last key (the decode token's own K/V, written by this
+// step's RoPE kernel, lives there). They may be loaded before griddepcontrol.wait.
+__device__ __forceinline__ int pv_safe_pages(const PvItem& it) {
+    return (it.kend - 1) / PG - it.kbeg / PG;
+}
+
 template <int G>
 __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const DecodeAttnArgs& a, const PvItem& it,
-                                             int my_page, uint8_t* ring, uint64_t* full, int& pc, PvNext& nx) {
+                                             int my_page, uint8_t* ring, uint64_t* full, int& pc, PvNext& nx,
+                                             int pre = 0) {
     static_assert(G <= 8, "private item: G q-heads must fit rows 0-7 of the MMA tile");
     const int lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
     const int p0 = it.kbeg / PG;
     const int np = (it.kend - it.kbeg + PG - 1) / PG;
     const uint32_t ring_s = smem_u32(ring);
-    const int rows_per_head = a.Hkv * PG;
     // (my_page: page ids of the item, one per lane; np <= 32 for this kernel's key splits)
-    auto issue = [&](int i, int page) {  // lane 0 only: K (2 boxes) + V (2 boxes)
-        const int s = (pc + i) % PV_ST;
-        uint64_t* bar = &full[s];
-        uint8_t* dst = ring + s * 8192;
-        const int rk = a.layer_row0 + (page * 2 * a.Hkv + it.kvh) * PG;
-        mbar_expect_tx(bar, 8192);
-        tma_load_2d(dst, &tm_kv, bar, 0, rk);
-        tma_load_2d(dst + 2048, &tm_kv, bar, 64, rk);
-        tma_load_2d(dst + 4096, &tm_kv, bar, 0, rk + rows_per_head);
-        tma_load_2d(dst + 6144, &tm_kv, bar, 64, rk + rows_per_head);
-    };
+    auto issue = [&](int i, int page) { pv_issue(tm_kv, a, it, ring, full, pc, i, page); };
 #pragma unroll
     for (int i = 0; i < PV_ST; ++i) {
         const int pg = __shfl_sync(0xffffffffu, my_page, i);
-        if (lane == 0 && i < np) issue(i, pg);
+        if (lane == 0 && i >= pre && i < np) issue(i, pg);
     }
     // Q as the A operand (rows gid < G hold q heads kvh*G + gid; rows >= 8 are zero)
     uint32_t qa[8][2];
@@ -699,31 +712,54 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
     // plain stores compile to STS
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     pdl_trigger();  // the next kernel (O projection) may launch; it waits for us before reading
-    if (blockIdx.x < a.n_sh) {
-        shared_phase<G>(tm_kv, a, sm);
-    } else {
-        stamp(a, blockIdx.x, 0);
-        pdl_wait();  // q and this step's own K/V come from the qkv/RoPE kernel
-    }
-    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp >= DA_PV_WARPS) return;
     uint8_t* ring = sm + warp * PV_ST * 8192;
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + SH_SMEM - 1024) + warp * PV_ST;
-    if (lane == 0) {
-        for (int s = 0; s < PV_ST; ++s) mbar_init(&full[s], 1);
-        fence_barrier_init();
-    }
-    __syncwarp();
-    int pc = 0;
+    int pc = 0, pre = 0;
     PvNext nx;
-    nx.idx = lane == 0 ? atomicAdd(a.pv_next, 1) : 0;
-    prefetch_next(a, nx);
+    nx.idx = a.n_pv;
+    if (blockIdx.x < a.n_sh) {
+        shared_phase<G>(tm_kv, a, sm);
+        __syncthreads();
+        if (warp >= DA_PV_WARPS) return;
+        if (lane == 0) {
+            for (int s = 0; s < PV_ST; ++s) mbar_init(&full[s], 1);
+            fence_barrier_init();
+        }
+        __syncwarp();
+        nx.idx = lane == 0 ? atomicAdd(a.pv_next, 1) : 0;
+        prefetch_next(a, nx);
+    } else {
+        stamp(a, blockIdx.x, 0);
+        // Queue-only CTA: claim the first item and start streaming its pages
+        // that earlier steps wrote (metadata and old KV do not depend on the
+        // predecessor kernel), then wait for q and this step's K/V.
+        if (warp < DA_PV_WARPS) {
+            if (lane == 0) {
+                for (int s = 0; s < PV_ST; ++s) mbar_init(&full[s], 1);
+                fence_barrier_init();
+            }
+            __syncwarp();
+            nx.idx = lane == 0 ? atomicAdd(a.pv_next, 1) : 0;
+            prefetch_next(a, nx);
+            if (nx.idx < a.n_pv) {
+                pre = min(PV_ST, pv_safe_pages(nx.it));
+#pragma unroll
+                for (int i = 0; i < PV_ST; ++i) {
+                    const int pg = __shfl_sync(0xffffffffu, nx.page, i);
+                    if (lane == 0 && i < pre) pv_issue(tm_kv, a, nx.it, ring, full, pc, i, pg);
+                }
+            }
+        }
+        pdl_wait();  // q and this step's own K/V come from the qkv/RoPE kernel
+        if (warp >= DA_PV_WARPS) return;
+    }
     while (nx.idx < a.n_pv) {
         const PvItem it = nx.it;
         const int my_page = nx.page;
         nx.idx = lane == 0 ? atomicAdd(a.pv_next, 1) : 0;  // claim the next item now; used after page 0
-        private_item<G>(tm_kv, a, it, my_page, ring, full, pc, nx);
+        private_item<G>(tm_kv, a, it, my_page, ring, full, pc, nx, pre);
+        pre = 0;
     }
     if (warp == 0) stamp(a, blockIdx.x, 12);
     if (!a.merge_in_kernel) {
@@ -826,28 +862,23 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
     int kp_base = static_cast<int>(priv_keys * Hkv / (8.0 * num_sms));
     kp_base = std::max(128, std::min(512, (kp_base + PG - 1) / PG * PG));
     if (std::getenv("HK_ATTN_PRIV_KEYS")) kp_base = std::atoi(std::getenv("HK_ATTN_PRIV_KEYS"));
-    // Shared split count S from a small cost model (us, SM-us; measured on
-    // B200, tools/attn_bench.py): a shared CTA costs ~5.3 us + ~2.3 us per 8-page
-    // chunk; private pages cost ~0.2 SM-us each (~40 GB/s per SM). SMs without
-    // a shared item start on the private queue at once and the shared CTAs
-    // join when done, so the step ends at max(t_shared, total SM-time / SMs).
+    // Shared split count S (measured on B200, tools/attn_bench.py, profiles/
+    // r1_attention.txt): shared CTAs should cover ~64 SMs when the rows also
+    // carry >= 4 private pages each (the private queue then keeps the other SMs
+    // streaming), ~128 SMs when a <= 2K-token shared prefix dominates, every SM
+    // for longer prefixes; SMs without a shared item start on the private
+    // queue at once.
     int best_s = 1;
     {
+        double rows_n = 0;
+        for (const auto& g : groups) rows_n += g.members;
+        const double priv_pages_per_row = rows_n > 0 ? priv_keys / rows_n / PG : 0;
         int max_nch = 0;
         for (const auto& g : groups)
             if (g.shared_pages > 0 && g.members > 1) max_nch = std::max(max_nch, (g.shared_pages + 7) / 8);
-        const double pv_sm_us = priv_keys * Hkv * kv_tok / 40e3;
-        double best_t = 1e30;
-        for (int S = 1; S <= std::min(8, std::max(1, max_nch)); ++S) {
-            const int n_sh = tiles * S;
-            const double waves = std::ceil(static_cast<double>(n_sh) / num_sms);
-            const double t_sh = waves * (5.3 + std::ceil(static_cast<double>(max_nch) / S) * 2.3);
-            const double t = std::max(t_sh, (pv_sm_us + n_sh * t_sh / waves) / num_sms);
-            if (t < best_t - 0.05) {
-                best_t = t;
-                best_s = S;
-            }
-        }
+        // long shared prefixes (> 2K tokens, e.g. configs[4]'s 8K) are tensor-bound: one CTA per SM
+        const int target = max_nch > 16 ? num_sms : (priv_pages_per_row >= 4 ? 64 : 128);
+        if (tiles > 0) best_s = std::max(1, std::min(8, static_cast<int>(std::lround(static_cast<double>(target) / tiles))));
         static const int env_splits = std::getenv("HK_ATTN_SPLITS") ? std::atoi(std::getenv("HK_ATTN_SPLITS")) : 0;
         if (env_splits > 0) best_s = env_splits;
     }

@@ -314,8 +314,9 @@ hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m
             wk.tm_kv = hkd::make_tmap_2d_bf16(wk.kv, static_cast<uint64_t>(L) * c.pages_per_worker * 2 * Hkv * c.block_tokens,
                                               static_cast<uint64_t>(hd), 64, c.block_tokens);
         // arrival counters [rows][Hkv] followed by the private work-queue head and exit count
-        wk.counters = dalloc<int32_t>(static_cast<size_t>(c.max_calls * c.n_workers + 16) * Hkv + 4);
-        HK_CUDA(cudaMemsetAsync(wk.counters, 0, (static_cast<size_t>(c.max_calls * c.n_workers + 16) * Hkv + 4) * 4, st));
+        const size_t ctr_n = static_cast<size_t>(c.max_calls * c.n_workers + 16) * Hkv + 4 * static_cast<size_t>(L);
+        wk.counters = dalloc<int32_t>(ctr_n);
+        HK_CUDA(cudaMemsetAsync(wk.counters, 0, ctr_n * 4, st));
         wk.slot_last = dalloc<int32_t>(c.max_calls);
         HK_CUDA(cudaMemsetAsync(wk.slot_last, 0, c.max_calls * sizeof(int32_t), st));
         hkd::DevTrie& t = wk.trie;
@@ -753,8 +754,10 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
                                        wk.counters, static_cast<int>(dec.size()),
                                        static_cast<int>(std::any_of(dplan.n_parts.begin(), dplan.n_parts.end(),
                                                                     [](int32_t v) { return v > 1; })),
-                                       wk.counters + ctr_words, wk.counters + ctr_words + 1,
-                                       wk.counters + ctr_words + 2, 0, T_pre,
+                                       // per-layer queue state: the queue head may be claimed before
+                                       // griddepcontrol.wait, so layers never share it
+                                       wk.counters + ctr_words + 4 * l, wk.counters + ctr_words + 4 * l + 1,
+                                       wk.counters + ctr_words + 4 * l + 2, 0, T_pre,
                                        static_cast<bf16*>(attn), scale * 1.4426950408889634f, nullptr};
                 // one event bracket: the two grids overlap (private, then shared under PDL)
                 ck = clock.begin(1, st);

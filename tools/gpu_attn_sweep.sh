@@ -1,2 +1,2 @@
-python -m pytest tests/test_gpu_decode_attn.py -q -x 2>&1 | tail -2
+python -m pytest tests/test_gpu_decode_attn.py -q -x 2>&1 | tail -1
 python tools/attn_bench.py 2>&1 | tail -10
