@@ -880,7 +880,7 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
         for (int m = 0; m < g.members; ++m) priv_keys += rows[static_cast<size_t>(g.row0 + m)].pos + 1 - k0;
     }
     int kp_base = static_cast<int>(priv_keys * Hkv / (8.0 * num_sms));
-    kp_base = std::max(128, std::min(512, (kp_base + PG - 1) / PG * PG));
+    kp_base = std::max(64, std::min(512, (kp_base + PG - 1) / PG * PG));
     if (std::getenv("HK_ATTN_PRIV_KEYS")) kp_base = std::atoi(std::getenv("HK_ATTN_PRIV_KEYS"));
     // Shared split count S (measured on B200, tools/attn_bench.py, profiles/
     // r1_attention.txt): shared CTAs should cover ~64 SMs when the rows also
