@@ -214,6 +214,7 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
     stamp(a, blockIdx.x, 0);
     const ShItem it = a.sh[blockIdx.x];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int crank = static_cast<int>(cluster_ctarank());  // pair rank: which half of the pages it fetches
     const int nrows = it.ntok * G;
     const int nch = (it.npages + 7) / 8;
 
@@ -221,7 +222,7 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
         tma_prefetch_desc(&tm_kv);
         for (int b = 0; b < 2; ++b) {
             mbar_init(&kv_full[b], 1);
-            mbar_init(&kv_empty[b], 1);
+            mbar_init(&kv_empty[b], 2);  // the MMA issuers of both CTAs of the pair
             mbar_init(&s_full[b], 1);
             mbar_init(&s_free[b], 256);
         }
@@ -232,7 +233,9 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
     }
     if (warp == 8) tmem_alloc(tslot, 512);  // S0 [0,128) | S1 [128,256) | O [256,384)
     tc_fence_before();
-    __syncthreads();
+    // the pair's peer multicasts K/V into this CTA's stages and arrives on its
+    // barriers: both CTAs' barriers must be initialised first
+    cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tslot;
     stamp(a, blockIdx.x, 1);
@@ -250,13 +253,17 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                 const int np = min(8, it.npages - c * 8);
                 uint8_t* sK = sKV + b * 2 * SKV_BYTES;
                 uint8_t* sV = sK + SKV_BYTES;
+                // the chunk lands in both CTAs of the pair: each fetches every other
+                // page once from HBM and multicasts it (the shared prefix is read
+                // once for all 2 x 128 rows of this kv head)
                 mbar_expect_tx(&kv_full[b], static_cast<uint32_t>(np) * 4 * 2048);
-                for (int i = 0; i < np; ++i) {
+                for (int i = crank; i < np; i += 2) {
                     const int rk = a.layer_row0 + (spg[c * 8 + i] * 2 * a.Hkv + it.kvh) * PG;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        tma_load_2d(sK + h * SKV_BYTES / 2 + i * 2048, &tm_kv, &kv_full[b], h * 64, rk);
-                        tma_load_2d(sV + h * SKV_BYTES / 2 + i * 2048, &tm_kv, &kv_full[b], h * 64, rk + rows_per_head);
+                        tma_load_2d_mc(sK + h * SKV_BYTES / 2 + i * 2048, &tm_kv, &kv_full[b], h * 64, rk, 3);
+                        tma_load_2d_mc(sV + h * SKV_BYTES / 2 + i * 2048, &tm_kv, &kv_full[b], h * 64,
+                                       rk + rows_per_head, 3);
                     }
                 }
                 if (c == 0) stamp(a, blockIdx.x, 6);
@@ -281,7 +288,7 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                               umma_desc_sw128_lbo(v0 + kk * 2048, SKV_BYTES / 2, 1024), idesc,
                               (j > 0 || kk > 0) ? 1u : 0u);
                 umma_commit(o_done);
-                umma_commit(&kv_empty[j & 1]);
+                umma_commit_mc(&kv_empty[j & 1], 3);  // stage free in both CTAs once both PVs are done
             };
             mbar_wait(q_full, 0);
             for (int c = 0; c < nch; ++c) {
@@ -447,7 +454,9 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
         stamp(a, blockIdx.x, 5);
     }
     tc_fence_before();
-    __syncthreads();
+    // neither CTA of the pair may reuse its shared memory while the peer's
+    // multicast commits / copies can still target it
+    cluster_sync_all();
     if (warp == 8) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -826,10 +835,26 @@ void launch_g(const DecodeAttnArgs& a, const CUtensorMap& tm, cudaStream_t st) {
         configured = true;
     }
     // every SM: shared items first, the rest of the grid starts on the private queue at once
-    const int grid = std::max(a.n_sh, a.n_pv > 0 ? g_num_sms : 1);
+    int grid = std::max(a.n_sh, a.n_pv > 0 ? g_num_sms : 1);
+    grid += grid & 1;  // CTA pairs (clusters of 2)
+    if (a.n_sh & 1) throw std::runtime_error("decode_attention: shared items must come in pairs");
     DecodeAttnArgs k = a;
     k.merge_in_kernel = a.any_merge && grid <= g_num_sms ? 1 : 0;
-    launch_pdl(attn_decode_kernel<G>, dim3(grid), dim3(SH_THREADS), DA_SMEM, st, tm, k);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(SH_THREADS);
+    cfg.dynamicSmemBytes = DA_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    HK_CUDA(cudaLaunchKernelEx(&cfg, attn_decode_kernel<G>, tm, k));
     HK_LAUNCHED(1);
     static const bool no_merge = std::getenv("HK_ATTN_DEBUG_NO_MERGE") != nullptr;  // timing experiments only
     if (a.n_rows > 0 && a.any_merge && !no_merge && !k.merge_in_kernel) {
@@ -869,9 +894,12 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
     plan.pv.clear();
     plan.n_parts.assign(rows.size(), 0);
     plan.shared_bytes = plan.private_bytes = 0;
-    int tiles = 0;
+    int tiles = 0;  // shared CTAs per split (row blocks padded to pairs) x kv heads
     for (const auto& g : groups)
-        if (g.shared_pages > 0 && g.members > 1) tiles += (g.members + rb - 1) / rb * Hkv;
+        if (g.shared_pages > 0 && g.members > 1) {
+            const int nrb = (g.members + rb - 1) / rb;
+            tiles += (nrb + (nrb & 1)) * Hkv;
+        }
     plan.sh_cluster = 1;
     // private key split: about 8 private warps per SM over the whole step
     double priv_keys = 0;
@@ -912,12 +940,19 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
             int cpc = (nch + splits - 1) / splits;
             cpc = std::min(cpc, SH_MAX_PAGES / 8);
             splits = (nch + cpc - 1) / cpc;
-            for (int r0 = 0; r0 < g.members; r0 += rb)
-                for (int h = 0; h < Hkv; ++h)
-                    for (int k = 0; k < splits; ++k) {
+            // row blocks of the same (kv head, page range) are adjacent CTAs: they
+            // stream the same pages at the same time, so L2 serves the second copy
+            // row blocks of the same (kv head, page range) are CTA pairs (clusters
+            // of 2) that fetch the pages once and multicast them; an odd count is
+            // padded with an empty row block that only helps fetch
+            const int nrb = (g.members + rb - 1) / rb;
+            for (int h = 0; h < Hkv; ++h)
+                for (int k = 0; k < splits; ++k)
+                    for (int j = 0; j < nrb + (nrb & 1); ++j) {
+                        const int r0 = std::min(j * rb, g.members);
                         ShItem it{};
                         it.row0 = g.row0 + r0;
-                        it.ntok = std::min(rb, g.members - r0);
+                        it.ntok = std::max(0, std::min(rb, g.members - r0));
                         it.kvh = h;
                         it.ptab = rows[static_cast<size_t>(g.row0)].ptab;
                         it.page0 = k * cpc * 8;
