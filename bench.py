@@ -237,24 +237,39 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    traffic = {}
+    tp = ROOT / "profiles" / "r1_ncu_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text())
     if prof:
         g = prof["gemm"]
         gemm_ach = g["bytes"] / (g["ms"] / 1e3) / 1e9 if g["ms"] > 0 else None
-        line["roofline"] = {"bound": "hbm", "kernel": "gemm_tc_kernel (tcgen05 weight streaming, all GEMMs)",
+        gu = traffic.get("gemm_tc_kernel<64,4> gate/up (224 CTAs, T=64, N=28672, K=4096)")
+        line["roofline"] = {"bound": "hbm", "kernel": "gemm_tc_kernel / gemm_sk_kernel (tcgen05 weight streaming, all GEMMs)",
                             "achieved": gemm_ach, "peak": hbm, "unit": "GB/s",
                             "frac": gemm_ach / hbm if gemm_ach else None,
-                            "traffic": None, "peak_source": peak_src,
+                            "traffic": (gu["dram_read_bytes"] + gu["dram_write_bytes"]) if gu else None,
+                            "traffic_kernel": "gate/up launch, ncu --set full (algorithmic %d B)" % gu["algorithmic_bytes"]
+                            if gu else None,
+                            "peak_source": peak_src,
                             "share_of_step": g["ms"] / (prof_stats["pin_ms"] + prof_stats["iter_ms"])}
         # prefix-shared decode attention = shared-prefix items + private-suffix items + merge
         a_ms = prof["attn_shared"]["ms"] + prof["attn_private"]["ms"] + prof["attn_merge"]["ms"]
         a_b = prof["attn_shared"]["bytes"] + prof["attn_private"]["bytes"]
         if a_ms > 0:
             ach = a_b / (a_ms / 1e3) / 1e9
+            at = traffic.get("attn_decode_kernel<4> (configs[1] decode, k~5, 148 CTAs)")
             line["attention_roofline"] = {
-                "bound": "hbm", "kernel": "attn_mma_kernel<64,4> shared + attn_mma_kernel<32,3> private + merge",
-                "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
-                "peak_source": peak_src, "algorithmic_bytes_per_step": a_b / max(1, prof_stats["steps"]) * 0 + a_b,
-                "note": "bytes = shared-prefix KV once per group + private KV + Q/O, per layer, summed over the run"}
+                "bound": "hbm",
+                "kernel": "attn_decode_kernel (tcgen05 prefix-shared tiles, multicast CTA pairs + mma.sync private "
+                          "queue + in-kernel merge), one launch per layer",
+                "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": (at["dram_read_bytes"] + at["dram_write_bytes"]) if at else None,
+                "traffic_kernel": "one decode launch at k~5 (algorithmic %.0f B), ncu --set full" % at["algorithmic_bytes"]
+                if at else None,
+                "peak_source": peak_src, "algorithmic_bytes_run": a_b,
+                "note": "bytes = shared-prefix KV once per group + private KV + Q/O, per layer, summed over the run; "
+                        "time = CUDA events around each launch in one profiled run (no PDL overlap)"}
         line["kernel_ms_per_step"] = {k: v["ms"] for k, v in prof.items()}
     if not args.no_cpu_baseline:
         from oracle.cpu_sample import decode_step_sample
