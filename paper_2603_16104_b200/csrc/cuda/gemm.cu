@@ -195,33 +195,26 @@ __global__ void __launch_bounds__(128, 1)
         }
         cluster_sync_all();  // peers keep their smem until every rank has read it
     } else if (p.epi == kEpiSwiGLU) {
-        // TMEM lanes 0-63 hold gate rows, 64-127 the matching up rows (warp w
-        // may only read lanes 32w..32w+31): up values go through smem.
-        float* xs = reinterpret_cast<float*>(smem);  // [64][BN + 1], pipeline buffers are free now
-        if (warp >= 2) {
+        // TMEM lanes 0-63 hold gate rows, 64-127 the matching up rows (a warp
+        // may only read lanes 32w..32w+31): every warp parks its rows in smem,
+        // then all 128 threads produce silu(gate) * up with coalesced stores.
+        float* xs = reinterpret_cast<float*>(smem);  // [128][BN + 1], pipeline buffers are free now
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 8) {
-                float v[8];
-                tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+        for (int c = 0; c < BN; c += 8) {
+            float v[8];
+            tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) xs[(row - 64) * (BN + 1) + c + j] = v[j];
-            }
+            for (int j = 0; j < 8; ++j) xs[row * (BN + 1) + c + j] = v[j];
         }
         __syncthreads();
-        if (warp < 2) {
-            const int f = blockIdx.x * 64 + row;  // output feature
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 8) {
-                float v[8];
-                tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int n = n0 + c + j;
-                    if (n < p.T && m_ok) {
-                        const float g = v[j], u = xs[row * (BN + 1) + c + j];
-                        static_cast<bf16*>(p.out)[static_cast<size_t>(n) * p.ldo + f] = f2bf(g / (1.0f + expf(-g)) * u);
-                    }
-                }
+        const int nt = min(BN, p.T - n0);
+        for (int idx = threadIdx.x; idx < 64 * nt; idx += blockDim.x) {
+            const int r = idx & 63, c = idx >> 6;
+            const int f = blockIdx.x * 64 + r;  // output feature
+            if (blockIdx.x * BM + r < p.N) {
+                const float g = xs[r * (BN + 1) + c], u = xs[(r + 64) * (BN + 1) + c];
+                static_cast<bf16*>(p.out)[static_cast<size_t>(n0 + c) * p.ldo + f] =
+                    f2bf(__fdividef(g, 1.0f + __expf(-g)) * u);
             }
         }
     } else if (p.epi == kEpiArgmax) {
@@ -439,7 +432,9 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
     // (tools/gemm_sweep.py, profiles/r1_gemm_sweep.txt).
     const bool wide = (N + BM - 1) / BM >= g_num_sms;  // at least one whole wave of weight tiles
     static const bool sk_swiglu = std::getenv("HK_SK_SWIGLU") != nullptr;  // opt-in: slower on B200 (sweep)
-    if (T <= 64 && wide && (epi == kEpiArgmax || (sk_swiglu && epi == kEpiSwiGLU)) && force_splits == 0 &&
+    static const bool sk_all = std::getenv("HK_SK_ALL") != nullptr;        // experiments: every decode GEMM
+    if (T <= 64 && (wide || sk_all) && (epi == kEpiArgmax || (sk_swiglu && epi == kEpiSwiGLU) || sk_all) &&
+        force_splits == 0 &&
         bias == nullptr &&
         gemm_streamk_enabled()) {
         gemm_bf16_streamk(W, X, N, K, T, epi, out, ldo, st);

@@ -1,3 +1,2 @@
-timeout -s KILL 600 python -m pytest tests/test_gpu_kernels.py -q -x --timeout 300 2>&1 | tail -2
-echo "## default routing"; python tools/gemm_sweep.py 64
-echo "## no stream-K"; HK_GEMM_NO_STREAMK=1 python tools/gemm_sweep.py 64
+timeout -s KILL 600 python -m pytest tests/test_gpu_kernels.py -q -x --timeout 300 2>&1 | tail -1
+python tools/gemm_sweep.py 64
