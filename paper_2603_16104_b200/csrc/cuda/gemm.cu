@@ -38,6 +38,7 @@ struct GemmParams {
     const bf16* bias;
     float* partial;
     int cluster;  // 1: the grid.z split-K CTAs form a cluster and reduce through DSMEM
+    int skip_epi; // timing experiments only (HK_GEMM_DEBUG_SKIP_EPI): no output stores
 };
 
 template <int BN, int STAGES>
@@ -250,30 +251,60 @@ __global__ void __launch_bounds__(128, 1)
             if (n < p.T) reinterpret_cast<float2*>(p.out)[static_cast<size_t>(blockIdx.x) * p.T + n] = b;
         }
     }
-    const float bias = (p.bias && m_ok && p.epi != kEpiPartial) ? bf2f(p.bias[m]) : 0.f;
-#pragma unroll 1
-    for (int c = 0; c < BN && p.epi < kEpiSwiGLU && !p.cluster; c += 8) {
-        float v[8];
-        tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
-        if (!m_ok) continue;
+    if (p.epi < kEpiSwiGLU && !p.cluster && !p.skip_epi) {
+        // Stage the fp32 tile through shared memory as [token][feature] (the
+        // pipeline buffers are free now), then every warp writes whole rows of
+        // 128 consecutive features: 16-byte stores, 512 contiguous bytes per
+        // warp instruction, in the [token][ldo] / [split][token][N] layouts.
+        constexpr int SO = BM + 4;  // padded row: conflict-free column writes and float4 row reads
+        float* so = reinterpret_cast<float*>(smem);
+        const float bias = (p.bias && m_ok && p.epi != kEpiPartial) ? bf2f(p.bias[m]) : 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int n = n0 + c + j;
-            if (n >= p.T) break;
-            const float r = v[j] + bias;
-            switch (p.epi) {
-                case kEpiStoreBf16:
-                    static_cast<bf16*>(p.out)[static_cast<size_t>(n) * p.ldo + m] = f2bf(r);
-                    break;
-                case kEpiAddF32:
-                    static_cast<float*>(p.out)[static_cast<size_t>(n) * p.ldo + m] += r;
-                    break;
-                case kEpiStoreF32:
-                    static_cast<float*>(p.out)[static_cast<size_t>(n) * p.ldo + m] = r;
-                    break;
-                default:  // split-K partial
-                    p.partial[(static_cast<size_t>(blockIdx.z) * p.T + n) * p.N + m] = r;
-                    break;
+        for (int c = 0; c < BN; c += 32) {
+            if constexpr (BN >= 32) {
+                float v[32];
+                tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) so[(c + j) * SO + row] = v[j] + bias;
+            }
+        }
+        if constexpr (BN < 32) {
+#pragma unroll
+            for (int c = 0; c < BN; c += 8) {
+                float v[8];
+                tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) so[(c + j) * SO + row] = v[j] + bias;
+            }
+        }
+        __syncthreads();
+        const int rows = min(BN, p.T - n0);
+        const bool full_m = m0 + BM <= p.N;
+        for (int r = warp; r < rows; r += 4) {
+            const int n = n0 + r;
+            const float4 v = reinterpret_cast<const float4*>(so + r * SO)[lane];
+            const int mm = m0 + lane * 4;
+            if (p.epi == kEpiPartial) {
+                float* dst = p.partial + (static_cast<size_t>(blockIdx.z) * p.T + n) * p.N + mm;
+                if (full_m) {
+                    *reinterpret_cast<float4*>(dst) = v;
+                } else {
+                    const float e[4] = {v.x, v.y, v.z, v.w};
+                    for (int q = 0; q < 4; ++q)
+                        if (mm + q < p.N) dst[q] = e[q];
+                }
+            } else {
+                const float e[4] = {v.x, v.y, v.z, v.w};
+                for (int q = 0; q < 4; ++q) {
+                    if (mm + q >= p.N) break;
+                    const size_t o = static_cast<size_t>(n) * p.ldo + mm + q;
+                    if (p.epi == kEpiStoreBf16)
+                        static_cast<bf16*>(p.out)[o] = f2bf(e[q]);
+                    else if (p.epi == kEpiAddF32)
+                        static_cast<float*>(p.out)[o] += e[q];
+                    else
+                        static_cast<float*>(p.out)[o] = e[q];
+                }
             }
         }
     }
@@ -479,8 +510,9 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
         kbps = kb;
     }
     const bool via_ws = splits > 1 && !cluster && epi != kEpiPartial;
+    static const int skip_epi = std::getenv("HK_GEMM_DEBUG_SKIP_EPI") ? 1 : 0;
     GemmParams p{N, K, T, kb, kbps, via_ws ? kEpiPartial : epi, out, ldo, bias,
-                 epi == kEpiPartial ? static_cast<float*>(out) : workspace, cluster ? 1 : 0};
+                 epi == kEpiPartial ? static_cast<float*>(out) : workspace, cluster ? 1 : 0, skip_epi};
     const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
     const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
     dim3 grid(mt, nt, splits);
