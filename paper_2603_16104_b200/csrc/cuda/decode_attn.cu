@@ -374,54 +374,49 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
             xm[half * ROWS + row] = mx;
             named_bar(1, 256);
             mx = fmaxf(xm[row], xm[ROWS + row]) * a.sl2;  // log2 domain
+            // lazy rescale (exact: O and l always refer to m_run; p <= 2^8 between
+            // rescales). The exponentials only need the new running max, so they
+            // are computed (and packed to bf16 in registers) before waiting for
+            // PV(c-1); only the O rescale and the P store wait for it.
+            const bool need = mx > m_run + 8.f;
+            const float al = need ? ex2(m_run - mx) : 1.f;
+            if (need) {
+                l_half *= al;
+                m_run = mx;
+            }
+            const float nm = -m_run;
+            uint32_t pk[32];
+            float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float p0 = ex2(fmaf(s[2 * j], a.sl2, nm));
+                const float p1 = ex2(fmaf(s[2 * j + 1], a.sl2, nm));
+                ls[j & 3] += p0 + p1;
+                pk[j] = pack2(p0, p1);
+            }
+            l_half += (ls[0] + ls[1]) + (ls[2] + ls[3]);
             // PV(c-1) must be done before O is rescaled or P rewritten
             if (c > 0) {
                 mbar_wait(o_done, (c - 1) & 1);
                 tc_fence_after();
             }
-            // lazy rescale (exact: O and l always refer to m_run; p <= 2^8 between
-            // rescales). tcgen05.ld/st are warp-collective: a warp rescales together.
-            const bool need = mx > m_run + 8.f;
-            if (__any_sync(0xffffffffu, need)) {
-                const float al = need ? ex2(m_run - mx) : 1.f;
-                if (c > 0) {
+            // tcgen05.ld/st are warp-collective: a warp rescales together
+            if (c > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        float v[32];
-                        const uint32_t ta = t_lane + 256 + half * 64 + j * 32;
-                        tmem_ld32(ta, v);
+                for (int j = 0; j < 2; ++j) {
+                    float v[32];
+                    const uint32_t ta = t_lane + 256 + half * 64 + j * 32;
+                    tmem_ld32(ta, v);
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) v[e] *= al;
-                        tmem_st32(ta, v);
-                    }
-                    tmem_wait_st();
+                    for (int e = 0; e < 32; ++e) v[e] *= al;
+                    tmem_st32(ta, v);
                 }
-                if (need) {
-                    l_half *= al;
-                    m_run = mx;
-                }
+                tmem_wait_st();
             }
-            // p = 2^(s*scale - m) on the MUFU unit (a polynomial exp2 on the FMA pipes
-            // for half of the elements, ex2_poly, measured slower here: 1.67 vs 1.36 us/chunk)
-            const float nm = -m_run;
-            float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int j8 = 0; j8 < 8; ++j8) {
-                float p[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const float x = fmaf(s[j8 * 8 + e], a.sl2, nm);
-                    p[e] = ex2(x);
-                    ls[e & 3] += p[e];
-                }
-                uint4 w;
-                w.x = pack2(p[0], p[1]);
-                w.y = pack2(p[2], p[3]);
-                w.z = pack2(p[4], p[5]);
-                w.w = pack2(p[6], p[7]);
-                *reinterpret_cast<uint4*>(sP + half * (ROWS * 128) + sw128(row, j8)) = w;
-            }
-            l_half += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+            for (int j8 = 0; j8 < 8; ++j8)
+                *reinterpret_cast<uint4*>(sP + half * (ROWS * 128) + sw128(row, j8)) =
+                    make_uint4(pk[4 * j8], pk[4 * j8 + 1], pk[4 * j8 + 2], pk[4 * j8 + 3]);
             fence_proxy_async();
             tc_fence_before();
             mbar_arrive(p_full);
