@@ -37,6 +37,13 @@ double hkx_gemm_bench(const void* W, const void* X, void* out, int N, int K, int
 double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_rows, int H, int Hkv,
                             const int32_t* tables, const int32_t* offs, const int32_t* pos, const int32_t* group_rows,
                             const int32_t* group_shared_pages, int n_groups, void* out, int iters);
+/* Causal prefill attention of one chunk on the tensor-core tile path: n_tok
+ * tokens at positions start .. start+n_tok-1 (qkv rows 0 .. n_tok-1) attend keys
+ * [0, own position] through the page table (host array, table_len pages);
+ * out [n_tok][H][128] bf16. Replaces the attention implied by the reference's
+ * chunked prefill (simulator.cpp:331-343). Returns 0 or -1. */
+int hkx_prefill_attention(const void* qkv, const void* kv, int n_pages, int n_tok, int start, int H, int Hkv,
+                          const int32_t* table, int table_len, void* out);
 /* Debug: record per-CTA phase timestamps (%globaltimer, ns) of later
  * hkx_decode_attention calls into device_buf ([shared CTAs + private CTAs][8] u64);
  * NULL turns it off. */

@@ -169,7 +169,7 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 constexpr int SQ_BYTES = ROWS * HD * 2;   // 32 KB
 constexpr int SKV_BYTES = KC * HD * 2;    // 32 KB (K or V of one chunk)
 constexpr int SH_THREADS = 320;
-constexpr int SH_MAX_PAGES = 512;         // pages of one shared item
+constexpr int SH_MAX_PAGES = 1024;        // pages of one tile item (16K keys)
 constexpr int SH_SMEM = 1024 + SQ_BYTES + 2 * 2 * SKV_BYTES + ROWS * KC * 2 + 256 + 7 * ROWS * 4 + (ROWS + 4) * 4 +
                         SH_MAX_PAGES * 4;
 
@@ -241,10 +241,13 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
     stamp(a, blockIdx.x, 1);
 
     if (warp == 9) {
-        // ---- TMA producer. Shared pages were written by earlier steps, so their
-        // loads need not wait for this step's producers.
+        // ---- TMA producer. Decode tiles read shared pages written by earlier
+        // steps, so their loads need not wait for this step's producers; a causal
+        // prefill tile reads the chunk's own K/V, written by this step's RoPE
+        // kernel, and waits for it first.
         for (int i = lane; i < it.npages; i += 32) spg[i] = a.pages[it.ptab + it.page0 + i];
         __syncwarp();
+        if (it.flags & 1) pdl_wait();
         if (lane == 0) {
             const int rows_per_head = a.Hkv * PG;  // pool-map rows between K and V of a page
             for (int c = 0; c < nch; ++c) {
@@ -316,8 +319,12 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
         const int row = (warp & 3) * 32 + lane;
         const int half = warp >> 2;
         const uint32_t t_lane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        const bool causal = (it.flags & 1) != 0;
+        const int tok_base = causal ? it.row0 : a.dec_tok0 + it.row0;  // batch token of tile row 0
         pdl_wait();  // q comes from the qkv/RoPE kernel
         pdl_trigger();
+        // causal prefill rows attend keys <= their own position
+        const int prow = causal && row < nrows ? a.pos[tok_base + row / G] : 0x7fffffff;
         {
             // Q tile rows (token r / G, head kvh*G + r % G); rows >= nrows are zero.
             uint4 qv[8];
@@ -327,7 +334,7 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                 qv[i] = make_uint4(0u, 0u, 0u, 0u);
                 if (r < nrows)
                     qv[i] = __ldg(reinterpret_cast<const uint4*>(
-                        a.qkv + static_cast<size_t>(a.dec_tok0 + it.row0 + r / G) * a.QKV + (it.kvh * G + r % G) * HD +
+                        a.qkv + static_cast<size_t>(tok_base + r / G) * a.QKV + (it.kvh * G + r % G) * HD +
                         ch * 8));
             }
 #pragma unroll
@@ -358,7 +365,9 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                 if (col0 < nk) {
                     tmem_ld32(t_lane + b * 128 + col0, v);
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) s[j * 32 + e] = col0 + e < nk ? v[e] : -INFINITY;
+                    const int key0 = (it.page0 + c * 8) * PG + col0;
+                    for (int e = 0; e < 32; ++e)
+                        s[j * 32 + e] = (col0 + e < nk && key0 + e <= prow) ? v[e] : -INFINITY;
                 } else {
 #pragma unroll
                     for (int e = 0; e < 32; ++e) s[j * 32 + e] = -INFINITY;
@@ -440,10 +449,26 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
             for (int e = 0; e < 8; ++e) dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
         }
         named_bar(1, 256);
-        for (int r = warp; r < nrows; r += 8) {
-            const size_t pi = (static_cast<size_t>(it.row0 + r / G) * a.H + it.kvh * G + r % G) * a.max_parts + it.rank;
-            reinterpret_cast<float4*>(a.part_o + pi * HD)[lane] = reinterpret_cast<const float4*>(sO + r * SO)[lane];
-            if (lane == 0) a.part_ml[pi] = make_float2(red_m[r], red_l[r] + red_l[ROWS + r]);
+        if (causal) {
+            // the item covers every key of its rows: normalised bf16 output, one
+            // 256-byte row per (token, head) per warp instruction
+            for (int r = warp; r < nrows; r += 8) {
+                const float L = red_l[r] + red_l[ROWS + r];
+                const float inv = L > 0.f ? 1.f / L : 0.f;
+                const float4 v = reinterpret_cast<const float4*>(sO + r * SO)[lane];
+                bf16* o = a.out + (static_cast<size_t>(tok_base + r / G) * a.H + it.kvh * G + r % G) * HD + lane * 4;
+                uint2 pk;
+                pk.x = pack2(v.x * inv, v.y * inv);
+                pk.y = pack2(v.z * inv, v.w * inv);
+                *reinterpret_cast<uint2*>(o) = pk;
+            }
+        } else {
+            for (int r = warp; r < nrows; r += 8) {
+                const size_t pi =
+                    (static_cast<size_t>(it.row0 + r / G) * a.H + it.kvh * G + r % G) * a.max_parts + it.rank;
+                reinterpret_cast<float4*>(a.part_o + pi * HD)[lane] = reinterpret_cast<const float4*>(sO + r * SO)[lane];
+                if (lane == 0) a.part_ml[pi] = make_float2(red_m[r], red_l[r] + red_l[ROWS + r]);
+            }
         }
         stamp(a, blockIdx.x, 4);
         stamp(a, blockIdx.x, 5);
@@ -866,7 +891,6 @@ void launch_g(const DecodeAttnArgs& a, const CUtensorMap& tm, cudaStream_t st) {
 }  // namespace
 
 void decode_attention(const DecodeAttnArgs& a, const CUtensorMap& tm_kv, cudaStream_t st) {
-    if (a.n_sh > 0 && a.n_pv == 0) throw std::runtime_error("decode_attention: shared items need private items");
     switch (a.H / a.Hkv) {
         case 1: launch_g<1>(a, tm_kv, st); break;
         case 2: launch_g<2>(a, tm_kv, st); break;
@@ -987,6 +1011,38 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
             plan.private_bytes += 2.0 * H * HD * 2;  // q in, o out
         }
     }
+}
+
+double plan_prefill_attention(const std::vector<PrefillSegIn>& segs, int H, int Hkv, DecodePlan& plan) {
+    const int G = H / Hkv;
+    const int rb = ROWS / G;
+    double bytes = 0;
+    for (const auto& sg : segs) {
+        const int nrb = (sg.count + rb - 1) / rb;
+        for (int h = 0; h < Hkv; ++h)
+            for (int j = 0; j < nrb + (nrb & 1); j += 2) {
+                // a CTA pair shares the pages of its later row block (causal mask
+                // trims the earlier one); an odd block count gets an empty partner
+                const int last_tok = std::min(sg.count, (j + 2) * rb) - 1;
+                const int npages = (sg.start + last_tok) / PG + 1;
+                if (npages > SH_MAX_PAGES) throw std::runtime_error("prefill attention: context too long for a tile");
+                for (int q = 0; q < 2; ++q) {
+                    const int r0 = std::min((j + q) * rb, sg.count);
+                    ShItem it{};
+                    it.row0 = sg.tok0 + r0;
+                    it.ntok = std::max(0, std::min(rb, sg.count - r0));
+                    it.kvh = h;
+                    it.ptab = sg.ptab;
+                    it.page0 = 0;
+                    it.npages = npages;
+                    it.rank = -1;
+                    it.flags = 1;
+                    plan.sh.push_back(it);
+                }
+            }
+        bytes += (static_cast<double>(sg.start) + sg.count) * Hkv * 2.0 * HD * 2 + 2.0 * sg.count * H * HD * 2;
+    }
+    return bytes;
 }
 
 }  // namespace hkd

@@ -513,6 +513,7 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     int n_pre_items = 0, n_sh_items = 0, n_pv_items = 0;
     double alg_bytes = 0, alg_single = 0;  // algorithmic attention bytes: multi-token items | private items
     const double kv_tok_bytes = 2.0 * Hkv * hd * esz;
+    std::vector<hkd::PrefillSegIn> psegs;
     for (int i : pre) {
         SegIn& s = segs[i];
         const int off = static_cast<int>(pages.size());
@@ -530,11 +531,15 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
             kvw[t + j] = s.write_kv ? 1 : 0;
             ptab[t + j] = off;
         }
-        for (int c = 0; c < s.count; c += 16) {
-            const int n = std::min(16, s.count - c);
-            for (int kh = 0; kh < Hkv; ++kh)
-                items.push_back(hkd::AttnItem{t + c, n, kh, off, 0, s.start + c + n, 1, -1});
-            n_pre_items += Hkv;
+        if (f32) {
+            for (int c = 0; c < s.count; c += 16) {
+                const int n = std::min(16, s.count - c);
+                for (int kh = 0; kh < Hkv; ++kh)
+                    items.push_back(hkd::AttnItem{t + c, n, kh, off, 0, s.start + c + n, 1, -1});
+                n_pre_items += Hkv;
+            }
+        } else {
+            psegs.push_back(hkd::PrefillSegIn{t, s.count, s.start, off});  // tensor-core tiles (decode_attn.cu)
         }
         alg_bytes += (s.start + s.count) * kv_tok_bytes + 2.0 * s.count * H * hd * esz;
         if (s.sample) {
@@ -612,9 +617,13 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         gi = gj;
     }
     hkd::DecodePlan dplan;
-    if (!f32 && !dec.empty()) {
-        hkd::plan_decode_attention(drows, dgroups, H, Hkv, max_parts, hkd::g_num_sms, dplan);
-        nparts = dplan.n_parts;
+    double prefill_bytes = 0;
+    if (!f32) {
+        if (!dec.empty()) {
+            hkd::plan_decode_attention(drows, dgroups, H, Hkv, max_parts, hkd::g_num_sms, dplan);
+            nparts = dplan.n_parts;
+        }
+        prefill_bytes = hkd::plan_prefill_attention(psegs, H, Hkv, dplan);  // appended after the decode tiles
     }
     const int S = static_cast<int>(srows.size());
     if (S > maxS) throw std::runtime_error("engine: too many sampled rows in one step");
@@ -739,14 +748,9 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
                                  f32, st);
             clock.end(ck, st);
         } else {
-            if (n_multi > 0) {  // prefill chunks (causal, written directly)
-                ck = clock.begin(3, st);
-                hkd::attention_partial(aa, st);
-                clock.end(ck, st, alg_bytes - dplan.shared_bytes);
-            }
-            if (!dplan.pv.empty()) {
+            if (!dplan.pv.empty() || !dplan.sh.empty()) {
                 const size_t ctr_words = static_cast<size_t>(ec.max_calls * ec.n_workers + 16) * Hkv;
-                hkd::DecodeAttnArgs da{static_cast<const bf16*>(qkv), H, Hkv, QKV,
+                hkd::DecodeAttnArgs da{static_cast<const bf16*>(qkv), d_pos, H, Hkv, QKV,
                                        static_cast<const bf16*>(kv_layer(w, l)),
                                        static_cast<int>(static_cast<size_t>(l) * ec.pages_per_worker * 2 * Hkv * block),
                                        d_pages, d_sh, static_cast<int>(dplan.sh.size()), dplan.sh_cluster, d_pv,
@@ -759,10 +763,10 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
                                        wk.counters + ctr_words + 4 * l, wk.counters + ctr_words + 4 * l + 1,
                                        wk.counters + ctr_words + 4 * l + 2, 0, T_pre,
                                        static_cast<bf16*>(attn), scale * 1.4426950408889634f, nullptr};
-                // one event bracket: the two grids overlap (private, then shared under PDL)
-                ck = clock.begin(1, st);
+                // one launch: decode tiles + private queue + prefill tiles
+                ck = clock.begin(dec.empty() ? 3 : 1, st);
                 hkd::decode_attention(da, wk.tm_kv, st);
-                clock.end(ck, st, dplan.shared_bytes + dplan.private_bytes, 2);
+                clock.end(ck, st, dplan.shared_bytes + dplan.private_bytes + prefill_bytes, 1);
             }
         }
         sp = gemm(lw.wo, attn, d, H * hd, T, hkd::kEpiPartial, pbuf, d);

@@ -121,7 +121,7 @@ double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_
         HK_CUDA(cudaMemset(bufs[3], 0, (static_cast<size_t>(n_rows) * Hkv + 4) * 4));
         int32_t* ctr = static_cast<int32_t*>(bufs[3]);
         const CUtensorMap tm = hkd::make_tmap_2d_bf16(kv, static_cast<uint64_t>(n_pages) * 2 * Hkv * 16, 128, 64, 16);
-        hkd::DecodeAttnArgs a{static_cast<const hkd::bf16*>(qkv), H, Hkv, (H + 2 * Hkv) * 128,
+        hkd::DecodeAttnArgs a{static_cast<const hkd::bf16*>(qkv), nullptr, H, Hkv, (H + 2 * Hkv) * 128,
                               static_cast<const hkd::bf16*>(kv), 0, reinterpret_cast<const int32_t*>(m),
                               reinterpret_cast<const hkd::ShItem*>(m + o_sh), static_cast<int>(plan.sh.size()), plan.sh_cluster,
                               reinterpret_cast<const hkd::PvItem*>(m + o_pv), static_cast<int>(plan.pv.size()),
@@ -197,6 +197,46 @@ double hkx_decode_attention_bytes(int n_rows, int H, int Hkv, const int32_t* off
         return -1;
     }
     return plan.shared_bytes + plan.private_bytes;
+}
+
+int hkx_prefill_attention(const void* qkv, const void* kv, int n_pages, int n_tok, int start, int H, int Hkv,
+                          const int32_t* table, int table_len, void* out) {
+    void* bufs[2] = {nullptr, nullptr};
+    try {
+        init_sms();
+        if ((start + n_tok + 15) / 16 > table_len) throw std::runtime_error("hkx_prefill_attention: short table");
+        hkd::DecodePlan plan;
+        std::vector<hkd::PrefillSegIn> segs{hkd::PrefillSegIn{0, n_tok, start, 0}};
+        hkd::plan_prefill_attention(segs, H, Hkv, plan);
+        std::vector<int32_t> pos(static_cast<size_t>(n_tok));
+        for (int i = 0; i < n_tok; ++i) pos[static_cast<size_t>(i)] = start + i;
+        const size_t b_tab = static_cast<size_t>(table_len) * 4, b_pos = pos.size() * 4,
+                     b_sh = plan.sh.size() * sizeof(hkd::ShItem);
+        const size_t o_pos = (b_tab + 15) / 16 * 16, o_sh = o_pos + (b_pos + 15) / 16 * 16;
+        HK_CUDA(cudaMalloc(&bufs[0], o_sh + b_sh + 64));
+        uint8_t* m = static_cast<uint8_t*>(bufs[0]);
+        HK_CUDA(cudaMemcpy(m, table, b_tab, cudaMemcpyHostToDevice));
+        HK_CUDA(cudaMemcpy(m + o_pos, pos.data(), b_pos, cudaMemcpyHostToDevice));
+        HK_CUDA(cudaMemcpy(m + o_sh, plan.sh.data(), b_sh, cudaMemcpyHostToDevice));
+        HK_CUDA(cudaMalloc(&bufs[1], 64));
+        HK_CUDA(cudaMemset(bufs[1], 0, 64));
+        int32_t* ctr = static_cast<int32_t*>(bufs[1]);
+        const CUtensorMap tm = hkd::make_tmap_2d_bf16(kv, static_cast<uint64_t>(n_pages) * 2 * Hkv * 16, 128, 64, 16);
+        hkd::DecodeAttnArgs a{static_cast<const hkd::bf16*>(qkv), reinterpret_cast<const int32_t*>(m + o_pos), H, Hkv,
+                              (H + 2 * Hkv) * 128, static_cast<const hkd::bf16*>(kv), 0,
+                              reinterpret_cast<const int32_t*>(m), reinterpret_cast<const hkd::ShItem*>(m + o_sh),
+                              static_cast<int>(plan.sh.size()), 1, nullptr, 0, nullptr, nullptr, 32, nullptr, ctr, 0, 0,
+                              ctr + 4, ctr + 5, ctr + 6, 0, n_tok, static_cast<hkd::bf16*>(out),
+                              1.4426950408889634f / sqrtf(128.f), nullptr};
+        hkd::decode_attention(a, tm, nullptr);
+        HK_CUDA(cudaDeviceSynchronize());
+        for (void* b : bufs) cudaFree(b);
+        return 0;
+    } catch (const std::exception& e) {
+        for (void* b : bufs) cudaFree(b);
+        hk::set_error(e.what());
+        return -1;
+    }
 }
 
 }  // extern "C"

@@ -136,8 +136,9 @@ struct ShItem {
     int ptab;    // block table (arena offset) of the group's first member
     int page0;   // first shared page (index into the table)
     int npages;  // shared pages covered by this item (may be 0)
-    int rank;    // rank in the cluster of items covering the same rows (all pages of the group)
-    int pad;
+    int rank;    // partial index (decode items)
+    int flags;   // bit0: causal prefill item — row0 is a batch token, keys <= the row's
+                 // position, the normalised bf16 output is written directly
 };
 struct PvItem {
     int row;     // decode row
@@ -150,6 +151,7 @@ struct PvItem {
 };
 struct DecodeAttnArgs {
     const bf16* qkv;        // [T][QKV]
+    const int32_t* pos;     // [T] token positions (causal prefill items)
     int H, Hkv, QKV;
     const bf16* kv_layer;   // this layer's pool [P][2][Hkv][16][128]
     int layer_row0;         // first row of this layer in the pool tensor map
@@ -193,6 +195,16 @@ struct DecodePlan {
 };
 void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vector<DecodeGroupIn>& groups, int H,
                            int Hkv, int max_parts, int num_sms, DecodePlan& plan);
+// Causal prefill chunks on the same tensor-core tile path: appends paired
+// items (prompt tokens x q-heads of one kv head, keys = the call's pages up
+// to the chunk's last position) to plan.sh. Returns the algorithmic bytes.
+struct PrefillSegIn {
+    int tok0;   // batch token of the chunk's first token
+    int count;  // tokens in the chunk
+    int start;  // position of the first token
+    int ptab;   // block table offset in the arena
+};
+double plan_prefill_attention(const std::vector<PrefillSegIn>& segs, int H, int Hkv, DecodePlan& plan);
 // tm_kv: the worker's whole pool as a [L*P*2*Hkv*16][128] bf16 tensor map, box {64, 16}.
 void decode_attention(const DecodeAttnArgs& a, const CUtensorMap& tm_kv, cudaStream_t st);
 

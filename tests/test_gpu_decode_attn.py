@@ -140,3 +140,36 @@ def test_decode_attention_hbm_throughput_reported():
     _, ms, nbytes = run(case, iters=20)
     print(f"decode attention c2 k=128: {ms * 1e3:.2f} us/launch, {nbytes / ms / 1e6:.0f} GB/s algorithmic")
     assert ms > 0
+
+
+# ------------------------------------------------ causal prefill (tile path)
+PREFILL_CASES = [(2, 1, 10, 0), (2, 1, 33, 0), (2, 1, 60, 0), (2, 1, 77, 5), (2, 1, 130, 0),
+                 (32, 8, 10, 0), (32, 8, 33, 17), (32, 8, 64, 0), (32, 8, 100, 300), (40, 8, 50, 0)]
+
+
+@pytest.mark.parametrize("H,Hkv,n,start", PREFILL_CASES)
+def test_prefill_attention_matches_causal_fp32_reference(H, Hkv, n, start):
+    g = torch.Generator(device="cpu").manual_seed(n * 131 + start)
+    n_pages = (start + n + 15) // 16 + 8
+    table = torch.randperm(n_pages, generator=g)[: (start + n + 15) // 16].tolist()
+    kv = (torch.randn(n_pages, 2, Hkv, PG, HD, generator=g) * 0.5).to(torch.bfloat16).cuda()
+    qkv = torch.randn(n, (H + 2 * Hkv) * HD, generator=g).to(torch.bfloat16).cuda()
+    out = torch.zeros(n, H, HD, dtype=torch.bfloat16, device="cuda")
+    t, tp = _i32(table)
+    rc = _lib.load().hkx_prefill_attention(C.c_void_p(qkv.data_ptr()), C.c_void_p(kv.data_ptr()), n_pages, n, start,
+                                           H, Hkv, tp, len(table), C.c_void_p(out.data_ptr()))
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    G = H // Hkv
+    pages = torch.tensor(table, device="cuda", dtype=torch.long)
+    k = kv[pages, 0].float().permute(1, 0, 2, 3).reshape(Hkv, -1, HD)
+    v = kv[pages, 1].float().permute(1, 0, 2, 3).reshape(Hkv, -1, HD)
+    q = qkv[:, :H * HD].float().view(n, Hkv, G, HD)
+    s = torch.einsum("thgd,hkd->thgk", q, k) / np.sqrt(HD)
+    keys = torch.arange(k.shape[1], device="cuda")
+    pos = start + torch.arange(n, device="cuda")
+    s = s.masked_fill((keys[None, :] > pos[:, None])[:, None, None, :], float("-inf"))
+    ref = torch.einsum("thgk,hkd->thgd", torch.softmax(s, dim=-1), v).reshape(n, H, HD)
+    err = (out.float() - ref).abs().amax(dim=(1, 2))
+    bad = (err > 1e-2 * ref.abs().max()).nonzero().flatten().tolist()
+    assert not bad, (bad[:10], err.max().item())
