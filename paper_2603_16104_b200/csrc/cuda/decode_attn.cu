@@ -154,6 +154,19 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// This CTA's slice of the L2 prefetch of the next kernel's weights (lane 0).
+__device__ __forceinline__ void prefetch_next_weights(const DecodeAttnArgs& a) {
+    if (!a.l2_prefetch || a.l2_prefetch_bytes == 0) return;
+    const size_t per = (a.l2_prefetch_bytes / gridDim.x + 4095) & ~size_t(4095);
+    const size_t b0 = per * blockIdx.x;
+    if (b0 >= a.l2_prefetch_bytes) return;
+    const size_t b1 = b0 + per < a.l2_prefetch_bytes ? b0 + per : a.l2_prefetch_bytes;
+    const uint64_t pol = policy_evict_last();
+    const char* base = static_cast<const char*>(a.l2_prefetch);
+    for (size_t o = b0; o < b1; o += 32768)
+        l2_prefetch_bulk(base + o, static_cast<uint32_t>(b1 - o < 32768 ? b1 - o : 32768), pol);
+}
+
 // ------------------------------------------------------- shared (tcgen05)
 // Warp-specialised, one CTA per SM (320 threads):
 //   warp 9  (TMA)     page ids -> smem, then K/V chunks of 8 pages into a
@@ -271,6 +284,7 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                 }
                 if (c == 0) stamp(a, blockIdx.x, 6);
             }
+            prefetch_next_weights(a);
         }
         pdl_wait();
         pdl_trigger();
@@ -800,6 +814,7 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
                 }
             }
         }
+        if (warp == DA_PV_WARPS + 1 && lane == 0) prefetch_next_weights(a);  // (weights: no dependency)
         pdl_wait();  // q and this step's own K/V come from the qkv/RoPE kernel
         if (warp >= DA_PV_WARPS) return;
     }

@@ -169,6 +169,7 @@ struct hk_engine {
     std::map<std::vector<int64_t>, GraphEntry> graphs;
     std::map<std::vector<int64_t>, int> graph_seen;
     bool use_graphs = true;
+    bool l2_prefetch_o = false;  // decode attention pulls the O-projection weights into L2 (opt-in)
     void drop_graphs() {
         for (auto& [k, g] : graphs) cudaGraphExecDestroy(g.exec);
         graphs.clear();
@@ -287,6 +288,9 @@ hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m
         throw std::runtime_error("engine: bad engine config");
     HK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     use_graphs = std::getenv("HK_NO_GRAPHS") == nullptr;
+    // opt-in: measured -2% on configs[1] (the prefetch traffic slows the attention more
+    // than the O projection gains; profiles/r1_attention.txt)
+    l2_prefetch_o = std::getenv("HK_L2_PREFETCH_O") != nullptr;
     hkd::g_pdl = std::getenv("HK_NO_PDL") == nullptr;
     init_weights();
 
@@ -762,7 +766,9 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
                                        // griddepcontrol.wait, so layers never share it
                                        wk.counters + ctr_words + 4 * l, wk.counters + ctr_words + 4 * l + 1,
                                        wk.counters + ctr_words + 4 * l + 2, 0, T_pre,
-                                       static_cast<bf16*>(attn), scale * 1.4426950408889634f, nullptr};
+                                       static_cast<bf16*>(attn), scale * 1.4426950408889634f, nullptr,
+                                       l2_prefetch_o ? lw.wo : nullptr,
+                                       static_cast<size_t>(d) * H * hd * esz};
                 // one launch: decode tiles + private queue + prefill tiles
                 ck = clock.begin(dec.empty() ? 3 : 1, st);
                 hkd::decode_attention(da, wk.tm_kv, st);

@@ -130,7 +130,7 @@ double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_
                               ctr + static_cast<size_t>(n_rows) * Hkv,
                               ctr + static_cast<size_t>(n_rows) * Hkv + 1, ctr + static_cast<size_t>(n_rows) * Hkv + 2,
                               0, 0,
-                              static_cast<hkd::bf16*>(out), 1.4426950408889634f / sqrtf(128.f), g_trace};
+                              static_cast<hkd::bf16*>(out), 1.4426950408889634f / sqrtf(128.f), g_trace, nullptr, 0};
         hkd::decode_attention(a, tm, nullptr);
         HK_CUDA(cudaDeviceSynchronize());
         double ms = 0;
@@ -227,7 +227,7 @@ int hkx_prefill_attention(const void* qkv, const void* kv, int n_pages, int n_to
                               reinterpret_cast<const int32_t*>(m), reinterpret_cast<const hkd::ShItem*>(m + o_sh),
                               static_cast<int>(plan.sh.size()), 1, nullptr, 0, nullptr, nullptr, 32, nullptr, ctr, 0, 0,
                               ctr + 4, ctr + 5, ctr + 6, 0, n_tok, static_cast<hkd::bf16*>(out),
-                              1.4426950408889634f / sqrtf(128.f), nullptr};
+                              1.4426950408889634f / sqrtf(128.f), nullptr, nullptr, 0};
         hkd::decode_attention(a, tm, nullptr);
         HK_CUDA(cudaDeviceSynchronize());
         for (void* b : bufs) cudaFree(b);

@@ -176,6 +176,8 @@ struct DecodeAttnArgs {
     bf16* out;              // [T][H][128]
     float sl2;              // softmax scale * log2(e)
     unsigned long long* trace;  // optional [n_sh + n_pv][8] %globaltimer stamps per CTA phase (null = off)
+    const void* l2_prefetch;    // optional: bytes the next kernel streams (O-projection weights), pulled
+    size_t l2_prefetch_bytes;   // into L2 by otherwise idle warps while HBM is under-used
 };
 // Host planning of one step's decode rows. Rows of a group are consecutive
 // and share `shared_pages` leading pages of their block tables.
