@@ -144,8 +144,24 @@ __device__ __forceinline__ void stamp(const DecodeAttnArgs& a, int cta, int k) {
     if (a.trace && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (k == 6 || k == 9 || k == 10 || k == 11) t = clock64();  // fine-grained (cycles) chunk-1 stamps
         a.trace[static_cast<size_t>(cta) * 16 + k] = t;
         if (k == 0 || k == 5) a.trace[static_cast<size_t>(cta) * 16 + 14 + (k == 5)] = clock64();
+    }
+}
+
+// per private item (debug trace): [claim, first page landed, done, (smid << 8) | warp]
+__device__ __forceinline__ void item_stamp(const DecodeAttnArgs& a, int item, int k) {
+    if (a.trace && (threadIdx.x & 31) == 0 && item < 6000) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        unsigned long long* q = a.trace + 32768 + static_cast<size_t>(item) * 4;
+        q[k] = t;
+        if (k == 0) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            q[3] = (static_cast<unsigned long long>(smid) << 8) | (threadIdx.x >> 5);
+        }
     }
 }
 
@@ -211,14 +227,18 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
     uint8_t* sKV = sm + SQ_BYTES;  // stage b: K at b*2*SKV_BYTES, V at +SKV_BYTES
     uint8_t* sP = sKV + 4 * SKV_BYTES;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sP + ROWS * KC * 2);
-    uint64_t* kv_full = bars;       // [2] chunk landed (TMA tx)
-    uint64_t* kv_empty = bars + 2;  // [2] chunk consumed (PV commit)
+    // K and V of a chunk have their own barriers: K(c + 2) streams in as soon as
+    // S(c) has read K(c), long before PV(c) frees V(c)
+    uint64_t* k_full = bars;        // [2] K chunk landed (TMA tx)
+    uint64_t* k_empty = bars + 2;   // [2] K chunk consumed (S commit, both CTAs of the pair)
     uint64_t* s_full = bars + 4;    // [2] S buffer written (MMA commit)
     uint64_t* s_free = bars + 6;    // [2] S buffer read (256 softmax threads)
     uint64_t* p_full = bars + 8;    // P written (256 softmax threads)
     uint64_t* o_done = bars + 9;    // PV complete (MMA commit)
     uint64_t* q_full = bars + 10;   // Q tile written (256 softmax threads)
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 12);
+    uint64_t* v_full = bars + 11;   // [2] V chunk landed
+    uint64_t* v_empty = bars + 13;  // [2] V chunk consumed (PV commit, both CTAs)
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
 
     float* red = reinterpret_cast<float*>(sm + SQ_BYTES + 4 * SKV_BYTES + ROWS * KC * 2 + 256);  // [2][128] x 2
     int* flags = reinterpret_cast<int*>(red + 7 * ROWS);  // [ROWS] tokens this CTA merges, [ROWS] count
@@ -234,8 +254,10 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
     if (tid == 0) {
         tma_prefetch_desc(&tm_kv);
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&kv_full[b], 1);
-            mbar_init(&kv_empty[b], 2);  // the MMA issuers of both CTAs of the pair
+            mbar_init(&k_full[b], 1);
+            mbar_init(&k_empty[b], 2);  // the MMA issuers of both CTAs of the pair
+            mbar_init(&v_full[b], 1);
+            mbar_init(&v_empty[b], 2);
             mbar_init(&s_full[b], 1);
             mbar_init(&s_free[b], 256);
         }
@@ -263,26 +285,26 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
         if (it.flags & 1) pdl_wait();
         if (lane == 0) {
             const int rows_per_head = a.Hkv * PG;  // pool-map rows between K and V of a page
-            for (int c = 0; c < nch; ++c) {
+            // the chunk lands in both CTAs of the pair: each fetches every other
+            // page once from HBM and multicasts it (the shared prefix is read
+            // once for all 2 x 128 rows of this kv head)
+            auto load = [&](int c, int v) {
                 const int b = c & 1;
-                if (c >= 2) mbar_wait(&kv_empty[b], ((c >> 1) - 1) & 1);
+                uint64_t* full = v ? &v_full[b] : &k_full[b];
+                if (c >= 2) mbar_wait(v ? &v_empty[b] : &k_empty[b], ((c >> 1) - 1) & 1);
                 const int np = min(8, it.npages - c * 8);
-                uint8_t* sK = sKV + b * 2 * SKV_BYTES;
-                uint8_t* sV = sK + SKV_BYTES;
-                // the chunk lands in both CTAs of the pair: each fetches every other
-                // page once from HBM and multicasts it (the shared prefix is read
-                // once for all 2 x 128 rows of this kv head)
-                mbar_expect_tx(&kv_full[b], static_cast<uint32_t>(np) * 4 * 2048);
+                uint8_t* dst = sKV + b * 2 * SKV_BYTES + v * SKV_BYTES;
+                mbar_expect_tx(full, static_cast<uint32_t>(np) * 2 * 2048);
                 for (int i = crank; i < np; i += 2) {
-                    const int rk = a.layer_row0 + (spg[c * 8 + i] * 2 * a.Hkv + it.kvh) * PG;
+                    const int rk = a.layer_row0 + (spg[c * 8 + i] * 2 * a.Hkv + it.kvh) * PG + v * rows_per_head;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        tma_load_2d_mc(sK + h * SKV_BYTES / 2 + i * 2048, &tm_kv, &kv_full[b], h * 64, rk, 3);
-                        tma_load_2d_mc(sV + h * SKV_BYTES / 2 + i * 2048, &tm_kv, &kv_full[b], h * 64,
-                                       rk + rows_per_head, 3);
-                    }
+                    for (int h = 0; h < 2; ++h) tma_load_2d_mc(dst + h * SKV_BYTES / 2 + i * 2048, &tm_kv, full, h * 64, rk, 3);
                 }
-                if (c == 0) stamp(a, blockIdx.x, 6);
+            };
+            // K runs one chunk ahead of V (V(c) is needed a softmax later than K(c))
+            for (int c = 0; c <= nch; ++c) {
+                if (c < nch) load(c, 0);
+                if (c >= 1) load(c - 1, 1);
             }
             prefetch_next_weights(a);
         }
@@ -296,6 +318,7 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
             const uint32_t q0 = smem_u32(sQ), p0 = smem_u32(sP);
             auto issue_pv = [&](int j) {
                 mbar_wait(p_full, j & 1);
+                mbar_wait(&v_full[j & 1], (j >> 1) & 1);
                 tc_fence_after();
                 const int np = min(8, it.npages - j * 8);
                 const uint32_t v0 = smem_u32(sKV + (j & 1) * 2 * SKV_BYTES + SKV_BYTES);
@@ -305,12 +328,11 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                               umma_desc_sw128_lbo(v0 + kk * 2048, SKV_BYTES / 2, 1024), idesc,
                               (j > 0 || kk > 0) ? 1u : 0u);
                 umma_commit(o_done);
-                umma_commit_mc(&kv_empty[j & 1], 3);  // stage free in both CTAs once both PVs are done
+                umma_commit_mc(&v_empty[j & 1], 3);  // V stage free in both CTAs once both PVs are done
             };
-            mbar_wait(q_full, 0);
-            for (int c = 0; c < nch; ++c) {
+            auto issue_s = [&](int c) {
                 const int b = c & 1;
-                mbar_wait(&kv_full[b], (c >> 1) & 1);
+                mbar_wait(&k_full[b], (c >> 1) & 1);
                 if (c >= 2) mbar_wait(&s_free[b], ((c >> 1) - 1) & 1);
                 tc_fence_after();
                 const int nk = min(8, it.npages - c * 8) * PG;
@@ -323,9 +345,20 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                               umma_desc_sw128(k0 + off), idesc, kk > 0 ? 1u : 0u);
                 }
                 umma_commit(&s_full[b]);
-                if (c >= 1) issue_pv(c - 1);
+                umma_commit_mc(&k_empty[b], 3);  // K stage free in both CTAs once both S are done
+            };
+            mbar_wait(q_full, 0);
+            issue_s(0);
+            if (nch > 1) issue_s(1);
+            for (int c = 0; c < nch; ++c) {
+                // PV(c) and S(c + 2) are issued only once the softmax warps hold
+                // S(c + 1) in registers: a tcgen05.ld queued behind in-flight MMAs
+                // waits for them (measured 0.8 us per chunk), so the tensor pipe
+                // works while the softmax computes, not while it reads TMEM
+                if (c + 1 < nch) mbar_wait(&s_free[(c + 1) & 1], ((c + 1) >> 1) & 1);
+                issue_pv(c);
+                if (c + 2 < nch) issue_s(c + 2);
             }
-            issue_pv(nch - 1);
         }
         __syncwarp();
     } else {
@@ -370,25 +403,25 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
             mbar_wait(&s_full[b], (c >> 1) & 1);
             tc_fence_after();
             if (c == 0) stamp(a, blockIdx.x, 7);
+            if (c == 1) stamp(a, blockIdx.x, 9);
             // raw scores (the softmax scale is folded into the exp2 argument)
             float s[64];
+            {
+                // one 64-column load (columns past nk hold stale bits: masked)
+                tmem_ld64(t_lane + b * 128 + half * 64, s);
+                if (c == 1) stamp(a, blockIdx.x, 6);
+                const int col0 = half * 64;
+                const int key0 = (it.page0 + c * 8) * PG + col0;
+                if (causal || col0 + 64 > nk) {  // (warp-uniform) full decode chunks need no mask
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int col0 = half * 64 + j * 32;
-                float v[32];
-                if (col0 < nk) {
-                    tmem_ld32(t_lane + b * 128 + col0, v);
-#pragma unroll
-                    const int key0 = (it.page0 + c * 8) * PG + col0;
-                    for (int e = 0; e < 32; ++e)
-                        s[j * 32 + e] = (col0 + e < nk && key0 + e <= prow) ? v[e] : -INFINITY;
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) s[j * 32 + e] = -INFINITY;
+                    for (int e = 0; e < 64; ++e)
+                        if (!(col0 + e < nk && key0 + e <= prow)) s[e] = -INFINITY;
                 }
             }
+            if (c == 1) stamp(a, blockIdx.x, 11);
             tc_fence_before();
             mbar_arrive(&s_free[b]);  // this thread is done with S buffer b
+            if (c == 1) stamp(a, blockIdx.x, 10);
             float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
             for (int j = 0; j < 64; ++j) mx4[j & 3] = fmaxf(mx4[j & 3], s[j]);
@@ -516,6 +549,11 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(addr));
 }
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
 __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -577,11 +615,11 @@ __device__ __forceinline__ int pv_safe_pages(const PvItem& it) {
 template <int G>
 __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const DecodeAttnArgs& a, const PvItem& it,
                                              int my_page, uint8_t* ring, uint64_t* full, int& pc, PvNext& nx,
-                                             int pre = 0) {
+                                             int pre = 0, int item = 0) {
+    item_stamp(a, item, 0);
     static_assert(G <= 8, "private item: G q-heads must fit rows 0-7 of the MMA tile");
     const int lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
-    const int p0 = it.kbeg / PG;
     const int np = (it.kend - it.kbeg + PG - 1) / PG;
     const uint32_t ring_s = smem_u32(ring);
     // (my_page: page ids of the item, one per lane; np <= 32 for this kernel's key splits)
@@ -591,7 +629,7 @@ __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const Dec
         const int pg = __shfl_sync(0xffffffffu, my_page, i);
         if (lane == 0 && i >= pre && i < np) issue(i, pg);
     }
-    // Q as the A operand (rows gid < G hold q heads kvh*G + gid; rows >= 8 are zero)
+    // Q^T as the B operand: column gid = q head kvh*G + gid (heads >= G are zero)
     uint32_t qa[8][2];
     {
         const bf16* qp = a.qkv + static_cast<size_t>(a.dec_tok0 + it.row) * a.QKV + (it.kvh * G + gid) * HD + 2 * tig;
@@ -601,65 +639,78 @@ __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const Dec
             qa[ks][1] = gid < G ? *reinterpret_cast<const uint32_t*>(qp + ks * 16 + 8) : 0u;
         }
     }
-    float o[16][4];
+    // Swapped operands (the q heads are the 8-wide N dimension, keys / dims the
+    // 16-row M dimension): S^T = K Q^T is 8 mma per page and O^T += V^T P^T is
+    // 8 more (half the MMAs of a 16-row Q tile padded from G rows). Lane
+    // (gid, tig) holds heads h0 = 2 tig, h1 = 2 tig + 1 (heads >= G are zero
+    // padding) for keys gid, gid + 8 (S^T) and dims mt*16 + gid (+ 8) (O^T).
+    float o[8][4];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;  // row gid (rows gid + 8 are padding)
+    for (int j = 0; j < 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // heads h0, h1 (log2 domain)
     // ldmatrix lane roles: matrix mi = lane / 8, row within it rr = lane % 8
     const int mi = lane >> 3, rr = lane & 7;
     for (int i = 0; i < np; ++i) {
         const int s = (pc + i) % PV_ST;
         mbar_wait(&full[s], ((pc + i) / PV_ST) & 1);
+        if (i == 0) item_stamp(a, item, 1);
         const uint32_t kt = ring_s + s * 8192, vt = kt + 4096;
-        // S = Q K^T: two n-tiles of 8 keys
-        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        // S^T = K Q^T: A = K [16 keys][16 dims] (ldmatrix), B = Q^T; two
+        // accumulators halve the dependent MMA chain
+        float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
-            uint32_t b0, b1, b2, b3;  // (keys 0-7 | 8-15) x (dims lo | hi of the k-step)
-            ldsm_x4(kt + tile_off((mi >> 1) * 8 + rr, 2 * ks + (mi & 1)), b0, b1, b2, b3);
-            const uint32_t af[4] = {qa[ks][0], 0u, qa[ks][1], 0u};
-            mma16816(sc[0], af, b0, b1);
-            mma16816(sc[1], af, b2, b3);
+            uint32_t af[4];
+            ldsm_x4(kt + tile_off((mi & 1) * 8 + rr, 2 * ks + (mi >> 1)), af[0], af[1], af[2], af[3]);
+            if (ks & 1)
+                mma16816(sb, af, qa[ks][0], qa[ks][1]);
+            else
+                mma16816(sa, af, qa[ks][0], qa[ks][1]);
         }
-        // online softmax on row gid (values sc[j][0..1]; [2..3] are padding rows)
         const int kb = it.kbeg + i * PG;
-        float mx = -INFINITY;
+        const bool vlo = kb + gid < it.kend, vhi = kb + gid + 8 < it.kend;
+        const float s0 = vlo ? (sa[0] + sb[0]) * a.sl2 : -INFINITY;  // key gid, head h0
+        const float s1 = vlo ? (sa[1] + sb[1]) * a.sl2 : -INFINITY;  // key gid, head h1
+        const float s2 = vhi ? (sa[2] + sb[2]) * a.sl2 : -INFINITY;  // key gid + 8, head h0
+        const float s3 = vhi ? (sa[3] + sb[3]) * a.sl2 : -INFINITY;  // key gid + 8, head h1
+        float x0 = fmaxf(s0, s2), x1 = fmaxf(s1, s3);
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const bool valid = kb + j * 8 + 2 * tig + e < it.kend;
-                sc[j][e] = valid ? sc[j][e] * a.sl2 : -INFINITY;
-                mx = fmaxf(mx, sc[j][e]);
-            }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        if (mx > m_run) {  // (quad-uniform)
-            const float al = ex2(m_run - mx);
-            l_run *= al;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                o[j][0] *= al;
-                o[j][1] *= al;
-            }
-            m_run = mx;
+        for (int off = 4; off < 32; off <<= 1) {
+            x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+            x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, off));
         }
-        float p[2][2];
+        if (x0 > m0) {  // (uniform over the 8 lanes of a head pair)
+            const float al = ex2(m0 - x0);
+            l0 *= al;
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                p[j][e] = ex2(sc[j][e] - m_run);
-                l_run += p[j][e];
+            for (int j = 0; j < 8; ++j) {
+                o[j][0] *= al;
+                o[j][2] *= al;
             }
-        const uint32_t pa[4] = {pack2(p[0][0], p[0][1]), 0u, pack2(p[1][0], p[1][1]), 0u};
-        // O += P V: V tile [key][dim], B operand via ldmatrix.trans, two dim n-tiles per load
+            m0 = x0;
+        }
+        if (x1 > m1) {
+            const float al = ex2(m1 - x1);
+            l1 *= al;
 #pragma unroll
-        for (int dp = 0; dp < 8; ++dp) {
-            uint32_t b0, b1, b2, b3;  // (keys 0-7 | 8-15) x (dims 16dp.. | 16dp+8..)
-            ldsm_x4_t(vt + tile_off((mi & 1) * 8 + rr, 2 * dp + (mi >> 1)), b0, b1, b2, b3);
-            mma16816(o[2 * dp], pa, b0, b1);
-            mma16816(o[2 * dp + 1], pa, b2, b3);
+            for (int j = 0; j < 8; ++j) {
+                o[j][1] *= al;
+                o[j][3] *= al;
+            }
+            m1 = x1;
+        }
+        const float p0 = ex2(s0 - m0), p1 = ex2(s1 - m1), p2 = ex2(s2 - m0), p3 = ex2(s3 - m1);
+        l0 += p0 + p2;
+        l1 += p1 + p3;
+        // P^T as the B operand [16 keys][8 heads]: transpose the two 8x8 bf16
+        // blocks of the S^T accumulator layout in registers
+        const uint32_t pb0 = movmatrix_t(pack2(p0, p1)), pb1 = movmatrix_t(pack2(p2, p3));
+        // O^T += V^T P^T: A = V^T [16 dims][16 keys] via ldmatrix.trans of the [key][dim] tile
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+            uint32_t af[4];
+            ldsm_x4_t(vt + tile_off((mi >> 1) * 8 + rr, 2 * mt + (mi & 1)), af[0], af[1], af[2], af[3]);
+            mma16816(o[mt], af, pb0, pb1);
         }
         // every lane has read stage s (the shuffle syncs the warp): refill it
         const int pg = __shfl_sync(0xffffffffu, my_page, (i + PV_ST) & 31);
@@ -667,24 +718,47 @@ __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const Dec
         if (i == 0) prefetch_next(a, nx);
     }
     pc += np;
-    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
-    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
-    const bool vrow = gid < G;
-    if (it.part < 0) {
-        if (vrow) {
-            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-            bf16* op = a.out + (static_cast<size_t>(a.dec_tok0 + it.row) * a.H + it.kvh * G + gid) * HD + 2 * tig;
+    item_stamp(a, item, 2);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) *reinterpret_cast<uint32_t*>(op + j * 8) = pack2(o[j][0] * inv, o[j][1] * inv);
+    for (int off = 4; off < 32; off <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+    }
+    const int h0 = 2 * tig, h1 = h0 + 1;
+    if (it.part < 0) {
+        const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+        bf16* op = a.out + (static_cast<size_t>(a.dec_tok0 + it.row) * a.H + it.kvh * G) * HD + gid;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (h0 < G) {
+                op[h0 * HD + j * 16] = __float2bfloat16_rn(o[j][0] * i0);
+                op[h0 * HD + j * 16 + 8] = __float2bfloat16_rn(o[j][2] * i0);
+            }
+            if (h1 < G) {
+                op[h1 * HD + j * 16] = __float2bfloat16_rn(o[j][1] * i1);
+                op[h1 * HD + j * 16 + 8] = __float2bfloat16_rn(o[j][3] * i1);
+            }
         }
         return;
     }
-    if (vrow) {
-        const size_t pi = (static_cast<size_t>(it.row) * a.H + it.kvh * G + gid) * a.max_parts + it.part;
-        float* po = a.part_o + pi * HD + 2 * tig;
+    const size_t pi0 = (static_cast<size_t>(it.row) * a.H + it.kvh * G + h0) * a.max_parts + it.part;
+    const size_t pi1 = pi0 + a.max_parts;
+    float* po0 = a.part_o + pi0 * HD + gid;
+    float* po1 = a.part_o + pi1 * HD + gid;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) *reinterpret_cast<float2*>(po + j * 8) = make_float2(o[j][0], o[j][1]);
-        if (tig == 0) a.part_ml[pi] = make_float2(m_run, l_run);
+    for (int j = 0; j < 8; ++j) {
+        if (h0 < G) {
+            po0[j * 16] = o[j][0];
+            po0[j * 16 + 8] = o[j][2];
+        }
+        if (h1 < G) {
+            po1[j * 16] = o[j][1];
+            po1[j * 16 + 8] = o[j][3];
+        }
+    }
+    if (gid == 0) {
+        if (h0 < G) a.part_ml[pi0] = make_float2(m0, l0);
+        if (h1 < G) a.part_ml[pi1] = make_float2(m1, l1);
     }
 }
 
@@ -821,8 +895,9 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
     while (nx.idx < a.n_pv) {
         const PvItem it = nx.it;
         const int my_page = nx.page;
+        const int cur = __shfl_sync(0xffffffffu, nx.idx, 0);
         nx.idx = lane == 0 ? atomicAdd(a.pv_next, 1) : 0;  // claim the next item now; used after page 0
-        private_item<G>(tm_kv, a, it, my_page, ring, full, pc, nx, pre);
+        private_item<G>(tm_kv, a, it, my_page, ring, full, pc, nx, pre, cur);
         pre = 0;
     }
     if (warp == 0) stamp(a, blockIdx.x, 12);
@@ -941,9 +1016,7 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
         const int k0 = (g.shared_pages > 0 && g.members > 1) ? g.shared_pages * PG : 0;
         for (int m = 0; m < g.members; ++m) priv_keys += rows[static_cast<size_t>(g.row0 + m)].pos + 1 - k0;
     }
-    int kp_base = static_cast<int>(priv_keys * Hkv / (8.0 * num_sms));
-    kp_base = std::max(64, std::min(512, (kp_base + PG - 1) / PG * PG));
-    if (std::getenv("HK_ATTN_PRIV_KEYS")) kp_base = std::atoi(std::getenv("HK_ATTN_PRIV_KEYS"));
+    static const int env_priv_keys = std::getenv("HK_ATTN_PRIV_KEYS") ? std::atoi(std::getenv("HK_ATTN_PRIV_KEYS")) : 0;
     // Shared split count S (measured on B200, tools/attn_bench.py, profiles/
     // r1_attention.txt): shared CTAs should cover ~64 SMs when the rows also
     // carry >= 4 private pages each (the private queue then keeps the other SMs
@@ -964,6 +1037,17 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
         static const int env_splits = std::getenv("HK_ATTN_SPLITS") ? std::atoi(std::getenv("HK_ATTN_SPLITS")) : 0;
         if (env_splits > 0) best_s = env_splits;
     }
+    // Private split: each (row, kv head) is cut into npv items so that all
+    // items run as ONE round on the warps that are free while the shared tiles
+    // stream (an item pays one HBM latency before its first page; a second
+    // round of short items doubles that, measured with tools/attn_items.py).
+    double priv_pages = 0;
+    for (const auto& g : groups) {
+        const int k0 = (g.shared_pages > 0 && g.members > 1) ? g.shared_pages * PG : 0;
+        for (int m = 0; m < g.members; ++m) priv_pages += (rows[static_cast<size_t>(g.row0 + m)].pos + 1 - k0 + PG - 1) / PG;
+    }
+    const int sh_ctas = tiles * best_s;
+    const double q_warps = 8.0 * (sh_ctas < num_sms ? num_sms - sh_ctas : num_sms);
     for (const auto& g : groups) {
         const bool shared = g.shared_pages > 0 && g.members > 1;
         const int shared_pages = shared ? g.shared_pages : 0;
@@ -1004,8 +1088,13 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
             const int first = splits;  // the shared items contribute partials 0 .. splits - 1
             // keep a row's partials within one 8-part merge batch when possible
             const int part_cap = first < 8 ? 8 - first : max_parts - first;
-            int kp = std::max(kp_base, (k1 - k0 + part_cap - 1) / part_cap);
-            kp = (kp + PG - 1) / PG * PG;
+            const int row_pages = (k1 - k0 + PG - 1) / PG;
+            int npv0 = static_cast<int>(row_pages * q_warps / (Hkv * std::max(1.0, priv_pages)));
+            npv0 = std::max(1, std::min(npv0, std::max(1, part_cap)));
+            npv0 = std::max(npv0, (row_pages + 31) / 32);  // <= 32 pages (one page id per lane)
+            int kp = (row_pages + npv0 - 1) / npv0 * PG;
+            if (env_priv_keys > 0)
+                kp = std::max((env_priv_keys + PG - 1) / PG * PG, (row_pages + std::max(1, part_cap) - 1) / std::max(1, part_cap) * PG);
             if (kp > 32 * PG) throw std::runtime_error("decode_attention: private range too long for max_parts");
             const int npv = (k1 - k0 + kp - 1) / kp;
             const int parts = first + npv;

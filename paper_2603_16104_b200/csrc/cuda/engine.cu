@@ -707,6 +707,14 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     const float eps = mc.rms_eps;
     const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
     // the step's kernel sequence (eager, or recorded once into a CUDA graph)
+    // timing experiments only (HK_DEBUG_DOUBLE=qkv,rope,attn,o,rms,gu,down): launch a kernel
+    // family twice per layer to measure its marginal cost inside the real PDL/graph pipeline
+    static const std::string dbl_env = std::getenv("HK_DEBUG_DOUBLE") ? std::getenv("HK_DEBUG_DOUBLE") : "";
+    auto dbl = [&](const char* fam) { return !dbl_env.empty() && dbl_env.find(fam) != std::string::npos && !dec.empty(); };
+    // HK_DEBUG_SKIP=rope,attn: drop a kernel family (wrong tokens; decode lengths are fixed, so the
+    // schedule is unchanged) to measure what a perfect fusion of it could save
+    static const std::string skip_env = std::getenv("HK_DEBUG_SKIP") ? std::getenv("HK_DEBUG_SKIP") : "";
+    auto skip = [&](const char* fam) { return !skip_env.empty() && skip_env.find(fam) != std::string::npos && !dec.empty(); };
     auto enqueue = [&]() {
     int ck = clock.begin(5, st);
     hkd::embed(embed, f32, d, d_ids, d_slots, wk.slot_last, T, x, st);
@@ -729,12 +737,27 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     };
     for (int l = 0; l < L; ++l) {
         const LayerW& lw = layers[static_cast<size_t>(l)];
-        int sp = gemm(lw.wqkv, h, QKV, d, T, hkd::kEpiPartial, pbuf, QKV);
-        hkd::QkvArgs qa{pbuf, sp, lw.bqkv,
-                        hkd::RopeArgs{qkv, f32, T, H, Hkv, hd, d_pos, d_kvw, d_ptab, d_pages, rope, kv_layer(w, l), block}};
-        ck = clock.begin(5, st);
-        hkd::qkv_rope_kv(qa, st);
-        clock.end(ck, st);
+        const hkd::RopeArgs ra{qkv, f32, T, H, Hkv, hd, d_pos, d_kvw, d_ptab, d_pages, rope, kv_layer(w, l), block};
+        // bf16: one kernel (cluster split-K + bias/RoPE/KV-write epilogue); fp32 or
+        // unsupported shapes: split-K partials + the qkv_rope_kv consumer
+        int fused = -1;
+        if (!f32) {
+            ck = clock.begin(0, st);
+            if (dbl("qkv")) hkd::gemm_bf16_qkv_rope(static_cast<const bf16*>(lw.wqkv), static_cast<const bf16*>(h), QKV, d,
+                                                    static_cast<const bf16*>(lw.bqkv), ra, st);
+            fused = hkd::gemm_bf16_qkv_rope(static_cast<const bf16*>(lw.wqkv), static_cast<const bf16*>(h), QKV, d,
+                                            static_cast<const bf16*>(lw.bqkv), ra, st);
+            clock.end(ck, st, static_cast<double>(QKV) * d * esz + static_cast<double>(T) * d * esz);
+        }
+        if (fused < 0) {
+            if (dbl("qkv")) gemm(lw.wqkv, h, QKV, d, T, hkd::kEpiPartial, pbuf, QKV);
+            const int sp = gemm(lw.wqkv, h, QKV, d, T, hkd::kEpiPartial, pbuf, QKV);
+            const hkd::QkvArgs qa{pbuf, sp, lw.bqkv, ra};
+            ck = clock.begin(5, st);
+            if (dbl("rope")) hkd::qkv_rope_kv(qa, st);
+            if (!skip("rope")) hkd::qkv_rope_kv(qa, st);
+            clock.end(ck, st);
+        }
         hkd::AttnArgs aa{qkv, f32, H, Hkv, hd, block, d_pos, d_pages, kv_layer(w, l), d_items,
                          n_multi, attn, part_o, part_ml, max_parts, T_pre, scale, 0};
         if (f32) {
@@ -771,12 +794,15 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
                                        static_cast<size_t>(d) * H * hd * esz};
                 // one launch: decode tiles + private queue + prefill tiles
                 ck = clock.begin(dec.empty() ? 3 : 1, st);
-                hkd::decode_attention(da, wk.tm_kv, st);
+                if (dbl("attn")) hkd::decode_attention(da, wk.tm_kv, st);
+                if (!skip("attn")) hkd::decode_attention(da, wk.tm_kv, st);
                 clock.end(ck, st, dplan.shared_bytes + dplan.private_bytes + prefill_bytes, 1);
             }
         }
-        sp = gemm(lw.wo, attn, d, H * hd, T, hkd::kEpiPartial, pbuf, d);
+        if (dbl("o")) gemm(lw.wo, attn, d, H * hd, T, hkd::kEpiPartial, pbuf, d);
+        int sp = gemm(lw.wo, attn, d, H * hd, T, hkd::kEpiPartial, pbuf, d);
         ck = clock.begin(5, st);
+        if (dbl("rms")) hkd::add_rmsnorm(pbuf, 0, x, lw.mlp_norm, f32, T, d, eps, h, nullptr, nullptr, st);
         hkd::add_rmsnorm(pbuf, sp, x, lw.mlp_norm, f32, T, d, eps, h, nullptr, nullptr, st);
         clock.end(ck, st);
         if (f32) {
@@ -785,8 +811,10 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
             hkd::swiglu_interleaved(static_cast<const float*>(gu), T, F, static_cast<float*>(act), st);
             clock.end(ck, st);
         } else {
+            if (dbl("gu")) gemm(lw.wgu, h, 2 * F, d, T, hkd::kEpiSwiGLU, act, F);
             gemm(lw.wgu, h, 2 * F, d, T, hkd::kEpiSwiGLU, act, F);  // SwiGLU fused in the epilogue
         }
+        if (dbl("down")) gemm(lw.wd, act, d, F, T, hkd::kEpiPartial, pbuf, d);
         sp = gemm(lw.wd, act, d, F, T, hkd::kEpiPartial, pbuf, d);
         const bool last = l + 1 == L;
         ck = clock.begin(5, st);

@@ -39,7 +39,77 @@ struct GemmParams {
     float* partial;
     int cluster;  // 1: the grid.z split-K CTAs form a cluster and reduce through DSMEM
     int skip_epi; // timing experiments only (HK_GEMM_DEBUG_SKIP_EPI): no output stores
+    RopeArgs rope; // kEpiQkvRope: the q/k/v rows and this layer's KV pages
 };
+
+// kEpiQkvRope (cluster split-K only): the tile is one 128-row head of the
+// fused QKV projection (BM == head_dim). Rank r of the s-CTA cluster owns
+// rotation pairs (i, i + 64), i in [r*ceil(64/s), ...), for all BN tokens: it
+// sums the s peers' fp32 tiles through DSMEM in rank (= split) order, adds the
+// bias, rounds to bf16, rotates q/k heads (RoPE on the stored bf16 values, as
+// qkv_rope_kv_kernel and the oracle do) and writes the q/k/v row plus, for
+// k/v heads of tokens with kvw set, the token's slot of its KV page. Replaces
+// the partial round trip through L2 and the separate qkv_rope_kv launch.
+template <int BN>
+__device__ __forceinline__ void qkv_rope_epilogue(const GemmParams& p, const float* tile, cg::cluster_group& cl, int s,
+                                                  int rank, int n0) {
+    constexpr int kHalf = BM / 2;
+    const RopeArgs& r = p.rope;
+    const int hh = static_cast<int>(blockIdx.x);
+    const bool is_v = hh >= r.H + r.Hkv;
+    const int per = (kHalf + s - 1) / s;
+    const int i0 = min(kHalf, rank * per), i1 = min(kHalf, i0 + per);
+    const int ni = i1 - i0;
+    if (ni <= 0) return;
+    const float* peer[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) peer[q] = cl.map_shared_rank(tile, q < s ? q : 0);
+    bf16* qkv = static_cast<bf16*>(r.qkv);
+    bf16* kv = static_cast<bf16*>(r.kv_layer);
+    const int c0 = hh * BM;
+    for (int idx = threadIdx.x; idx < ni * BN; idx += blockDim.x) {
+        const int i = i0 + idx % ni, c = idx / ni;
+        const int n = n0 + c;
+        if (n >= p.T) continue;
+        float v0[8], v1[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < s) {
+                v0[q] = peer[q][c * BM + i];
+                v1[q] = peer[q][c * BM + i + kHalf];
+            }
+        float x0 = 0.f, x1 = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < s) {  // fixed split order: deterministic
+                x0 += v0[q];
+                x1 += v1[q];
+            }
+        if (p.bias) {
+            x0 += bf2f(p.bias[c0 + i]);
+            x1 += bf2f(p.bias[c0 + i + kHalf]);
+        }
+        bf16 b0 = f2bf(x0), b1 = f2bf(x1);
+        const int pos = r.pos[n];
+        if (!is_v) {
+            const float y0 = bf2f(b0), y1 = bf2f(b1);
+            const float2 cs = r.rope[static_cast<size_t>(pos) * kHalf + i];
+            b0 = f2bf(y0 * cs.x - y1 * cs.y);
+            b1 = f2bf(y1 * cs.x + y0 * cs.y);
+        }
+        bf16* row = qkv + static_cast<size_t>(n) * p.N + c0;
+        row[i] = b0;
+        row[i + kHalf] = b1;
+        if (hh >= r.H && r.kvw[n]) {
+            const int page = r.pages[r.ptab[n] + pos / r.block];
+            const int kvh = is_v ? hh - r.H - r.Hkv : hh - r.H;
+            bf16* dst = kv + ((static_cast<size_t>(page) * 2 + (is_v ? 1 : 0)) * r.Hkv + kvh) * r.block * BM +
+                        static_cast<size_t>(pos % r.block) * BM;
+            dst[i] = b0;
+            dst[i + kHalf] = b1;
+        }
+    }
+}
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(128, 1)
@@ -152,9 +222,10 @@ __global__ void __launch_bounds__(128, 1)
         const int nq = (r1 - r0) / 4;                  // float4 row groups
         const float4* peer[8];
         cg::cluster_group cl = cg::this_cluster();
+        if (p.epi == kEpiQkvRope) qkv_rope_epilogue<BN>(p, tile, cl, s, rank, n0);
 #pragma unroll
         for (int q = 0; q < 8; ++q) peer[q] = reinterpret_cast<const float4*>(cl.map_shared_rank(tile, q < s ? q : 0));
-        for (int idx = threadIdx.x; idx < nq * BN; idx += blockDim.x) {
+        for (int idx = threadIdx.x; p.epi != kEpiQkvRope && idx < nq * BN; idx += blockDim.x) {
             const int rr = r0 + 4 * (idx % nq), c = idx / nq;
             const int off4 = (c * BM + rr) / 4;
             float4 v[8];
@@ -529,6 +600,38 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
         const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 4096));
         splitk_reduce_kernel<<<blocks, 256, 0, st>>>(workspace, splits, T, N, epi, out, ldo, bias);
         HK_LAUNCHED(1);
+    }
+    return splits;
+}
+
+int gemm_bf16_qkv_rope(const bf16* W, const bf16* X, int N, int K, const bf16* bias, const RopeArgs& r,
+                       cudaStream_t st) {
+    const int T = r.T;
+    if (T <= 0) return 0;
+    if (r.f32 || r.hd != BM || N != (r.H + 2 * r.Hkv) * BM || K % BK != 0) return -1;
+    // opt-in (HK_QKV_FUSED=1): measured slower in the decode pipeline on B200 than
+    // L2 partials + qkv_rope_kv (c2 bench 1163 vs 1083 ms/run): the 6-CTA
+    // clusters schedule worse than independent split-K CTAs (profiles/r1_marginal_costs.txt)
+    static const bool on = std::getenv("HK_QKV_FUSED") != nullptr;
+    if (!on) return -1;
+    const int BN = T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256;
+    const int mt = N / BM, nt = (T + BN - 1) / BN, kb = K / BK;
+    int splits = 1;
+    const int slots = BN <= 64 ? 2 * g_num_sms : g_num_sms;
+    if (mt * nt * 2 <= slots) splits = std::min(8, slots / (mt * nt));
+    splits = std::min(splits, std::max(1, kb / 4));
+    const int kbps = (kb + splits - 1) / splits;
+    splits = (kb + kbps - 1) / kbps;
+    GemmParams p{N, K, T, kb, kbps, kEpiQkvRope, nullptr, N, bias, nullptr, 1, 0, r};
+    const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
+    const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
+    dim3 grid(mt, nt, splits);
+    switch (BN) {
+        case 16: launch_tc<16, 4>(tw, tx, p, grid, st); break;
+        case 32: launch_tc<32, 4>(tw, tx, p, grid, st); break;
+        case 64: launch_tc<64, 4>(tw, tx, p, grid, st); break;
+        case 128: launch_tc<128, 4>(tw, tx, p, grid, st); break;
+        default: launch_tc<256, 4>(tw, tx, p, grid, st); break;
     }
     return splits;
 }

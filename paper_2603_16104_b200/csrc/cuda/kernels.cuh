@@ -14,7 +14,8 @@ namespace hkd {
 // kEpiSwiGLU expects W rows interleaved per 128-row tile as [64 gate | 64 up]
 // and writes silu(gate) * up as bf16 [T][N/2]; kEpiArgmax writes per-(tile,
 // token) (max, argmax) pairs [N/128][T] for argmax_reduce.
-enum : int { kEpiStoreBf16 = 0, kEpiAddF32 = 1, kEpiStoreF32 = 2, kEpiPartial = 3, kEpiSwiGLU = 4, kEpiArgmax = 5 };
+enum : int { kEpiStoreBf16 = 0, kEpiAddF32 = 1, kEpiStoreF32 = 2, kEpiPartial = 3, kEpiSwiGLU = 4, kEpiArgmax = 5,
+       kEpiQkvRope = 6 };
 extern int g_num_sms;
 extern unsigned long long g_launches;  // kernels launched by this library (all launchers count)
 
@@ -63,6 +64,13 @@ struct RopeArgs {
     int block;
 };
 void rope_kv_write(const RopeArgs& a, cudaStream_t st);
+// Fused QKV projection (bf16, head_dim 128): split-K CTAs of a cluster reduce
+// through DSMEM and apply bias + RoPE + the K/V page write in the epilogue
+// (the result of gemm_bf16 kEpiPartial followed by qkv_rope_kv, one kernel).
+// Returns the split count, or -1 when the shape is not supported (caller
+// falls back to the two-kernel path).
+int gemm_bf16_qkv_rope(const bf16* W, const bf16* X, int N, int K, const bf16* bias, const RopeArgs& r,
+                       cudaStream_t st);
 void swiglu(const void* gu, bool f32, int T, int F, void* out, cudaStream_t st);
 // gate/up weights are stored with rows interleaved per 128-row tile ([64 gate | 64 up]);
 // init maps the physical index back to the logical (gate | up) index of the oracle.
