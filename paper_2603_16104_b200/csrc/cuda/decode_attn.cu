@@ -49,86 +49,12 @@ constexpr int KC = 128;       // keys per tcgen05 chunk (8 pages)
 constexpr int ROWS = 128;     // MMA rows of a shared item
 
 // -------------------------------------------------------------------- merge
-// Merge of (decode row, head) partials: an 8-lane group per pair, lane owns
-// 16 dims; a warp merges 4 pairs at once. All part loads of a lane are
-// independent, so a merge costs about two L2 round trips.
-__device__ __forceinline__ void merge_group(const DecodeAttnArgs& a, int row, int head, bool active, int sub) {
-    const unsigned full = 0xffffffffu;
-    const int np = active ? a.n_parts[row] : 0;
-    const size_t base = (static_cast<size_t>(active ? row : 0) * a.H + head) * a.max_parts;
-    float2 ml[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int k = sub + 8 * j;
-        ml[j] = k < np ? __ldcg(&a.part_ml[base + k]) : make_float2(-INFINITY, 0.f);
-    }
-    float M = fmaxf(fmaxf(ml[0].x, ml[1].x), fmaxf(ml[2].x, ml[3].x));
-    M = fmaxf(M, __shfl_xor_sync(full, M, 1));
-    M = fmaxf(M, __shfl_xor_sync(full, M, 2));
-    M = fmaxf(M, __shfl_xor_sync(full, M, 4));
-    float w[4], L = 0.f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        w[j] = sub + 8 * j < np ? exp2f(ml[j].x - M) : 0.f;
-        L += w[j] * ml[j].y;
-    }
-    L += __shfl_xor_sync(full, L, 1);
-    L += __shfl_xor_sync(full, L, 2);
-    L += __shfl_xor_sync(full, L, 4);
-    float acc[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
-    const int lane = threadIdx.x & 31;
-    const int g0 = lane & ~7;
-    // 4 parts per round trip: all 16 loads issued before any use
-    for (int k0 = 0; k0 < 32; k0 += 4) {
-        if (!__any_sync(full, k0 < np)) break;
-        const float wsel = k0 < 8 ? w[0] : (k0 < 16 ? w[1] : (k0 < 24 ? w[2] : w[3]));
-        float4 v[4][4];
-        float wk[4];
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-            const int k = k0 + kk;
-            wk[kk] = __shfl_sync(full, wsel, g0 + (k & 7));
-            const float4* src = reinterpret_cast<const float4*>(a.part_o + (base + (k < np ? k : 0)) * HD + sub * 16);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) v[kk][e] = __ldcg(src + e);
-            if (k >= np) wk[kk] = 0.f;
-        }
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                acc[4 * e] += wk[kk] * v[kk][e].x;
-                acc[4 * e + 1] += wk[kk] * v[kk][e].y;
-                acc[4 * e + 2] += wk[kk] * v[kk][e].z;
-                acc[4 * e + 3] += wk[kk] * v[kk][e].w;
-            }
-    }
-    if (!active) return;
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    bf16* o = a.out + (static_cast<size_t>(a.dec_tok0 + row) * a.H + head) * HD + sub * 16;
-    uint4 w0, w1;
-    __nv_bfloat162 t[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) t[e] = __floats2bfloat162_rn(acc[2 * e] * inv, acc[2 * e + 1] * inv);
-    w0 = *reinterpret_cast<uint4*>(&t[0]);
-    w1 = *reinterpret_cast<uint4*>(&t[4]);
-    reinterpret_cast<uint4*>(o)[0] = w0;
-    reinterpret_cast<uint4*>(o)[1] = w1;
-}
+// Partials are stored NORMALISED in bf16 (o_p / l_p, half the bytes of fp32
+// unnormalised rows; the writes were the slowest step of a shared tile) with
+// (m_p, l_p) in fp32 (m in the log2 domain); merge: out = sum_p w_p o_p / sum_p
+// w_p with w_p = l_p 2^(m_p - max m).
 
-// Merge the n (row, head) pairs pair(i) = (row_i, head_i), i < n, with one warp.
-template <typename PairFn>
-__device__ __forceinline__ void merge_pairs(const DecodeAttnArgs& a, int n, PairFn pair) {
-    const int lane = threadIdx.x & 31, grp = lane >> 3, sub = lane & 7;
-    for (int i0 = 0; i0 < n; i0 += 4) {
-        const int i = i0 + grp;
-        int row = 0, head = 0;
-        if (i < n) pair(i, row, head);
-        merge_group(a, row, head, i < n, sub);
-    }
-}
+__device__ __forceinline__ bf16* part_bf16(const DecodeAttnArgs& a) { return reinterpret_cast<bf16*>(a.part_o); }
 
 // Arrival on a (row, kv head) counter: release orders this thread's partial
 // stores (after a warp/CTA barrier, those of its peers too, by cumulativity)
@@ -403,13 +329,11 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
             mbar_wait(&s_full[b], (c >> 1) & 1);
             tc_fence_after();
             if (c == 0) stamp(a, blockIdx.x, 7);
-            if (c == 1) stamp(a, blockIdx.x, 9);
             // raw scores (the softmax scale is folded into the exp2 argument)
             float s[64];
             {
                 // one 64-column load (columns past nk hold stale bits: masked)
                 tmem_ld64(t_lane + b * 128 + half * 64, s);
-                if (c == 1) stamp(a, blockIdx.x, 6);
                 const int col0 = half * 64;
                 const int key0 = (it.page0 + c * 8) * PG + col0;
                 if (causal || col0 + 64 > nk) {  // (warp-uniform) full decode chunks need no mask
@@ -418,10 +342,8 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                         if (!(col0 + e < nk && key0 + e <= prow)) s[e] = -INFINITY;
                 }
             }
-            if (c == 1) stamp(a, blockIdx.x, 11);
             tc_fence_before();
             mbar_arrive(&s_free[b]);  // this thread is done with S buffer b
-            if (c == 1) stamp(a, blockIdx.x, 10);
             float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
             for (int j = 0; j < 64; ++j) mx4[j & 3] = fmaxf(mx4[j & 3], s[j]);
@@ -481,42 +403,44 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
         mbar_wait(o_done, (nch - 1) & 1);
         tc_fence_after();
         stamp(a, blockIdx.x, 3);
-        if (half == 0) red_m[row] = m_run;
-        // ---- partial rows, staged through smem (the K/V stages are free) so that
-        // each warp stores whole 512-byte rows (coalesced)
-        constexpr int SO = HD + 4;  // padded fp32 row stride: conflict-free float4 stores
-        float* sO = reinterpret_cast<float*>(sKV);
+        stamp(a, blockIdx.x, 9);
+        // ---- output rows: normalised bf16 (final rows of a causal tile, else
+        // partials), staged row-major in smem (the K/V stages are free) and
+        // written by bulk copies, 256 B per (token, head) row
         red_l[half * ROWS + row] = l_half;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            float v[32];
-            tmem_ld32(t_lane + 256 + half * 64 + j * 32, v);
-            float4* dst = reinterpret_cast<float4*>(sO + row * SO + half * 64 + j * 32);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
-        }
+        float v[64];
+        tmem_ld64(t_lane + 256 + half * 64, v);
         named_bar(1, 256);
-        if (causal) {
-            // the item covers every key of its rows: normalised bf16 output, one
-            // 256-byte row per (token, head) per warp instruction
-            for (int r = warp; r < nrows; r += 8) {
-                const float L = red_l[r] + red_l[ROWS + r];
-                const float inv = L > 0.f ? 1.f / L : 0.f;
-                const float4 v = reinterpret_cast<const float4*>(sO + r * SO)[lane];
-                bf16* o = a.out + (static_cast<size_t>(tok_base + r / G) * a.H + it.kvh * G + r % G) * HD + lane * 4;
-                uint2 pk;
-                pk.x = pack2(v.x * inv, v.y * inv);
-                pk.y = pack2(v.z * inv, v.w * inv);
-                *reinterpret_cast<uint2*>(o) = pk;
-            }
-        } else {
-            for (int r = warp; r < nrows; r += 8) {
-                const size_t pi =
-                    (static_cast<size_t>(it.row0 + r / G) * a.H + it.kvh * G + r % G) * a.max_parts + it.rank;
-                reinterpret_cast<float4*>(a.part_o + pi * HD)[lane] = reinterpret_cast<const float4*>(sO + r * SO)[lane];
-                if (lane == 0) a.part_ml[pi] = make_float2(red_m[r], red_l[r] + red_l[ROWS + r]);
-            }
+        stamp(a, blockIdx.x, 10);
+        const float L = red_l[row] + red_l[ROWS + row];
+        const float inv = L > 0.f ? __frcp_rn(L) : 0.f;
+        constexpr int RS = HD * 2 + 16;  // padded staging row (bytes): conflict-free 16-byte stores
+        uint8_t* stage = sKV;
+        {
+            uint4* dst = reinterpret_cast<uint4*>(stage + row * RS + half * 128);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                dst[e] = make_uint4(pack2(v[8 * e] * inv, v[8 * e + 1] * inv), pack2(v[8 * e + 2] * inv, v[8 * e + 3] * inv),
+                                    pack2(v[8 * e + 4] * inv, v[8 * e + 5] * inv), pack2(v[8 * e + 6] * inv, v[8 * e + 7] * inv));
         }
+        auto row_pi = [&](int r) {
+            return (static_cast<size_t>(it.row0 + r / G) * a.H + it.kvh * G + r % G) * a.max_parts + it.rank;
+        };
+        if (!causal && half == 0 && row < nrows) a.part_ml[row_pi(row)] = make_float2(m_run, L);
+        fence_proxy_async();
+        named_bar(1, 256);
+        stamp(a, blockIdx.x, 11);
+        if (lane < 16) {
+            const int r = warp * 16 + lane;
+            if (r < nrows) {
+                bf16* dst = causal ? a.out + (static_cast<size_t>(tok_base + r / G) * a.H + it.kvh * G + r % G) * HD
+                                   : part_bf16(a) + row_pi(r) * HD;
+                bulk_s2g(dst, stage + r * RS, HD * 2);
+            }
+            bulk_commit_wait_read();  // staging reusable; completion is awaited before the grid barrier
+        }
+        __syncwarp();
+        stamp(a, blockIdx.x, 6);
         stamp(a, blockIdx.x, 4);
         stamp(a, blockIdx.x, 5);
     }
@@ -726,7 +650,7 @@ __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const Dec
     }
     const int h0 = 2 * tig, h1 = h0 + 1;
     if (it.part < 0) {
-        const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+        const float i0 = l0 > 0.f ? __frcp_rn(l0) : 0.f, i1 = l1 > 0.f ? __frcp_rn(l1) : 0.f;
         bf16* op = a.out + (static_cast<size_t>(a.dec_tok0 + it.row) * a.H + it.kvh * G) * HD + gid;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -743,17 +667,18 @@ __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const Dec
     }
     const size_t pi0 = (static_cast<size_t>(it.row) * a.H + it.kvh * G + h0) * a.max_parts + it.part;
     const size_t pi1 = pi0 + a.max_parts;
-    float* po0 = a.part_o + pi0 * HD + gid;
-    float* po1 = a.part_o + pi1 * HD + gid;
+    bf16* po0 = part_bf16(a) + pi0 * HD + gid;
+    bf16* po1 = part_bf16(a) + pi1 * HD + gid;
+    const float i0 = l0 > 0.f ? __frcp_rn(l0) : 0.f, i1 = l1 > 0.f ? __frcp_rn(l1) : 0.f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         if (h0 < G) {
-            po0[j * 16] = o[j][0];
-            po0[j * 16 + 8] = o[j][2];
+            po0[j * 16] = __float2bfloat16_rn(o[j][0] * i0);
+            po0[j * 16 + 8] = __float2bfloat16_rn(o[j][2] * i0);
         }
         if (h1 < G) {
-            po1[j * 16] = o[j][1];
-            po1[j * 16 + 8] = o[j][3];
+            po1[j * 16] = __float2bfloat16_rn(o[j][1] * i1);
+            po1[j * 16 + 8] = __float2bfloat16_rn(o[j][3] * i1);
         }
     }
     if (gid == 0) {
@@ -779,21 +704,18 @@ __device__ __forceinline__ void merge16(const DecodeAttnArgs& a, int pair, int n
     for (int k0 = 0; k0 < a.max_parts; k0 += 8) {
         if (!__any_sync(full, k0 < np)) break;
         const float2 ml = sub < 8 ? __ldcg(&a.part_ml[base + k0 + sub]) : make_float2(-INFINITY, 0.f);
-        float4 v[8][2];
+        uint4 v[8];  // 8 bf16 dims of each of the batch's parts
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float4* src = reinterpret_cast<const float4*>(a.part_o + (base + k0 + k) * HD) + sub * 2;
-            v[k][0] = __ldcg(src);
-            v[k][1] = __ldcg(src + 1);
-        }
+        for (int k = 0; k < 8; ++k)
+            v[k] = __ldcg(reinterpret_cast<const uint4*>(part_bf16(a) + (base + k0 + k) * HD) + sub);
         const bool mine = sub < 8 && k0 + sub < np;
         float mx = mine ? ml.x : -INFINITY;
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(full, mx, o));
         const float Mn = fmaxf(M, mx);
         const float sc = M == -INFINITY ? 0.f : exp2f(M - Mn);  // rescale the previous batches
-        const float w = mine ? exp2f(ml.x - Mn) : 0.f;
-        float lw = mine ? w * ml.y : 0.f;
+        const float w = mine ? exp2f(ml.x - Mn) * ml.y : 0.f;  // l_p 2^(m_p - M)
+        float lw = w;
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) lw += __shfl_xor_sync(full, lw, o);
         L = L * sc + lw;
@@ -804,20 +726,18 @@ __device__ __forceinline__ void merge16(const DecodeAttnArgs& a, int pair, int n
         for (int k = 0; k < 8; ++k) {
             const float wk = __shfl_sync(full, w, g0 + k);
             if (k0 + k < np) {
-                acc[0] += wk * v[k][0].x;
-                acc[1] += wk * v[k][0].y;
-                acc[2] += wk * v[k][0].z;
-                acc[3] += wk * v[k][0].w;
-                acc[4] += wk * v[k][1].x;
-                acc[5] += wk * v[k][1].y;
-                acc[6] += wk * v[k][1].z;
-                acc[7] += wk * v[k][1].w;
+                const uint32_t u[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    acc[2 * e] += wk * __uint_as_float(u[e] << 16);
+                    acc[2 * e + 1] += wk * __uint_as_float(u[e] & 0xffff0000u);
+                }
             }
         }
         M = Mn;
     }
     if (!active || np <= 1) return;
-    const float inv = L > 0.f ? 1.f / L : 0.f;
+    const float inv = L > 0.f ? __frcp_rn(L) : 0.f;
     uint4 w4;
     w4.x = pack2(acc[0] * inv, acc[1] * inv);
     w4.y = pack2(acc[2] * inv, acc[3] * inv);
@@ -901,6 +821,7 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
         pre = 0;
     }
     if (warp == 0) stamp(a, blockIdx.x, 12);
+    bulk_wait_all();  // a shared tile's bulk-copied output rows are written (before the grid barrier / exit)
     if (!a.merge_in_kernel) {
         // the last warp out rewinds the queue for the next launch
         if (lane == 0 && atomicAdd(a.pv_done, 1) == static_cast<int>(gridDim.x) * DA_PV_WARPS - 1) {

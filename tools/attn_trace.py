@@ -54,7 +54,7 @@ print(f"  queue loop ends: shared CTAs {us(sh[:,12]).min():.1f}..{us(sh[:,12]).m
 mhz = (sh[:, 15] - sh[:, 14]) / (sh[:, 5] - sh[:, 0]) * 1e3
 print(f"  SM clock inside shared CTAs: {mhz.mean():.0f} MHz; shared phase ends {us(sh[:,5]).min():.1f}..{us(sh[:,5]).max():.1f} us")
 # chunk 1 of the softmax warps (thread 0): S1 ready (9) -> row max exchanged (10) -> exps packed (11) -> PV(0) done (6)
-c1 = [(9, "S1 ready"), (6, "after ld"), (11, "masked"), (10, "arrived")]
+c1 = [(9, "O done"), (10, "l exchanged"), (11, "staged"), (6, "bulk stored")]
 for (i0, n0), (i1, n1) in zip(c1, c1[1:]):
     d = sh[:, i1] - sh[:, i0]
     print(f"  c1 {n0:>14s} -> {n1:<14s} mean {d.mean():8.0f} cycles  max {d.max():8.0f}")
