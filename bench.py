@@ -276,6 +276,9 @@ def main():
         s = decode_step_sample()
         line["cpu_baseline"] = {"value": s["tokens_per_s"], "unit": UNIT, "cores": s["cores"], "kind": "port",
                                 "sample": s["sample"]}
+    if os.environ.get("HK_GEMM_TRACE"):  # debug: in-pipeline GEMM spans (tools/gemm_trace.py)
+        from paper_2603_16104_b200 import _lib
+        _lib.load().hkx_gemm_trace_dump(os.environ.get("HK_GEMM_TRACE_OUT", "gpurun_out/gemm_trace.csv").encode())
     eng.close()
     print(json.dumps(line))
     if ws > 1:

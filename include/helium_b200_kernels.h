@@ -48,6 +48,8 @@ int hkx_prefill_attention(const void* qkv, const void* kv, int n_pages, int n_to
  * hkx_decode_attention calls into device_buf ([shared CTAs + private CTAs][8] u64);
  * NULL turns it off. */
 int hkx_decode_attention_trace(void* device_buf);
+/* debug: dump the HK_GEMM_TRACE per-launch spans (first CTA start, wait exit, last end) as CSV */
+int hkx_gemm_trace_dump(const char* path);
 /* Algorithmic bytes of that call: shared KV once per group + private KV + q and o. */
 double hkx_decode_attention_bytes(int n_rows, int H, int Hkv, const int32_t* offs, const int32_t* pos,
                                   const int32_t* group_rows, const int32_t* group_shared_pages, int n_groups);

@@ -105,6 +105,7 @@ _SIGS = {
     "hkx_decode_attention": (C.c_double, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, i32p, i32p, i32p,
                                           i32p, i32p, C.c_int, C.c_void_p, C.c_int]),
     "hkx_decode_attention_trace": (C.c_int, [C.c_void_p]),
+    "hkx_gemm_trace_dump": (C.c_int, [C.c_char_p]),
     "hkx_prefill_attention": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i32p,
                                         C.c_int, C.c_void_p]),
     "hkx_decode_attention_bytes": (C.c_double, [C.c_int, C.c_int, C.c_int, i32p, i32p, i32p, i32p, C.c_int]),

@@ -779,13 +779,19 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
         shared_phase<G>(tm_kv, a, sm);
         __syncthreads();
         if (warp >= DA_PV_WARPS) return;
-        if (lane == 0) {
-            for (int s = 0; s < PV_ST; ++s) mbar_init(&full[s], 1);
-            fence_barrier_init();
+        // the planner sizes private items for one round on the queue-only CTAs;
+        // a shared CTA only joins the queue when there are none or too few (the
+        // claim of an already empty queue is an L2 round trip on its tail)
+        const int q_ctas = static_cast<int>(gridDim.x) - a.n_sh;
+        if (q_ctas <= 0 || a.n_pv > q_ctas * DA_PV_WARPS) {
+            if (lane == 0) {
+                for (int s = 0; s < PV_ST; ++s) mbar_init(&full[s], 1);
+                fence_barrier_init();
+            }
+            __syncwarp();
+            nx.idx = lane == 0 ? atomicAdd(a.pv_next, 1) : 0;
+            prefetch_next(a, nx);
         }
-        __syncwarp();
-        nx.idx = lane == 0 ? atomicAdd(a.pv_next, 1) : 0;
-        prefetch_next(a, nx);
     } else {
         stamp(a, blockIdx.x, 0);
         // Queue-only CTA: claim the first item and start streaming its pages

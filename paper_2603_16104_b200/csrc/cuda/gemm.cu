@@ -14,6 +14,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <array>
+#include <cstdio>
+#include <vector>
 #include <cstdlib>
 #include <mutex>
 
@@ -40,7 +43,15 @@ struct GemmParams {
     int cluster;  // 1: the grid.z split-K CTAs form a cluster and reduce through DSMEM
     int skip_epi; // timing experiments only (HK_GEMM_DEBUG_SKIP_EPI): no output stores
     RopeArgs rope; // kEpiQkvRope: the q/k/v rows and this layer's KV pages
+    int l2_pf;     // weight k-blocks prefetched into L2 before griddepcontrol.wait
+    unsigned long long* trace;  // debug (HK_GEMM_TRACE): [first CTA start, first wait done, ~last end] (atomicMin)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // kEpiQkvRope (cluster split-K only): the tile is one 128-row head of the
 // fused QKV projection (BM == head_dim). Rank r of the s-CTA cluster owns
@@ -151,6 +162,7 @@ __global__ void __launch_bounds__(128, 1)
     const uint32_t tmem = *tmem_slot;
 
     pdl_trigger();  // let the next kernel of the chain get scheduled (it prefetches its own weights)
+    if (p.trace && threadIdx.x == 0) atomicMin(&p.trace[0], gtimer());
     if (warp == 0) {
         if (lane == 0) {
             const uint64_t pol_w = policy_evict_first();
@@ -162,7 +174,11 @@ __global__ void __launch_bounds__(128, 1)
                 mbar_expect_tx(&full[i], A_BYTES + B_BYTES);
                 tma_load_2d_hint(sA + i * A_BYTES, &tmW, &full[i], (kb0 + i) * BK, m0, pol_w);
             }
+            // ...and pull the next weight blocks into L2 while the predecessor
+            // (often a latency-bound row kernel) still runs
+            for (int i = pre; i < min(nkb, pre + p.l2_pf); ++i) tma_prefetch_2d(&tmW, (kb0 + i) * BK, m0);
             pdl_wait();
+            if (p.trace) atomicMin(&p.trace[1], gtimer());
             for (int i = 0; i < pre; ++i) tma_load_2d_hint(sB + i * B_BYTES, &tmX, &full[i], (kb0 + i) * BK, n0, pol_x);
             for (int i = pre; i < nkb; ++i) {
                 const int s = i % STAGES;
@@ -382,6 +398,7 @@ __global__ void __launch_bounds__(128, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 2) tmem_dealloc(tmem, TMEM_COLS);
+    if (p.trace && threadIdx.x == 0) atomicMin(&p.trace[2], ~gtimer());
 }
 
 // Deterministic split-K reduction (fixed summation order) fused with the epilogue.
@@ -524,6 +541,53 @@ int g_num_sms = 148;
 unsigned long long g_launches = 0;
 bool g_pdl = true;
 
+// HK_GEMM_TRACE=1 (debug; run with HK_NO_GRAPHS=1): every tcgen05 GEMM launch
+// gets a slot recording its first CTA start, first griddepcontrol.wait exit
+// and last CTA end (%globaltimer); hkx_gemm_trace_dump writes them out.
+namespace {
+struct GemmTrace {
+    unsigned long long* d = nullptr;
+    int n = 0, cap = 0;
+    std::vector<std::array<int, 5>> meta;  // N, K, T, splits, grid CTAs
+};
+GemmTrace g_gtrace;
+unsigned long long* gemm_trace_slot(int N, int K, int T, int splits, int ctas) {
+    static const bool on = std::getenv("HK_GEMM_TRACE") != nullptr;
+    if (!on) return nullptr;
+    if (!g_gtrace.d) {
+        g_gtrace.cap = 1 << 16;
+        HK_CUDA(cudaMalloc(&g_gtrace.d, static_cast<size_t>(g_gtrace.cap) * 4 * 8));
+        HK_CUDA(cudaMemset(g_gtrace.d, 0xff, static_cast<size_t>(g_gtrace.cap) * 4 * 8));
+    }
+    if (g_gtrace.n >= g_gtrace.cap) return nullptr;
+    g_gtrace.meta.push_back({N, K, T, splits, ctas});
+    return g_gtrace.d + 4 * static_cast<size_t>(g_gtrace.n++);
+}
+}  // namespace
+
+int gemm_trace_dump(const char* path) {
+    if (!g_gtrace.d) return 0;
+    HK_CUDA(cudaDeviceSynchronize());
+    std::vector<unsigned long long> h(static_cast<size_t>(g_gtrace.n) * 4);
+    HK_CUDA(cudaMemcpy(h.data(), g_gtrace.d, h.size() * 8, cudaMemcpyDeviceToHost));
+    FILE* f = std::fopen(path, "w");
+    if (!f) return -1;
+    std::fprintf(f, "slot,N,K,T,splits,ctas,start,wait_done,end\n");
+    for (int i = 0; i < g_gtrace.n; ++i) {
+        const auto& m = g_gtrace.meta[static_cast<size_t>(i)];
+        std::fprintf(f, "%d,%d,%d,%d,%d,%d,%llu,%llu,%llu\n", i, m[0], m[1], m[2], m[3], m[4], h[4 * i], h[4 * i + 1],
+                     ~h[4 * i + 2]);
+    }
+    std::fclose(f);
+    return g_gtrace.n;
+}
+
+// HK_GEMM_L2PF=<k-blocks>: weight blocks per CTA prefetched into L2 before griddepcontrol.wait
+static int gemm_l2_prefetch_blocks() {
+    static const int v = std::getenv("HK_GEMM_L2PF") ? std::atoi(std::getenv("HK_GEMM_L2PF")) : 0;
+    return v;
+}
+
 int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, const bf16* bias,
               float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits, int max_splits) {
     if (T <= 0) return 0;
@@ -584,6 +648,8 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
     static const int skip_epi = std::getenv("HK_GEMM_DEBUG_SKIP_EPI") ? 1 : 0;
     GemmParams p{N, K, T, kb, kbps, via_ws ? kEpiPartial : epi, out, ldo, bias,
                  epi == kEpiPartial ? static_cast<float*>(out) : workspace, cluster ? 1 : 0, skip_epi};
+    p.l2_pf = gemm_l2_prefetch_blocks();
+    p.trace = gemm_trace_slot(N, K, T, splits, mt * nt * splits);
     const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
     const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
     dim3 grid(mt, nt, splits);
@@ -622,7 +688,7 @@ int gemm_bf16_qkv_rope(const bf16* W, const bf16* X, int N, int K, const bf16* b
     splits = std::min(splits, std::max(1, kb / 4));
     const int kbps = (kb + splits - 1) / splits;
     splits = (kb + kbps - 1) / kbps;
-    GemmParams p{N, K, T, kb, kbps, kEpiQkvRope, nullptr, N, bias, nullptr, 1, 0, r};
+    GemmParams p{N, K, T, kb, kbps, kEpiQkvRope, nullptr, N, bias, nullptr, 1, 0, r, gemm_l2_prefetch_blocks()};
     const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
     const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
     dim3 grid(mt, nt, splits);

@@ -173,6 +173,14 @@ double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_
 
 /* Phase timestamps (%globaltimer ns) of the next hkx_decode_attention calls:
  * [n_sh + n_pv CTAs][8] into a device buffer of `words` u64 (NULL = off). */
+int hkx_gemm_trace_dump(const char* path) {
+    try {
+        return hkd::gemm_trace_dump(path);
+    } catch (...) {
+        return -1;
+    }
+}
+
 int hkx_decode_attention_trace(void* device_buf) {
     g_trace = static_cast<unsigned long long*>(device_buf);
     return 0;

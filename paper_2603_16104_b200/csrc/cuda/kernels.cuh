@@ -30,6 +30,8 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
 // split-K partials): kEpiPartial/kEpiStoreF32 write fp32 [T][ldo].
 void gemm_bf16_streamk(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, cudaStream_t st);
 bool gemm_streamk_enabled();
+// debug: write the HK_GEMM_TRACE launch spans as CSV; returns the launch count
+int gemm_trace_dump(const char* path);
 // allocate the stream-K workspace/counters ahead of any CUDA-graph capture
 void gemm_streamk_reserve(int max_tiles, int max_bn);
 // ids[t] = argmax over the n_tiles (max, idx) partials of kEpiArgmax (lowest index wins ties)

@@ -2,6 +2,7 @@
 // write, SwiGLU, greedy argmax) and the counter-based weight init.
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -383,6 +384,84 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(const float* __restric
     cluster_sync_all();  // peers read cta_sum: keep it alive until everyone has
 }
 
+// bf16 path: one CTA per row (no cluster barriers / DSMEM round trips), up
+// to 1024 threads x VPT float4; the norm weights are loaded before
+// griddepcontrol.wait. Same split order for x as add_rmsnorm_kernel.
+template <int VPT>
+__global__ void __launch_bounds__(1024) add_rmsnorm_row_kernel(const float* __restrict__ part, int splits, float* x,
+                                                               const bf16* __restrict__ w, int T_, int d, float eps,
+                                                               bf16* h, const int32_t* __restrict__ cmap, bf16* hc) {
+    pdl_trigger();
+    const int t = blockIdx.x;
+    const int n4 = d / 4;
+    uint2 wv[VPT];
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+        const int i = threadIdx.x + j * blockDim.x;
+        wv[j] = i < n4 ? __ldg(reinterpret_cast<const uint2*>(w) + i) : make_uint2(0u, 0u);
+    }
+    pdl_wait();
+    float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(t) * d);
+    const size_t pstride = static_cast<size_t>(T_) * d / 4;
+    const float4* pr = reinterpret_cast<const float4*>(part) + static_cast<size_t>(t) * d / 4;
+    float4 v[VPT];
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+        const int i = threadIdx.x + j * blockDim.x;
+        v[j] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int s0 = 0; s0 < splits; s0 += 8) {
+        float4 b[VPT][8];
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const int i = threadIdx.x + j * blockDim.x;
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+                b[j][s] = (i < n4 && s0 + s < splits) ? __ldcg(pr + (s0 + s) * pstride + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < VPT; ++j)
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {  // fixed split order: deterministic
+                v[j].x += b[j][s].x;
+                v[j].y += b[j][s].y;
+                v[j].z += b[j][s].z;
+                v[j].w += b[j][s].w;
+            }
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
+    __shared__ float red[32];
+    __shared__ float tot_s;
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float a = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        a = warp_sum(a);
+        if (threadIdx.x == 0) tot_s = a;
+    }
+    __syncthreads();
+    const float inv = rsqrtf(tot_s / static_cast<float>(d) + eps);
+    const int cr = cmap ? cmap[t] : -1;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+        const int i = threadIdx.x + j * blockDim.x;
+        if (i >= n4) continue;
+        if (splits > 0) xr[i] = v[j];
+        const __nv_bfloat162 w01 = *reinterpret_cast<const __nv_bfloat162*>(&wv[j].x);
+        const __nv_bfloat162 w23 = *reinterpret_cast<const __nv_bfloat162*>(&wv[j].y);
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(v[j].x * inv * __low2float(w01), v[j].y * inv * __high2float(w01));
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(v[j].z * inv * __low2float(w23), v[j].w * inv * __high2float(w23));
+        uint2 pk;
+        pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(h + static_cast<size_t>(t) * d + 4 * i) = pk;
+        if (cr >= 0) *reinterpret_cast<uint2*>(hc + static_cast<size_t>(cr) * d + 4 * i) = pk;
+    }
+}
+
 }  // namespace
 
 void init_uniform_gu(void* w, bool f32, int F, int d, uint64_t seed, uint64_t tensor_id, float scale, cudaStream_t st) {
@@ -412,6 +491,23 @@ void add_rmsnorm(const float* part, int splits, float* x, const void* w, bool f3
                  const int32_t* cmap, void* hc, cudaStream_t st) {
     if (!T) return;
     if (d % 4 || d > 8192 * 4) throw std::runtime_error("add_rmsnorm: d must be a multiple of 4");
+    static const bool cluster_rms = std::getenv("HK_RMS_CLUSTER") != nullptr;  // A/B: the 8-CTA cluster kernel
+    if (!f32 && !cluster_rms && d / 4 <= 4 * 1024) {
+        const int n4 = d / 4;
+        const int vpt = n4 <= 1024 ? 1 : (n4 <= 2048 ? 2 : 4);
+        const int threads = std::min(1024, ((n4 + vpt - 1) / vpt + 31) / 32 * 32);
+        const bf16* wb = static_cast<const bf16*>(w);
+        bf16* hb = static_cast<bf16*>(h);
+        bf16* hcb = static_cast<bf16*>(hc);
+        if (vpt == 1)
+            launch_pdl(add_rmsnorm_row_kernel<1>, dim3(T), dim3(threads), 0, st, part, splits, x, wb, T, d, eps, hb, cmap, hcb);
+        else if (vpt == 2)
+            launch_pdl(add_rmsnorm_row_kernel<2>, dim3(T), dim3(threads), 0, st, part, splits, x, wb, T, d, eps, hb, cmap, hcb);
+        else
+            launch_pdl(add_rmsnorm_row_kernel<4>, dim3(T), dim3(threads), 0, st, part, splits, x, wb, T, d, eps, hb, cmap, hcb);
+        HK_LAUNCHED(1);
+        return;
+    }
     const int per = (d / 4 + kRowSplit - 1) / kRowSplit;          // float4 per CTA
     const int threads = std::max(32, (per + 31) / 32 * 32);
     if (threads > 256) throw std::runtime_error("add_rmsnorm: d too large");
