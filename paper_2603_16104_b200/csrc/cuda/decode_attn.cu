@@ -232,7 +232,6 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                 if (c < nch) load(c, 0);
                 if (c >= 1) load(c - 1, 1);
             }
-            prefetch_next_weights(a);
         }
         pdl_wait();
         pdl_trigger();
@@ -814,7 +813,6 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
                 }
             }
         }
-        if (warp == DA_PV_WARPS + 1 && lane == 0) prefetch_next_weights(a);  // (weights: no dependency)
         pdl_wait();  // q and this step's own K/V come from the qkv/RoPE kernel
         if (warp >= DA_PV_WARPS) return;
     }
@@ -827,6 +825,9 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
         pre = 0;
     }
     if (warp == 0) stamp(a, blockIdx.x, 12);
+    // this CTA's work is done; HBM idles while stragglers finish and rows merge:
+    // pull its slice of the O-projection weights into L2 (opt-in, HK_L2_PREFETCH_O)
+    if (threadIdx.x == 0) prefetch_next_weights(a);
     bulk_wait_all();  // a shared tile's bulk-copied output rows are written (before the grid barrier / exit)
     if (!a.merge_in_kernel) {
         // the last warp out rewinds the queue for the next launch

@@ -170,6 +170,7 @@ struct hk_engine {
     std::map<std::vector<int64_t>, int> graph_seen;
     bool use_graphs = true;
     bool l2_prefetch_o = false;  // decode attention pulls the O-projection weights into L2 (opt-in)
+    size_t pf_rms_bytes = 0;     // add_rmsnorm pulls this many bytes of the next GEMM's weights into L2
     void drop_graphs() {
         for (auto& [k, g] : graphs) cudaGraphExecDestroy(g.exec);
         graphs.clear();
@@ -291,6 +292,7 @@ hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m
     // opt-in: measured -2% on configs[1] (the prefetch traffic slows the attention more
     // than the O projection gains; profiles/r1_attention.txt)
     l2_prefetch_o = std::getenv("HK_L2_PREFETCH_O") != nullptr;
+    pf_rms_bytes = std::getenv("HK_PF_RMS_MB") ? static_cast<size_t>(std::atof(std::getenv("HK_PF_RMS_MB")) * 1048576) : 0;
     hkd::g_pdl = std::getenv("HK_NO_PDL") == nullptr;
     init_weights();
 
@@ -803,7 +805,9 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         int sp = gemm(lw.wo, attn, d, H * hd, T, hkd::kEpiPartial, pbuf, d);
         ck = clock.begin(5, st);
         if (dbl("rms")) hkd::add_rmsnorm(pbuf, 0, x, lw.mlp_norm, f32, T, d, eps, h, nullptr, nullptr, st);
-        hkd::add_rmsnorm(pbuf, sp, x, lw.mlp_norm, f32, T, d, eps, h, nullptr, nullptr, st);
+        if (!skip("rms"))
+            hkd::add_rmsnorm(pbuf, sp, x, lw.mlp_norm, f32, T, d, eps, h, nullptr, nullptr, st, lw.wgu,
+                             std::min(pf_rms_bytes, static_cast<size_t>(2) * F * d * esz));
         clock.end(ck, st);
         if (f32) {
             gemm(lw.wgu, h, 2 * F, d, T, hkd::kEpiStoreF32, gu, 2 * F);
@@ -818,8 +822,11 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         sp = gemm(lw.wd, act, d, F, T, hkd::kEpiPartial, pbuf, d);
         const bool last = l + 1 == L;
         ck = clock.begin(5, st);
-        hkd::add_rmsnorm(pbuf, sp, x, last ? final_norm : layers[static_cast<size_t>(l) + 1].attn_norm, f32, T, d, eps,
-                         h, last && S > 0 ? d_cmap : nullptr, last && S > 0 ? hs : nullptr, st);
+        if (last || !skip("rms"))
+            hkd::add_rmsnorm(pbuf, sp, x, last ? final_norm : layers[static_cast<size_t>(l) + 1].attn_norm, f32, T, d,
+                             eps, h, last && S > 0 ? d_cmap : nullptr, last && S > 0 ? hs : nullptr, st,
+                             last ? nullptr : layers[static_cast<size_t>(l) + 1].wqkv,
+                             std::min(pf_rms_bytes, static_cast<size_t>(QKV) * d * esz));
         clock.end(ck, st);
     }
     if (S > 0) {

@@ -90,8 +90,9 @@ struct QkvArgs {
 void qkv_rope_kv(const QkvArgs& a, cudaStream_t st);
 // Split-K consumer: x[t] += sum_s part[s][t]; h[t] = rmsnorm(x[t]) * w; rows with
 // cmap[t] >= 0 are also written to hc[cmap[t]] (compact rows for the LM head).
+// pf / pf_bytes: optional L2 prefetch of the next GEMM's weights (bf16 path)
 void add_rmsnorm(const float* part, int splits, float* x, const void* w, bool f32, int T, int d, float eps, void* h,
-                 const int32_t* cmap, void* hc, cudaStream_t st);
+                 const int32_t* cmap, void* hc, cudaStream_t st, const void* pf = nullptr, size_t pf_bytes = 0);
 // ids[r] = argmax_v logits[r][v] (lowest index on ties); also slot_last[slots[r]] = ids[r]
 void argmax_rows(const float* logits, int R, int V, int32_t* ids, const int32_t* slots, int32_t* slot_last,
                  cudaStream_t st);
