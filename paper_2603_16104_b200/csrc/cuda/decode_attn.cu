@@ -946,11 +946,10 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
     }
     static const int env_priv_keys = std::getenv("HK_ATTN_PRIV_KEYS") ? std::atoi(std::getenv("HK_ATTN_PRIV_KEYS")) : 0;
     // Shared split count S (measured on B200, tools/attn_bench.py, profiles/
-    // r1_attention.txt): shared CTAs should cover ~64 SMs when the rows also
-    // carry >= 4 private pages each (the private queue then keeps the other SMs
-    // streaming), ~128 SMs when a <= 2K-token shared prefix dominates, every SM
-    // for longer prefixes; SMs without a shared item start on the private
-    // queue at once.
+    // r1_attention.txt): shared CTAs should cover ~64 SMs for a <= 2K-token
+    // prefix (the private queue keeps the other SMs streaming), every SM for
+    // longer prefixes; SMs without a shared item start on the private queue
+    // at once.
     int best_s = 1;
     {
         double rows_n = 0;
@@ -960,7 +959,10 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
         for (const auto& g : groups)
             if (g.shared_pages > 0 && g.members > 1) max_nch = std::max(max_nch, (g.shared_pages + 7) / 8);
         // long shared prefixes (> 2K tokens, e.g. configs[4]'s 8K) are tensor-bound: one CTA per SM
-        const int target = max_nch > 16 ? num_sms : (priv_pages_per_row >= 4 ? 64 : 128);
+        // (r1c re-measure: ~64 shared CTAs at every k for a 2K prefix — the
+        // private items then run as one round on the other ~84 SMs)
+        (void)priv_pages_per_row;
+        const int target = max_nch > 16 ? num_sms : 64;
         if (tiles > 0) best_s = std::max(1, std::min(8, static_cast<int>(std::lround(static_cast<double>(target) / tiles))));
         static const int env_splits = std::getenv("HK_ATTN_SPLITS") ? std::atoi(std::getenv("HK_ATTN_SPLITS")) : 0;
         if (env_splits > 0) best_s = env_splits;
