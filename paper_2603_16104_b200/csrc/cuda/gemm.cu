@@ -45,7 +45,122 @@ struct GemmParams {
     RopeArgs rope; // kEpiQkvRope: the q/k/v rows and this layer's KV pages
     int l2_pf;     // weight k-blocks prefetched into L2 before griddepcontrol.wait
     unsigned long long* trace;  // debug (HK_GEMM_TRACE): [first CTA start, first wait done, ~last end] (atomicMin)
+    int rn_on;          // kEpiPartial + residual/RMSNorm tile reduction (gemm_bf16_resid_norm)
+    ResidNormArgs rn;
+    const float* in_ssq;  // kEpiSwiGLU: scale input rows by rsqrt(sum in_ssq / K + eps)
+    int n_ssq;
+    float in_eps;
 };
+
+__device__ __forceinline__ int ld_relaxed(const int32_t* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// wait until *c >= n: relaxed polls with back-off (many CTAs poll while the
+// tile's last split still streams), then an acquire fence
+__device__ __forceinline__ void spin_until(const int32_t* c, int n) {
+    while (ld_relaxed(c) < n) __nanosleep(20);
+    __threadfence();
+}
+
+// Residual + RMSNorm tail of a split-K tile (all 128 threads; partials of this
+// CTA already stored). See ResidNormArgs.
+template <int BN>
+__device__ __forceinline__ void resid_norm_tile(const GemmParams& p, int m0, int n0) {
+    const int s = static_cast<int>(gridDim.z), z = static_cast<int>(blockIdx.z);
+    const int tile = static_cast<int>(blockIdx.x);
+    const int ntiles = static_cast<int>(gridDim.x);
+    const ResidNormArgs& rn = p.rn;
+    int32_t* c0 = rn.ctr + 64 * tile;  // each counter on its own 128-byte line (polled by the tile's CTAs)
+    // arrival: bar.sync orders the CTA's partial stores before thread 0's
+    // fence + atomic (cumulative release); the acquire below pairs with it
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(c0, 1);
+        spin_until(c0, s);
+    }
+    __syncthreads();
+    const int SL = BM / s, nq = SL / 4;  // rows (features) of this CTA's slice, float4 groups per token
+    const int rows = min(BN, p.T - n0);
+    const size_t pstride = static_cast<size_t>(p.T) * p.N;
+    // two items per thread per pass, every load of both issued before any use
+    // (one L2 round trip per pass); nq is a power of two <= 16, so the nq
+    // lanes of a token are adjacent in one warp
+    for (int base = 0; base < nq * rows; base += 2 * blockDim.x) {
+        float4 v[2], b[2][8];
+        uint2 wv[2];
+        bool ok[2];
+        int tt[2], cc[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int idx = base + h * static_cast<int>(blockDim.x) + static_cast<int>(threadIdx.x);
+            ok[h] = idx < nq * rows;
+            tt[h] = n0 + (ok[h] ? idx / nq : 0);
+            cc[h] = m0 + z * SL + 4 * (idx % nq);
+            const size_t o = static_cast<size_t>(tt[h]) * p.N + cc[h];
+            v[h] = ok[h] ? *reinterpret_cast<const float4*>(rn.x + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+            wv[h] = ok[h] ? *reinterpret_cast<const uint2*>(rn.w + cc[h]) : make_uint2(0u, 0u);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                b[h][k] = (ok[h] && k < s) ? __ldcg(reinterpret_cast<const float4*>(p.partial + k * pstride + o))
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k < s) {  // split order, as add_rmsnorm: deterministic
+                    v[h].x += b[h][k].x;
+                    v[h].y += b[h][k].y;
+                    v[h].z += b[h][k].z;
+                    v[h].w += b[h][k].w;
+                }
+            float ss = v[h].x * v[h].x + v[h].y * v[h].y + v[h].z * v[h].z + v[h].w * v[h].w;
+            if (ok[h]) {
+                const size_t o = static_cast<size_t>(tt[h]) * p.N + cc[h];
+                *reinterpret_cast<float4*>(rn.x + o) = v[h];
+                const __nv_bfloat162 w01 = *reinterpret_cast<const __nv_bfloat162*>(&wv[h].x);
+                const __nv_bfloat162 w23 = *reinterpret_cast<const __nv_bfloat162*>(&wv[h].y);
+                uint2 pk;
+                pk.x = pack_bf16x2(v[h].x * __low2float(w01), v[h].y * __high2float(w01));
+                pk.y = pack_bf16x2(v[h].z * __low2float(w23), v[h].w * __high2float(w23));
+                *reinterpret_cast<uint2*>(rn.u + o) = pk;
+            }
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1)
+                if (o < nq) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            if (ok[h] && (threadIdx.x % nq) == 0) rn.ssq_slice[(static_cast<size_t>(tt[h]) * ntiles + tile) * 8 + z] = ss;
+        }
+    }
+    __syncthreads();
+    int32_t* c1 = c0 + 32;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(c1, 1);
+    }
+    if (z != 0) return;
+    if (threadIdx.x == 0) spin_until(c1, s);
+    __syncthreads();
+    // ssq[t][tile] = sum of the tile's slices (split order); [T][tiles] so a
+    // consumer reads a token's tiles contiguously
+    for (int t = n0 + static_cast<int>(threadIdx.x); t < n0 + rows; t += blockDim.x) {
+        const float4* q = reinterpret_cast<const float4*>(rn.ssq_slice + (static_cast<size_t>(t) * ntiles + tile) * 8);
+        const float4 lo = __ldcg(q), hi = __ldcg(q + 1);
+        const float e[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        float a = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < s) a += e[k];
+        rn.ssq[static_cast<size_t>(t) * ntiles + tile] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // every split CTA has passed both counters: rewind them for the next launch
+        *c0 = 0;
+        *c1 = 0;
+    }
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -294,13 +409,35 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
             for (int j = 0; j < 8; ++j) xs[row * (BN + 1) + c + j] = v[j];
         }
-        __syncthreads();
         const int nt = min(BN, p.T - n0);
+        float* rs = xs + BM * (BN + 1);  // [BN] per-token input scale
+        if (p.in_ssq) {
+            // ssq is [T][n_ssq]: two threads per token, each a half of the tiles
+            // as independent float4 loads, combined in a fixed order
+            const int c = threadIdx.x >> 1, hf = threadIdx.x & 1;
+            float a = 0.f;
+            if (c < nt) {
+                const float4* q = reinterpret_cast<const float4*>(p.in_ssq + static_cast<size_t>(n0 + c) * p.n_ssq);
+                const int n4 = p.n_ssq / 4, h0 = hf * ((n4 + 1) / 2), h1 = hf ? n4 : (n4 + 1) / 2;
+                float4 v[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = h0 + i < h1 ? __ldcg(q + h0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) a += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+            }
+            a += __shfl_xor_sync(0xffffffffu, a, 1);
+            if (c < nt && hf == 0) rs[c] = rsqrtf(a / static_cast<float>(p.K) + p.in_eps);
+        }
+        __syncthreads();
         for (int idx = threadIdx.x; idx < 64 * nt; idx += blockDim.x) {
             const int r = idx & 63, c = idx >> 6;
             const int f = blockIdx.x * 64 + r;  // output feature
             if (blockIdx.x * BM + r < p.N) {
-                const float g = xs[r * (BN + 1) + c], u = xs[(r + 64) * (BN + 1) + c];
+                float g = xs[r * (BN + 1) + c], u = xs[(r + 64) * (BN + 1) + c];
+                if (p.in_ssq) {
+                    g *= rs[c];
+                    u *= rs[c];
+                }
                 static_cast<bf16*>(p.out)[static_cast<size_t>(n0 + c) * p.ldo + f] =
                     f2bf(__fdividef(g, 1.0f + __expf(-g)) * u);
             }
@@ -398,6 +535,8 @@ __global__ void __launch_bounds__(128, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 2) tmem_dealloc(tmem, TMEM_COLS);
+    if (p.trace && threadIdx.x == 0) atomicMin(&p.trace[3], ~gtimer());  // last CTA to finish its main loop + stores
+    if (p.rn_on) resid_norm_tile<BN>(p, m0, n0);
     if (p.trace && threadIdx.x == 0) atomicMin(&p.trace[2], ~gtimer());
 }
 
@@ -572,11 +711,11 @@ int gemm_trace_dump(const char* path) {
     HK_CUDA(cudaMemcpy(h.data(), g_gtrace.d, h.size() * 8, cudaMemcpyDeviceToHost));
     FILE* f = std::fopen(path, "w");
     if (!f) return -1;
-    std::fprintf(f, "slot,N,K,T,splits,ctas,start,wait_done,end\n");
+    std::fprintf(f, "slot,N,K,T,splits,ctas,start,wait_done,end,mainloop_end\n");
     for (int i = 0; i < g_gtrace.n; ++i) {
         const auto& m = g_gtrace.meta[static_cast<size_t>(i)];
-        std::fprintf(f, "%d,%d,%d,%d,%d,%d,%llu,%llu,%llu\n", i, m[0], m[1], m[2], m[3], m[4], h[4 * i], h[4 * i + 1],
-                     ~h[4 * i + 2]);
+        std::fprintf(f, "%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu\n", i, m[0], m[1], m[2], m[3], m[4], h[4 * i], h[4 * i + 1],
+                     ~h[4 * i + 2], ~h[4 * i + 3]);
     }
     std::fclose(f);
     return g_gtrace.n;
@@ -668,6 +807,63 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
         HK_LAUNCHED(1);
     }
     return splits;
+}
+
+int gemm_bf16_resid_norm(const bf16* W, const bf16* X, int N, int K, int T, float* partial, size_t partial_floats,
+                         const ResidNormArgs& rn, cudaStream_t st) {
+    // opt-in (HK_RESID_FUSED=1): measured slower on B200 — the two counter
+    // barriers wait behind the fences on the tile's 8.4 MB partial-store burst
+    // (tail 8.5 us, 6.3 us with the barriers alone) vs ~5 us for the separate
+    // add_rmsnorm kernel + its PDL hand-off (profiles/r1_marginal_costs.txt)
+    static const bool on = std::getenv("HK_RESID_FUSED") != nullptr;
+    if (!on || T <= 0 || T > 64 || N % BM != 0 || K % BK != 0 || (N / BM) % 4 != 0 || N / BM > 64) return -1;
+    const int BN = T <= 16 ? 16 : (T <= 32 ? 32 : 64);
+    const int mt = N / BM, kb = K / BK;
+    int splits = 1;
+    if (mt * 2 <= 2 * g_num_sms) splits = std::min(8, 2 * g_num_sms / mt);
+    splits = std::min(splits, std::max(1, kb / 4));
+    while (splits & (splits - 1)) --splits;  // 2, 4 or 8: a slice of 128 / splits rows is whole float4 groups
+    if (splits < 2) return -1;
+    const int kbps = (kb + splits - 1) / splits;
+    if ((kb + kbps - 1) / kbps != splits) return -1;          // no empty split
+    if (mt * splits > 2 * g_num_sms) return -1;              // the tile's split CTAs wait for each other: co-resident
+    if (static_cast<size_t>(splits) * T * N > partial_floats) return -1;
+    GemmParams p{N, K, T, kb, kbps, kEpiPartial, partial, N, nullptr, partial, 0, 0};
+    p.rn_on = 1;
+    p.rn = rn;
+    p.trace = gemm_trace_slot(N, K, T, splits, mt * splits);
+    const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
+    const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
+    const dim3 grid(mt, 1, splits);
+    switch (BN) {
+        case 16: launch_tc<16, 4>(tw, tx, p, grid, st); break;
+        case 32: launch_tc<32, 4>(tw, tx, p, grid, st); break;
+        default: launch_tc<64, 4>(tw, tx, p, grid, st); break;
+    }
+    return splits;
+}
+
+void gemm_bf16_swiglu_scaled(const bf16* W, const bf16* X, int N, int K, int T, void* out, int ldo, const float* in_ssq,
+                             int n_ssq, float eps, cudaStream_t st) {
+    if (T <= 0) return;
+    if (K % BK != 0) throw std::runtime_error("gemm_bf16_swiglu_scaled: K must be a multiple of 64");
+    const int BN = T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256;
+    const int mt = (N + BM - 1) / BM, nt = (T + BN - 1) / BN, kb = K / BK;
+    GemmParams p{N, K, T, kb, kb, kEpiSwiGLU, out, ldo, nullptr, nullptr, 0, 0};
+    p.in_ssq = in_ssq;
+    p.n_ssq = n_ssq;
+    p.in_eps = eps;
+    p.trace = gemm_trace_slot(N, K, T, 1, mt * nt);
+    const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
+    const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
+    const dim3 grid(mt, nt, 1);
+    switch (BN) {
+        case 16: launch_tc<16, 4>(tw, tx, p, grid, st); break;
+        case 32: launch_tc<32, 4>(tw, tx, p, grid, st); break;
+        case 64: launch_tc<64, 4>(tw, tx, p, grid, st); break;
+        case 128: launch_tc<128, 4>(tw, tx, p, grid, st); break;
+        default: launch_tc<256, 4>(tw, tx, p, grid, st); break;
+    }
 }
 
 int gemm_bf16_qkv_rope(const bf16* W, const bf16* X, int N, int K, const bf16* bias, const RopeArgs& r,

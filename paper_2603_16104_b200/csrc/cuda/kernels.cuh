@@ -66,6 +66,30 @@ struct RopeArgs {
     int block;
 };
 void rope_kv_write(const RopeArgs& a, cudaStream_t st);
+// Residual + RMSNorm folded into a split-K GEMM (decode, T <= 64, bf16): the
+// split CTAs of a 128-row tile meet at a counter (all CTAs are co-resident:
+// mt * splits <= 2 CTAs per SM), each reduces 128/splits rows of the tile in
+// split order, adds them to the fp32 residual x, writes u = bf16(x * w) (the
+// next GEMM's input, NOT yet scaled by 1/rms) and per-token sums of squares;
+// split 0 folds them into ssq[tile][t]. Consumers scale by
+// rsqrt(sum_tiles ssq / d + eps) (qkv_rope_kv, the SwiGLU epilogue).
+struct ResidNormArgs {
+    float* x;           // [T][N] fp32 residual stream (in/out)
+    const bf16* w;      // [N] norm weight
+    bf16* u;            // [T][N] out
+    float* ssq;         // [T][N / 128] out (a token's tiles contiguous)
+    float* ssq_slice;   // scratch [T][N / 128][8]
+    int32_t* ctr;       // [N / 128][64] (two counters per tile, 128 B apart), zero between launches
+};
+// Returns the split count used (>= 2), or -1 when not applicable (caller falls
+// back to kEpiPartial + add_rmsnorm). `partial` holds splits * T * N floats.
+int gemm_bf16_resid_norm(const bf16* W, const bf16* X, int N, int K, int T, float* partial, size_t partial_floats,
+                         const ResidNormArgs& rn, cudaStream_t st);
+// The SwiGLU GEMM with its input rows scaled by rsqrt(sum_i in_ssq[t][i] / K + eps)
+// (i < n_ssq) — the consumer side of gemm_bf16_resid_norm.
+void gemm_bf16_swiglu_scaled(const bf16* W, const bf16* X, int N, int K, int T, void* out, int ldo, const float* in_ssq,
+                             int n_ssq, float eps, cudaStream_t st);
+
 // Fused QKV projection (bf16, head_dim 128): split-K CTAs of a cluster reduce
 // through DSMEM and apply bias + RoPE + the K/V page write in the epilogue
 // (the result of gemm_bf16 kEpiPartial followed by qkv_rope_kv, one kernel).
@@ -86,6 +110,10 @@ struct QkvArgs {
     int splits;
     const void* bias;       // [QKV] or null
     RopeArgs r;             // r.qkv receives the rotated q (and raw k, v) rows
+    const float* in_ssq = nullptr;  // input rows were u = x * w: scale by rsqrt(sum ssq / d + eps) first
+    int n_ssq = 0;
+    float eps = 0.f;
+    int d = 0;
 };
 void qkv_rope_kv(const QkvArgs& a, cudaStream_t st);
 // Split-K consumer: x[t] += sum_s part[s][t]; h[t] = rmsnorm(x[t]) * w; rows with

@@ -228,6 +228,17 @@ __global__ void qkv_rope_kv_kernel(QkvArgs a) {
     pdl_wait();
     const RopeArgs& r = a.r;
     const int t = blockIdx.y;
+    // input rows were u = x * w (gemm_bf16_resid_norm): this token's 1 / rms
+    __shared__ float s_inv;
+    if (a.in_ssq) {
+        if (threadIdx.x < 32) {
+            float v = 0.f;
+            for (int i = threadIdx.x; i < a.n_ssq; i += 32) v += a.in_ssq[static_cast<size_t>(t) * a.n_ssq + i];
+            v = warp_sum(v);
+            if (threadIdx.x == 0) s_inv = rsqrtf(v / static_cast<float>(a.d) + a.eps);
+        }
+        __syncthreads();
+    }
     const int half = r.hd / 2;
     const int n_rot = (r.H + r.Hkv) * half;   // (i, i + half) pairs of q and k heads
     const int n_v = r.Hkv * half;             // v handled as (2j, 2j + 1) pairs
@@ -267,6 +278,10 @@ __global__ void qkv_rope_kv_kernel(QkvArgs a) {
             x0 += p0[s];
             x1 += p1[s];
         }
+    }
+    if (a.in_ssq) {
+        x0 *= s_inv;
+        x1 *= s_inv;
     }
     if (a.bias) {
         if (sizeof(T) == 4) {

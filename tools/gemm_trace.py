@@ -19,12 +19,15 @@ for r in rows:
     st, wd, en = int(r["start"]), int(r["wait_done"]), int(r["end"])
     name = NAMES.get((N, K))
     if name and T <= 64 and wd < (1 << 63) and prev_end is not None:
-        d = stats.setdefault(name, {"eff": [], "early": [], "gap": [], "bytes": N * K * 2})
+        d = stats.setdefault(name, {"eff": [], "early": [], "gap": [], "tail": [], "bytes": N * K * 2})
+        if "mainloop_end" in r:
+            d["tail"].append((en - int(r["mainloop_end"])) / 1e3)
         d["eff"].append((en - wd) / 1e3)
         d["early"].append((wd - st) / 1e3)
         d["gap"].append((wd - prev_end) / 1e3)
     prev_end = en
-print(f"{'gemm':8s} {'n':>5s} {'eff us':>8s} {'GB/s':>8s} {'early us':>9s} {'gap before us':>14s}")
+print(f"{'gemm':8s} {'n':>5s} {'eff us':>8s} {'GB/s':>8s} {'early us':>9s} {'gap before us':>14s} {'tail us':>8s}")
 for name, d in stats.items():
     e = S.median(d["eff"])
-    print(f"{name:8s} {len(d['eff']):5d} {e:8.2f} {d['bytes'] / e / 1e3:8.0f} {S.median(d['early']):9.2f} {S.median(d['gap']):14.2f}")
+    tail = S.median(d['tail']) if d['tail'] else float('nan')
+    print(f"{name:8s} {len(d['eff']):5d} {e:8.2f} {d['bytes'] / e / 1e3:8.0f} {S.median(d['early']):9.2f} {S.median(d['gap']):14.2f} {tail:8.2f}")
