@@ -135,6 +135,7 @@ def main():
     ap.add_argument("--workload", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-pin-broadcast", action="store_true", help="N>1: every rank prefills its pinned prefix itself")
     args = ap.parse_args()
     ws, rank, local = dist_env()
     if ws > 1 and args.gpus != ws:
@@ -166,6 +167,13 @@ def main():
     eng = Engine(model, EngineConfig(device=device, n_workers=1, pages_per_worker=pages_for(sc, max_calls, 512),
                                      max_calls=max_calls, max_step_tokens=8192 + 256, max_ctx_tokens=8192,
                                      use_device_trie=True))
+
+    pin_role = 0
+    if ws > 1 and not args.no_pin_broadcast:
+        # K6: rank 0 prefills the shared pinned prefix, the others receive its
+        # KV pages over NCCL instead of recomputing them (when the pins match)
+        from paper_2603_16104_b200 import exchange
+        pin_role = exchange.enable_pin_broadcast(eng, helios.worker_pins(blob, sc, only if only >= 0 else 0))
 
     def barrier():
         if ws > 1:
@@ -231,7 +239,9 @@ def main():
                    "decode_tokens_per_step": decode // args.steps, "iterations": last_m.iterations,
                    "hit_rate_pct": last_m.hit_rate_pct, "parallelism": f"{args.gpus} worker(s), one per GPU",
                    "l2": "inputs > L2: 15 GB of weights streamed every decode iteration",
-                   "pin_precompute_ms_per_step": pin_ms / args.steps},
+                   "pin_precompute_ms_per_step": pin_ms / args.steps,
+                   "pin_exchange": {0: "local prefill", 1: "prefill + NCCL broadcast source",
+                                    2: "NCCL broadcast receiver"}[pin_role]},
         "e2e": {"value": decode / wall_s, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": launches,

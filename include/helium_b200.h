@@ -175,6 +175,21 @@ size_t hk_engine_page_bytes(const hk_engine* e);
 /* resets pools, slots and tries of every worker */
 int hk_engine_reset(hk_engine* e);
 
+/* K6 pinned-prefix replication (SURVEY.md §8(e) exchange 1; reference
+ * static_pin_prefixes + pin insert, simulator.cpp:132-199, :257-263): every
+ * worker pins the same prefix, so one rank computes its KV and the others
+ * receive the pages instead of recomputing them. The pin precompute of
+ * hk_simulate calls fn once per worker that pinned new blocks, with a device
+ * buffer of `bytes` = (newly pinned pages, in pin / block order) x
+ * hk_engine_page_bytes, each page laid out as hk_pool_gather writes it.
+ *   role 0: compute locally, no callback (default)
+ *   role 1: compute, then fn(buffer holding the pages)  (broadcast source)
+ *   role 2: skip the compute; fn fills the buffer, the engine scatters it
+ *           into this worker's pin pages                (receiver)
+ * fn returns 0 on success; non-zero fails hk_simulate with "simulate: ...". */
+typedef int (*hk_pin_exchange_fn)(void* user, int worker, void* device_buf, uint64_t bytes);
+int hk_engine_set_pin_exchange(hk_engine* e, int role, hk_pin_exchange_fn fn, void* user);
+
 /* K1 block pool: page-granular gather / scatter / copy on the device.
  * dst/src are device pointers of n * page_bytes bytes. */
 int hk_pool_gather(hk_engine* e, int worker, const int32_t* pages, size_t n, void* dst_device);

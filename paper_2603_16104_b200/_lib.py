@@ -58,6 +58,9 @@ class EngineStatsC(C.Structure):
                 ("step_tokens", C.c_uint64), ("attn_bytes", C.c_double)]
 
 
+# K6 pin exchange callback: int fn(void* user, int worker, void* device_buf, uint64_t bytes)
+PinExchangeFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_uint64)
+
 _SIGS = {
     "hk_engine_stats_get": (C.c_int, [C.c_void_p, C.POINTER(EngineStatsC)]),
     "hk_last_error": (C.c_char_p, []),
@@ -89,6 +92,7 @@ _SIGS = {
     "hk_engine_destroy": (None, [C.c_void_p]),
     "hk_engine_page_bytes": (C.c_size_t, [C.c_void_p]),
     "hk_engine_reset": (C.c_int, [C.c_void_p]),
+    "hk_engine_set_pin_exchange": (C.c_int, [C.c_void_p, C.c_int, PinExchangeFn, C.c_void_p]),
     "hk_pool_gather": (C.c_int, [C.c_void_p, C.c_int, i32p, C.c_size_t, C.c_void_p]),
     "hk_pool_scatter": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, i32p, C.c_size_t]),
     "hk_pool_copy": (C.c_int, [C.c_void_p, C.c_int, i32p, i32p, C.c_size_t]),

@@ -173,6 +173,10 @@ struct hk_engine {
     std::map<std::vector<int64_t>, int> graph_seen;
     bool use_graphs = true;
     bool l2_prefetch_o = false;  // decode attention pulls the O-projection weights into L2 (opt-in)
+    // K6 pinned-prefix replication (hk_engine_set_pin_exchange)
+    int pin_role = 0;
+    hk_pin_exchange_fn pin_fn = nullptr;
+    void* pin_user = nullptr;
     size_t pf_rms_bytes = 0;     // add_rmsnorm pulls this many bytes of the next GEMM's weights into L2
     void drop_graphs() {
         for (auto& [k, g] : graphs) cudaGraphExecDestroy(g.exec);
@@ -1077,20 +1081,49 @@ class DeviceBody : public LlmBody {
     void precompute_pins(int w, const std::vector<TokenSeq>& pins, const std::vector<std::vector<int>>& pin_pages,
                          const std::vector<std::size_t>& first_new) override {
         const int block = static_cast<int>(e_->ec.block_tokens);
-        for (std::size_t i = 0; i < pins.size(); ++i) {
-            const int start = static_cast<int>(first_new[i]) * block;
-            const int len = static_cast<int>(pins[i].size());
-            for (int c0 = start; c0 < len; c0 += e_->maxT) {
-                std::vector<hk_engine::SegIn> segs(1);
-                segs[0].slot = 0;
-                segs[0].start = c0;
-                segs[0].count = std::min(e_->maxT, len - c0);
-                segs[0].table = &pin_pages[i];
-                segs[0].prompt = &pins[i];
-                e_->step(pw(w), segs);
+        const int role = e_->pin_fn ? e_->pin_role : 0;
+        if (role != 2) {
+            for (std::size_t i = 0; i < pins.size(); ++i) {
+                const int start = static_cast<int>(first_new[i]) * block;
+                const int len = static_cast<int>(pins[i].size());
+                for (int c0 = start; c0 < len; c0 += e_->maxT) {
+                    std::vector<hk_engine::SegIn> segs(1);
+                    segs[0].slot = 0;
+                    segs[0].start = c0;
+                    segs[0].count = std::min(e_->maxT, len - c0);
+                    segs[0].table = &pin_pages[i];
+                    segs[0].prompt = &pins[i];
+                    e_->step(pw(w), segs);
+                }
             }
         }
         e_->sync();
+        if (role == 0) return;
+        // K6: the newly pinned pages, in pin / block order, leave (source) or
+        // arrive (receiver) through one device buffer
+        std::vector<int32_t> pages;
+        for (std::size_t i = 0; i < pins.size(); ++i)
+            for (std::size_t j = first_new[i]; j < pin_pages[i].size(); ++j) pages.push_back(pin_pages[i][j]);
+        if (pages.empty()) return;
+        const uint64_t bytes = static_cast<uint64_t>(pages.size()) * hk_engine_page_bytes(e_);
+        void* buf = nullptr;
+        HK_CUDA(cudaMalloc(&buf, bytes));
+        auto done = [&](int rc, const char* what) {
+            if (rc != 0) {
+                cudaFree(buf);
+                throw std::runtime_error(std::string("simulate: pin exchange ") + what + " failed for worker " +
+                                         std::to_string(w) + (rc < 0 ? ": " + std::string(hk_last_error()) : ""));
+            }
+        };
+        if (role == 1) {
+            done(hk_pool_gather(e_, pw(w), pages.data(), pages.size(), buf), "gather");
+            done(e_->pin_fn(e_->pin_user, w, buf, bytes), "callback");
+        } else {
+            done(e_->pin_fn(e_->pin_user, w, buf, bytes), "callback");
+            done(hk_pool_scatter(e_, pw(w), buf, pages.data(), pages.size()), "scatter");
+        }
+        e_->sync();
+        cudaFree(buf);
     }
     void sync_trie(int w, KvTree& tree) override {
         e_->trie_sync(pw(w), tree.journal(), [&tree](int node) { return tree.node_key(node); });
@@ -1188,6 +1221,16 @@ hk_engine* hk_engine_create(const hk_model_config* m, const hk_engine_config* c)
 }
 
 void hk_engine_destroy(hk_engine* e) { delete e; }
+
+int hk_engine_set_pin_exchange(hk_engine* e, int role, hk_pin_exchange_fn fn, void* user) {
+    return guarded([&] {
+        if (role < 0 || role > 2) throw std::runtime_error("hk_engine_set_pin_exchange: role must be 0, 1 or 2");
+        if (role != 0 && !fn) throw std::runtime_error("hk_engine_set_pin_exchange: roles 1 and 2 need a callback");
+        e->pin_role = role;
+        e->pin_fn = role ? fn : nullptr;
+        e->pin_user = user;
+    });
+}
 
 size_t hk_engine_page_bytes(const hk_engine* e) { return e ? e->page_bytes_layer * e->L : 0; }
 

@@ -97,7 +97,10 @@ class Engine:
 
     def close(self):
         if getattr(self, "handle", None):
-            _lib.load().hk_engine_destroy(self.handle)
+            try:
+                _lib.load().hk_engine_destroy(self.handle)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.handle = None
 
     def __del__(self):
@@ -162,6 +165,30 @@ class Engine:
                                        pt.ctypes.data_as(_lib.i32p), stride)
         _lib.check_status(rc, "hk_trie_match")
         return matched, path, pt
+
+    def set_pin_exchange(self, role: int, fn=None):
+        """K6 pinned-prefix replication (hk_engine_set_pin_exchange): role 0
+        computes pins locally; role 1 computes them and calls fn(worker,
+        device_ptr, nbytes) with the newly pinned pages; role 2 skips the
+        compute and expects fn to fill the buffer. An exception raised by fn
+        fails the run (hk_simulate raises "simulate: pin exchange ...")."""
+        self._pin_fn, self._pin_exc = fn, None
+
+        def _cb(_user, worker, buf, nbytes):
+            try:
+                fn(int(worker), int(buf or 0), int(nbytes))
+                return 0
+            except Exception as e:  # surfaced by take_pin_exchange_error()
+                self._pin_exc = e
+                return 1
+
+        self._pin_cb = _lib.PinExchangeFn(_cb) if fn is not None else _lib.PinExchangeFn()  # NULL
+        _lib.check_status(_lib.load().hk_engine_set_pin_exchange(self.handle, role, self._pin_cb, None),
+                          "hk_engine_set_pin_exchange")
+
+    def take_pin_exchange_error(self):
+        e, self._pin_exc = getattr(self, "_pin_exc", None), None
+        return e
 
     def pool_gather(self, worker: int, pages: Sequence[int], dst_ptr: int):
         p = np.ascontiguousarray(np.asarray(pages, dtype=np.int32))

@@ -1,0 +1,81 @@
+"""K6: pinned-prefix replication across ranks (exchange 1).
+
+The reference pins the same static prefix on every worker that runs >= 2
+calls under it (static_pin_prefixes + pin insert, simulator.cpp:132-199,
+:257-263; C2' pins 2,048 tokens on each of 8 workers). With one process per
+GPU, the source rank computes the pin's KV (the prefill) and the others
+receive the pages with one broadcast instead of recomputing them
+(hk_engine_set_pin_exchange, role 1 = source, 2 = receiver). Over NCCL the
+transfer runs NVLink peer to peer; 256 MiB for C2's prefix at Llama shape.
+
+The exchange is only enabled when every rank's worker pins exactly the same
+token sequences (checked with an all-gather of a digest): a worker with a
+different prefix (e.g. C4's per-operator overlap) keeps computing its own.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+from typing import List, Sequence
+
+import numpy as np
+
+
+class _CudaBytes:
+    """uint8 view of a raw device allocation (no copy) for torch.as_tensor."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+
+
+def buffer_tensor(ptr: int, nbytes: int, device: str):
+    """A torch uint8 tensor aliasing `nbytes` at `ptr` (device memory for
+    "cuda", host memory for "cpu", the gloo tests)."""
+    import torch
+    if device == "cpu":
+        arr = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(ptr))
+        return torch.from_numpy(arr)
+    return torch.as_tensor(_CudaBytes(ptr, nbytes), device=device)
+
+
+def pins_digest(pins: Sequence[Sequence[int]]) -> bytes:
+    h = hashlib.sha256()
+    for p in pins:
+        h.update(len(p).to_bytes(8, "little"))
+        h.update(np.asarray(p, dtype=np.uint64).tobytes())
+    return h.digest()
+
+
+def same_pins_everywhere(pins: List[List[int]], group=None) -> bool:
+    """True when every rank pins the same (non-empty) token sequences."""
+    import torch.distributed as dist
+    ws = dist.get_world_size(group)
+    digests = [None] * ws
+    dist.all_gather_object(digests, (pins_digest(pins), sum(len(p) for p in pins)), group=group)
+    return all(d == digests[0] for d in digests) and digests[0][1] > 0
+
+
+def make_broadcast_fn(src: int, device: str, group=None):
+    """The callback: broadcast the pin pages from rank `src` into every rank's buffer."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(worker: int, ptr: int, nbytes: int):
+        t = buffer_tensor(ptr, nbytes, device)
+        dist.broadcast(t, src=src, group=group)
+        if device != "cpu":
+            torch.cuda.synchronize()
+
+    return fn
+
+
+def enable_pin_broadcast(engine, pins: List[List[int]], src: int = 0, device: str = "cuda", group=None) -> int:
+    """Enable K6 on `engine` for this rank; returns the role set (0 = the
+    ranks' pins differ: every rank computes its own)."""
+    import torch.distributed as dist
+    if dist.get_world_size(group) < 2 or not same_pins_everywhere(pins, group):
+        engine.set_pin_exchange(0)
+        return 0
+    role = 1 if dist.get_rank(group) == src else 2
+    engine.set_pin_exchange(role, make_broadcast_fn(src, device, group))
+    return role

@@ -185,7 +185,8 @@ def simulate(plan: bytes, cfg: SimConfig, engine=None, verify_lookup: bool = Fal
     flags = (1 if verify_lookup else 0) | ((only_worker + 1) << 8)
     h = lib.hk_simulate(buf, len(plan), C.byref(c), engine.handle if engine is not None else None, flags)
     if not h:
-        raise RuntimeError(_lib.last_error())
+        cause = engine.take_pin_exchange_error() if engine is not None else None
+        raise RuntimeError(_lib.last_error()) from cause
     try:
         mc = _lib.MetricsC()
         lib.hk_run_metrics(h, C.byref(mc))
@@ -213,6 +214,15 @@ def sim_calls_csv(m: SimMetrics) -> str:
 
 def sim_trace_csv(m: SimMetrics) -> str:
     return m.trace_csv
+
+
+def worker_pins(plan: bytes, cfg: SimConfig, worker: int) -> List[List[int]]:
+    """The prefixes simulate() pins on `worker` (simulator.cpp:257-263): budget
+    = pin_capacity_frac x capacity; none when proactive pinning is off."""
+    if not cfg.proactive_pin:
+        return []
+    w = cfg.workers[worker]
+    return static_pin_prefixes(plan, worker, w.block, cfg.pin_threshold, int(cfg.pin_capacity_frac * w.capacity))
 
 
 def static_pin_prefixes(plan: bytes, worker: int, block: int, threshold: int, budget_tokens: int) -> List[List[int]]:
