@@ -936,6 +936,7 @@ __global__ void argmax_reduce_kernel(const float2* __restrict__ part, int n_tile
                 best = sv[w];
                 bi = si[w];
             }
+        if (bi == 0x7fffffff) bi = 0;  // all-NaN row: an in-range id (the embedding gather indexes with it)
         ids[t] = bi;
         if (slots) slot_last[slots[t]] = bi;
     }

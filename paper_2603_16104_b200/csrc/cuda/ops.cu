@@ -186,6 +186,7 @@ __global__ void argmax_kernel(const float* logits, int V, int32_t* ids, const in
                 best = sv[w];
                 bi = si[w];
             }
+        if (bi == 0x7fffffff) bi = 0;  // all-NaN row: an in-range id (the embedding gather indexes with it)
         ids[r] = bi;
         if (slots) slot_last[slots[r]] = bi;
     }
