@@ -71,8 +71,8 @@ __device__ __forceinline__ void stamp(const DecodeAttnArgs& a, int cta, int k) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         if (k == 6 || k == 9 || k == 10 || k == 11) t = clock64();  // fine-grained (cycles) chunk-1 stamps
-        a.trace[static_cast<size_t>(cta) * 16 + k] = t;
-        if (k == 0 || k == 5) a.trace[static_cast<size_t>(cta) * 16 + 14 + (k == 5)] = clock64();
+        a.trace[static_cast<size_t>(cta) * 24 + k] = t;
+        if (k == 0 || k == 5) a.trace[static_cast<size_t>(cta) * 24 + 22 + (k == 5)] = clock64();
     }
 }
 
@@ -700,13 +700,20 @@ __device__ __forceinline__ void merge16(const DecodeAttnArgs& a, int pair, int n
     const size_t base = (static_cast<size_t>(row) * a.H + head) * a.max_parts;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float M = -INFINITY, L = 0.f;
+    // the first batch's loads are issued together with the part count (they do
+    // not depend on it; unused slots are masked): one L2 round trip per row
+    float2 ml = sub < 8 ? __ldcg(&a.part_ml[base + sub]) : make_float2(-INFINITY, 0.f);
+    uint4 v[8];  // 8 bf16 dims of each of the batch's parts
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcg(reinterpret_cast<const uint4*>(part_bf16(a) + (base + k) * HD) + sub);
     for (int k0 = 0; k0 < a.max_parts; k0 += 8) {
         if (!__any_sync(full, k0 < np)) break;
-        const float2 ml = sub < 8 ? __ldcg(&a.part_ml[base + k0 + sub]) : make_float2(-INFINITY, 0.f);
-        uint4 v[8];  // 8 bf16 dims of each of the batch's parts
+        if (k0 > 0) {
+            ml = sub < 8 ? __ldcg(&a.part_ml[base + k0 + sub]) : make_float2(-INFINITY, 0.f);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-            v[k] = __ldcg(reinterpret_cast<const uint4*>(part_bf16(a) + (base + k0 + k) * HD) + sub);
+            for (int k = 0; k < 8; ++k)
+                v[k] = __ldcg(reinterpret_cast<const uint4*>(part_bf16(a) + (base + k0 + k) * HD) + sub);
+        }
         const bool mine = sub < 8 && k0 + sub < np;
         float mx = mine ? ml.x : -INFINITY;
 #pragma unroll
@@ -842,14 +849,15 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
     // it, all partials exist: the rows are merged by every SM in parallel.
     named_bar(2, DA_PV_WARPS * 32);
     const int tid = threadIdx.x;
+    if (warp == 0) stamp(a, blockIdx.x, 16);
     if (tid == 0) {
         __threadfence();
         atomicAdd(a.grid_arrive, 1);
         int seen;
         do {
-            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(a.grid_arrive) : "memory");
-            if (seen < static_cast<int>(gridDim.x)) __nanosleep(64);
+            asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(a.grid_arrive) : "memory");
         } while (seen < static_cast<int>(gridDim.x));
+        __threadfence();  // acquire: every CTA's partials are visible from here on
     }
     named_bar(2, DA_PV_WARPS * 32);
     if (warp == 0) stamp(a, blockIdx.x, 13);
@@ -857,6 +865,7 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
     for (int pb = blockIdx.x * (DA_PV_WARPS * 2); pb < n_pairs; pb += gridDim.x * (DA_PV_WARPS * 2))
         merge16(a, pb + (tid >> 4), n_pairs);
     named_bar(2, DA_PV_WARPS * 32);
+    if (warp == 0) stamp(a, blockIdx.x, 17);
     // the last CTA out rewinds the queue and the barrier for the next launch
     if (tid == 0 && atomicAdd(a.pv_done, 1) == static_cast<int>(gridDim.x) - 1) {
         *a.pv_next = 0;

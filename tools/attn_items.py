@@ -40,7 +40,7 @@ lib.hkx_decode_attention_trace(C.c_void_p(buf.data_ptr()))
 run(case)
 lib.hkx_decode_attention_trace(None)
 t = buf.cpu().numpy().astype(np.float64)
-cta = t[:148 * 16].reshape(148, 16)
+cta = t[:148 * 24].reshape(148, 24)
 items = t[32768:32768 + 6000 * 4].reshape(-1, 4)
 items = items[items[:, 0] > 0]
 t0 = cta[:, 0][cta[:, 0] > 0].min()

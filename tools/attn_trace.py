@@ -33,7 +33,7 @@ buf = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
 _lib.load().hkx_decode_attention_trace(C.c_void_p(buf.data_ptr()))
 run(case)
 _lib.load().hkx_decode_attention_trace(None)
-t = buf.view(-1, 16).cpu().numpy().astype(np.float64)
+t = buf[:148 * 24].view(-1, 24).cpu().numpy().astype(np.float64)  # [CTA][24] stamps
 n_sh = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 sh = t[:n_sh]
 rest = t[n_sh:][t[n_sh:, 0] > 0]
@@ -51,10 +51,13 @@ for idx, name in order:
     prev = (idx, name)
 print(f"  queue loop ends: shared CTAs {us(sh[:,12]).min():.1f}..{us(sh[:,12]).max():.1f} us, "
       f"queue-only CTAs {us(rest[:,12]).min() if len(rest) else 0:.1f}..{us(rest[:,12]).max() if len(rest) else 0:.1f} us")
-mhz = (sh[:, 15] - sh[:, 14]) / (sh[:, 5] - sh[:, 0]) * 1e3
+mhz = (sh[:, 23] - sh[:, 22]) / (sh[:, 5] - sh[:, 0]) * 1e3
 print(f"  SM clock inside shared CTAs: {mhz.mean():.0f} MHz; shared phase ends {us(sh[:,5]).min():.1f}..{us(sh[:,5]).max():.1f} us")
 # chunk 1 of the softmax warps (thread 0): S1 ready (9) -> row max exchanged (10) -> exps packed (11) -> PV(0) done (6)
 c1 = [(9, "O done"), (10, "l exchanged"), (11, "staged"), (6, "bulk stored")]
 for (i0, n0), (i1, n1) in zip(c1, c1[1:]):
     d = sh[:, i1] - sh[:, i0]
     print(f"  c1 {n0:>14s} -> {n1:<14s} mean {d.mean():8.0f} cycles  max {d.max():8.0f}")
+allc = t[t[:, 0] > 0]
+print(f"  tail: queue end {us(allc[:,12]).max():.2f}, grid barrier entered {us(allc[:,16]).min():.2f}..{us(allc[:,16]).max():.2f}, "
+      f"merge start {us(allc[:,13]).min():.2f}..{us(allc[:,13]).max():.2f}, merge end {us(allc[:,17]).min():.2f}..{us(allc[:,17]).max():.2f} us")
