@@ -142,9 +142,6 @@ struct hk_engine {
     size_t ws_floats = 0;
     float* pbuf = nullptr;  // fp32 split-K partials of QKV / O / down GEMMs
     size_t pbuf_floats = 0;
-    // residual + RMSNorm folded into the O / down GEMMs (decode steps, bf16)
-    float *ssq_o = nullptr, *ssq_d = nullptr, *ssq_slice = nullptr;
-    int32_t* rn_ctr = nullptr;
     void* hs = nullptr;     // normalized rows of sampled tokens (LM head input)
     float2* amax = nullptr; // per (vocab tile, row) argmax partials
     float* part_o = nullptr;
@@ -177,7 +174,6 @@ struct hk_engine {
     int pin_role = 0;
     hk_pin_exchange_fn pin_fn = nullptr;
     void* pin_user = nullptr;
-    size_t pf_rms_bytes = 0;     // add_rmsnorm pulls this many bytes of the next GEMM's weights into L2
     void drop_graphs() {
         for (auto& [k, g] : graphs) cudaGraphExecDestroy(g.exec);
         graphs.clear();
@@ -299,7 +295,6 @@ hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m
     // opt-in: measured -2% on configs[1] (the prefetch traffic slows the attention more
     // than the O projection gains; profiles/r1_attention.txt)
     l2_prefetch_o = std::getenv("HK_L2_PREFETCH_O") != nullptr;
-    pf_rms_bytes = std::getenv("HK_PF_RMS_MB") ? static_cast<size_t>(std::atof(std::getenv("HK_PF_RMS_MB")) * 1048576) : 0;
     hkd::g_pdl = std::getenv("HK_NO_PDL") == nullptr;
     init_weights();
 
@@ -363,14 +358,6 @@ hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m
     ws = dalloc<float>(ws_floats);
     pbuf_floats = std::max(static_cast<size_t>(maxT) * std::max(QKV, d) * 2, static_cast<size_t>(16) * 512 * std::max(QKV, d));
     pbuf = dalloc<float>(pbuf_floats);
-    {
-        const int tiles = (d + 127) / 128;
-        ssq_o = dalloc<float>(static_cast<size_t>(tiles) * 64);
-        ssq_d = dalloc<float>(static_cast<size_t>(tiles) * 64);
-        ssq_slice = dalloc<float>(static_cast<size_t>(tiles) * 8 * 64);
-        rn_ctr = dalloc<int32_t>(static_cast<size_t>(tiles) * 64);  // two counters per tile, 128 B apart
-        HK_CUDA(cudaMemsetAsync(rn_ctr, 0, static_cast<size_t>(tiles) * 64 * sizeof(int32_t), st));
-    }
     if (!f32) hkd::gemm_streamk_reserve(std::max((V + 127) / 128, 4096), 64);
     hs = dalloc<uint8_t>(static_cast<size_t>(maxS) * d * esz);
     amax = dalloc<float2>(static_cast<size_t>((V + 127) / 128) * maxS);
@@ -752,35 +739,13 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         clock.end(c, st, static_cast<double>(N) * K * esz + static_cast<double>(rows) * K * esz);
         return sp;
     };
-    // decode steps (bf16): the O / down GEMMs also reduce their split-K tiles into
-    // the residual and emit u = x * w_norm + per-tile sums of squares; the next
-    // kernels (SwiGLU epilogue / qkv_rope_kv) apply 1 / rms. No norm kernels.
-    const bool rn_step = !f32 && T <= 64 && !clock.enabled;
-    bool h_scaled = false;  // h holds u = x * w (scale pending, sums of squares in ssq_d)
     for (int l = 0; l < L; ++l) {
         const LayerW& lw = layers[static_cast<size_t>(l)];
         const hkd::RopeArgs ra{qkv, f32, T, H, Hkv, hd, d_pos, d_kvw, d_ptab, d_pages, rope, kv_layer(w, l), block};
-        // bf16: one kernel (cluster split-K + bias/RoPE/KV-write epilogue); fp32 or
-        // unsupported shapes: split-K partials + the qkv_rope_kv consumer
-        int fused = -1;
-        if (!f32 && !h_scaled) {
-            ck = clock.begin(0, st);
-            if (dbl("qkv")) hkd::gemm_bf16_qkv_rope(static_cast<const bf16*>(lw.wqkv), static_cast<const bf16*>(h), QKV, d,
-                                                    static_cast<const bf16*>(lw.bqkv), ra, st);
-            fused = hkd::gemm_bf16_qkv_rope(static_cast<const bf16*>(lw.wqkv), static_cast<const bf16*>(h), QKV, d,
-                                            static_cast<const bf16*>(lw.bqkv), ra, st);
-            clock.end(ck, st, static_cast<double>(QKV) * d * esz + static_cast<double>(T) * d * esz);
-        }
-        if (fused < 0) {
+        {
             if (dbl("qkv")) gemm(lw.wqkv, h, QKV, d, T, hkd::kEpiPartial, pbuf, QKV);
             const int sp = gemm(lw.wqkv, h, QKV, d, T, hkd::kEpiPartial, pbuf, QKV);
-            hkd::QkvArgs qa{pbuf, sp, lw.bqkv, ra};
-            if (h_scaled) {
-                qa.in_ssq = ssq_d;
-                qa.n_ssq = (d + 127) / 128;
-                qa.eps = eps;
-                qa.d = d;
-            }
+            const hkd::QkvArgs qa{pbuf, sp, lw.bqkv, ra};
             ck = clock.begin(5, st);
             if (dbl("rope")) hkd::qkv_rope_kv(qa, st);
             if (!skip("rope")) hkd::qkv_rope_kv(qa, st);
@@ -828,23 +793,11 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
             }
         }
         if (dbl("o")) gemm(lw.wo, attn, d, H * hd, T, hkd::kEpiPartial, pbuf, d);
-        const int o_rn = rn_step ? hkd::gemm_bf16_resid_norm(static_cast<const bf16*>(lw.wo), static_cast<const bf16*>(attn),
-                                                             d, H * hd, T, pbuf, pbuf_floats,
-                                                             hkd::ResidNormArgs{x, static_cast<const bf16*>(lw.mlp_norm),
-                                                                                static_cast<bf16*>(h), ssq_o, ssq_slice,
-                                                                                rn_ctr},
-                                                             st)
-                                 : -1;
-        int sp = 0;
-        if (o_rn < 0) {
-            sp = gemm(lw.wo, attn, d, H * hd, T, hkd::kEpiPartial, pbuf, d);
-            ck = clock.begin(5, st);
-            if (dbl("rms")) hkd::add_rmsnorm(pbuf, 0, x, lw.mlp_norm, f32, T, d, eps, h, nullptr, nullptr, st);
-            if (!skip("rms"))
-                hkd::add_rmsnorm(pbuf, sp, x, lw.mlp_norm, f32, T, d, eps, h, nullptr, nullptr, st, lw.wgu,
-                                 std::min(pf_rms_bytes, static_cast<size_t>(2) * F * d * esz));
-            clock.end(ck, st);
-        }
+        int sp = gemm(lw.wo, attn, d, H * hd, T, hkd::kEpiPartial, pbuf, d);
+        ck = clock.begin(5, st);
+        if (dbl("rms")) hkd::add_rmsnorm(pbuf, 0, x, lw.mlp_norm, f32, T, d, eps, h, nullptr, nullptr, st);
+        if (!skip("rms")) hkd::add_rmsnorm(pbuf, sp, x, lw.mlp_norm, f32, T, d, eps, h, nullptr, nullptr, st);
+        clock.end(ck, st);
         if (f32) {
             gemm(lw.wgu, h, 2 * F, d, T, hkd::kEpiStoreF32, gu, 2 * F);
             ck = clock.begin(5, st);
@@ -852,32 +805,15 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
             clock.end(ck, st);
         } else {
             if (dbl("gu")) gemm(lw.wgu, h, 2 * F, d, T, hkd::kEpiSwiGLU, act, F);
-            if (o_rn > 0)  // input rows u = x * w: the epilogue applies 1 / rms (sums of squares in ssq_o)
-                hkd::gemm_bf16_swiglu_scaled(static_cast<const bf16*>(lw.wgu), static_cast<const bf16*>(h), 2 * F, d, T,
-                                             act, F, ssq_o, (d + 127) / 128, eps, st);
-            else
-                gemm(lw.wgu, h, 2 * F, d, T, hkd::kEpiSwiGLU, act, F);  // SwiGLU fused in the epilogue
+            gemm(lw.wgu, h, 2 * F, d, T, hkd::kEpiSwiGLU, act, F);  // SwiGLU fused in the epilogue
         }
         if (dbl("down")) gemm(lw.wd, act, d, F, T, hkd::kEpiPartial, pbuf, d);
-        const bool last = l + 1 == L;
-        const int d_rn = rn_step && !last
-                             ? hkd::gemm_bf16_resid_norm(static_cast<const bf16*>(lw.wd), static_cast<const bf16*>(act), d,
-                                                         F, T, pbuf, pbuf_floats,
-                                                         hkd::ResidNormArgs{x,
-                                                                            static_cast<const bf16*>(
-                                                                                layers[static_cast<size_t>(l) + 1].attn_norm),
-                                                                            static_cast<bf16*>(h), ssq_d, ssq_slice, rn_ctr},
-                                                         st)
-                             : -1;
-        h_scaled = d_rn > 0;
-        if (d_rn > 0) continue;
         sp = gemm(lw.wd, act, d, F, T, hkd::kEpiPartial, pbuf, d);
+        const bool last = l + 1 == L;
         ck = clock.begin(5, st);
         if (last || !skip("rms"))
             hkd::add_rmsnorm(pbuf, sp, x, last ? final_norm : layers[static_cast<size_t>(l) + 1].attn_norm, f32, T, d,
-                             eps, h, last && S > 0 ? d_cmap : nullptr, last && S > 0 ? hs : nullptr, st,
-                             last ? nullptr : layers[static_cast<size_t>(l) + 1].wqkv,
-                             std::min(pf_rms_bytes, static_cast<size_t>(QKV) * d * esz));
+                             eps, h, last && S > 0 ? d_cmap : nullptr, last && S > 0 ? hs : nullptr, st);
         clock.end(ck, st);
     }
     if (S > 0) {

@@ -42,199 +42,14 @@ struct GemmParams {
     float* partial;
     int cluster;  // 1: the grid.z split-K CTAs form a cluster and reduce through DSMEM
     int skip_epi; // timing experiments only (HK_GEMM_DEBUG_SKIP_EPI): no output stores
-    RopeArgs rope; // kEpiQkvRope: the q/k/v rows and this layer's KV pages
-    int l2_pf;     // weight k-blocks prefetched into L2 before griddepcontrol.wait
-    unsigned long long* trace;  // debug (HK_GEMM_TRACE): [first CTA start, first wait done, ~last end] (atomicMin)
-    int rn_on;          // kEpiPartial + residual/RMSNorm tile reduction (gemm_bf16_resid_norm)
-    ResidNormArgs rn;
-    const float* in_ssq;  // kEpiSwiGLU: scale input rows by rsqrt(sum in_ssq / K + eps)
-    int n_ssq;
-    float in_eps;
+    unsigned long long* trace;  // debug (HK_GEMM_TRACE): [first CTA start, first wait done, ~last end,
+                                //  ~last main-loop end] (atomicMin)
 };
-
-__device__ __forceinline__ int ld_relaxed(const int32_t* p) {
-    int v;
-    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-// wait until *c >= n: relaxed polls with back-off (many CTAs poll while the
-// tile's last split still streams), then an acquire fence
-__device__ __forceinline__ void spin_until(const int32_t* c, int n) {
-    while (ld_relaxed(c) < n) __nanosleep(20);
-    __threadfence();
-}
-
-// Residual + RMSNorm tail of a split-K tile (all 128 threads; partials of this
-// CTA already stored). See ResidNormArgs.
-template <int BN>
-__device__ __forceinline__ void resid_norm_tile(const GemmParams& p, int m0, int n0) {
-    const int s = static_cast<int>(gridDim.z), z = static_cast<int>(blockIdx.z);
-    const int tile = static_cast<int>(blockIdx.x);
-    const int ntiles = static_cast<int>(gridDim.x);
-    const ResidNormArgs& rn = p.rn;
-    int32_t* c0 = rn.ctr + 64 * tile;  // each counter on its own 128-byte line (polled by the tile's CTAs)
-    // arrival: bar.sync orders the CTA's partial stores before thread 0's
-    // fence + atomic (cumulative release); the acquire below pairs with it
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(c0, 1);
-        spin_until(c0, s);
-    }
-    __syncthreads();
-    const int SL = BM / s, nq = SL / 4;  // rows (features) of this CTA's slice, float4 groups per token
-    const int rows = min(BN, p.T - n0);
-    const size_t pstride = static_cast<size_t>(p.T) * p.N;
-    // two items per thread per pass, every load of both issued before any use
-    // (one L2 round trip per pass); nq is a power of two <= 16, so the nq
-    // lanes of a token are adjacent in one warp
-    for (int base = 0; base < nq * rows; base += 2 * blockDim.x) {
-        float4 v[2], b[2][8];
-        uint2 wv[2];
-        bool ok[2];
-        int tt[2], cc[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int idx = base + h * static_cast<int>(blockDim.x) + static_cast<int>(threadIdx.x);
-            ok[h] = idx < nq * rows;
-            tt[h] = n0 + (ok[h] ? idx / nq : 0);
-            cc[h] = m0 + z * SL + 4 * (idx % nq);
-            const size_t o = static_cast<size_t>(tt[h]) * p.N + cc[h];
-            v[h] = ok[h] ? *reinterpret_cast<const float4*>(rn.x + o) : make_float4(0.f, 0.f, 0.f, 0.f);
-            wv[h] = ok[h] ? *reinterpret_cast<const uint2*>(rn.w + cc[h]) : make_uint2(0u, 0u);
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                b[h][k] = (ok[h] && k < s) ? __ldcg(reinterpret_cast<const float4*>(p.partial + k * pstride + o))
-                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (k < s) {  // split order, as add_rmsnorm: deterministic
-                    v[h].x += b[h][k].x;
-                    v[h].y += b[h][k].y;
-                    v[h].z += b[h][k].z;
-                    v[h].w += b[h][k].w;
-                }
-            float ss = v[h].x * v[h].x + v[h].y * v[h].y + v[h].z * v[h].z + v[h].w * v[h].w;
-            if (ok[h]) {
-                const size_t o = static_cast<size_t>(tt[h]) * p.N + cc[h];
-                *reinterpret_cast<float4*>(rn.x + o) = v[h];
-                const __nv_bfloat162 w01 = *reinterpret_cast<const __nv_bfloat162*>(&wv[h].x);
-                const __nv_bfloat162 w23 = *reinterpret_cast<const __nv_bfloat162*>(&wv[h].y);
-                uint2 pk;
-                pk.x = pack_bf16x2(v[h].x * __low2float(w01), v[h].y * __high2float(w01));
-                pk.y = pack_bf16x2(v[h].z * __low2float(w23), v[h].w * __high2float(w23));
-                *reinterpret_cast<uint2*>(rn.u + o) = pk;
-            }
-#pragma unroll
-            for (int o = 1; o < 16; o <<= 1)
-                if (o < nq) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            if (ok[h] && (threadIdx.x % nq) == 0) rn.ssq_slice[(static_cast<size_t>(tt[h]) * ntiles + tile) * 8 + z] = ss;
-        }
-    }
-    __syncthreads();
-    int32_t* c1 = c0 + 32;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(c1, 1);
-    }
-    if (z != 0) return;
-    if (threadIdx.x == 0) spin_until(c1, s);
-    __syncthreads();
-    // ssq[t][tile] = sum of the tile's slices (split order); [T][tiles] so a
-    // consumer reads a token's tiles contiguously
-    for (int t = n0 + static_cast<int>(threadIdx.x); t < n0 + rows; t += blockDim.x) {
-        const float4* q = reinterpret_cast<const float4*>(rn.ssq_slice + (static_cast<size_t>(t) * ntiles + tile) * 8);
-        const float4 lo = __ldcg(q), hi = __ldcg(q + 1);
-        const float e[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-        float a = 0.f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (k < s) a += e[k];
-        rn.ssq[static_cast<size_t>(t) * ntiles + tile] = a;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {  // every split CTA has passed both counters: rewind them for the next launch
-        *c0 = 0;
-        *c1 = 0;
-    }
-}
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
-}
-
-// kEpiQkvRope (cluster split-K only): the tile is one 128-row head of the
-// fused QKV projection (BM == head_dim). Rank r of the s-CTA cluster owns
-// rotation pairs (i, i + 64), i in [r*ceil(64/s), ...), for all BN tokens: it
-// sums the s peers' fp32 tiles through DSMEM in rank (= split) order, adds the
-// bias, rounds to bf16, rotates q/k heads (RoPE on the stored bf16 values, as
-// qkv_rope_kv_kernel and the oracle do) and writes the q/k/v row plus, for
-// k/v heads of tokens with kvw set, the token's slot of its KV page. Replaces
-// the partial round trip through L2 and the separate qkv_rope_kv launch.
-template <int BN>
-__device__ __forceinline__ void qkv_rope_epilogue(const GemmParams& p, const float* tile, cg::cluster_group& cl, int s,
-                                                  int rank, int n0) {
-    constexpr int kHalf = BM / 2;
-    const RopeArgs& r = p.rope;
-    const int hh = static_cast<int>(blockIdx.x);
-    const bool is_v = hh >= r.H + r.Hkv;
-    const int per = (kHalf + s - 1) / s;
-    const int i0 = min(kHalf, rank * per), i1 = min(kHalf, i0 + per);
-    const int ni = i1 - i0;
-    if (ni <= 0) return;
-    const float* peer[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) peer[q] = cl.map_shared_rank(tile, q < s ? q : 0);
-    bf16* qkv = static_cast<bf16*>(r.qkv);
-    bf16* kv = static_cast<bf16*>(r.kv_layer);
-    const int c0 = hh * BM;
-    for (int idx = threadIdx.x; idx < ni * BN; idx += blockDim.x) {
-        const int i = i0 + idx % ni, c = idx / ni;
-        const int n = n0 + c;
-        if (n >= p.T) continue;
-        float v0[8], v1[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-            if (q < s) {
-                v0[q] = peer[q][c * BM + i];
-                v1[q] = peer[q][c * BM + i + kHalf];
-            }
-        float x0 = 0.f, x1 = 0.f;
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-            if (q < s) {  // fixed split order: deterministic
-                x0 += v0[q];
-                x1 += v1[q];
-            }
-        if (p.bias) {
-            x0 += bf2f(p.bias[c0 + i]);
-            x1 += bf2f(p.bias[c0 + i + kHalf]);
-        }
-        bf16 b0 = f2bf(x0), b1 = f2bf(x1);
-        const int pos = r.pos[n];
-        if (!is_v) {
-            const float y0 = bf2f(b0), y1 = bf2f(b1);
-            const float2 cs = r.rope[static_cast<size_t>(pos) * kHalf + i];
-            b0 = f2bf(y0 * cs.x - y1 * cs.y);
-            b1 = f2bf(y1 * cs.x + y0 * cs.y);
-        }
-        bf16* row = qkv + static_cast<size_t>(n) * p.N + c0;
-        row[i] = b0;
-        row[i + kHalf] = b1;
-        if (hh >= r.H && r.kvw[n]) {
-            const int page = r.pages[r.ptab[n] + pos / r.block];
-            const int kvh = is_v ? hh - r.H - r.Hkv : hh - r.H;
-            bf16* dst = kv + ((static_cast<size_t>(page) * 2 + (is_v ? 1 : 0)) * r.Hkv + kvh) * r.block * BM +
-                        static_cast<size_t>(pos % r.block) * BM;
-            dst[i] = b0;
-            dst[i + kHalf] = b1;
-        }
-    }
 }
 
 template <int BN, int STAGES>
@@ -289,9 +104,6 @@ __global__ void __launch_bounds__(128, 1)
                 mbar_expect_tx(&full[i], A_BYTES + B_BYTES);
                 tma_load_2d_hint(sA + i * A_BYTES, &tmW, &full[i], (kb0 + i) * BK, m0, pol_w);
             }
-            // ...and pull the next weight blocks into L2 while the predecessor
-            // (often a latency-bound row kernel) still runs
-            for (int i = pre; i < min(nkb, pre + p.l2_pf); ++i) tma_prefetch_2d(&tmW, (kb0 + i) * BK, m0);
             pdl_wait();
             if (p.trace) atomicMin(&p.trace[1], gtimer());
             for (int i = 0; i < pre; ++i) tma_load_2d_hint(sB + i * B_BYTES, &tmX, &full[i], (kb0 + i) * BK, n0, pol_x);
@@ -353,10 +165,9 @@ __global__ void __launch_bounds__(128, 1)
         const int nq = (r1 - r0) / 4;                  // float4 row groups
         const float4* peer[8];
         cg::cluster_group cl = cg::this_cluster();
-        if (p.epi == kEpiQkvRope) qkv_rope_epilogue<BN>(p, tile, cl, s, rank, n0);
 #pragma unroll
         for (int q = 0; q < 8; ++q) peer[q] = reinterpret_cast<const float4*>(cl.map_shared_rank(tile, q < s ? q : 0));
-        for (int idx = threadIdx.x; p.epi != kEpiQkvRope && idx < nq * BN; idx += blockDim.x) {
+        for (int idx = threadIdx.x; idx < nq * BN; idx += blockDim.x) {
             const int rr = r0 + 4 * (idx % nq), c = idx / nq;
             const int off4 = (c * BM + rr) / 4;
             float4 v[8];
@@ -409,35 +220,13 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
             for (int j = 0; j < 8; ++j) xs[row * (BN + 1) + c + j] = v[j];
         }
-        const int nt = min(BN, p.T - n0);
-        float* rs = xs + BM * (BN + 1);  // [BN] per-token input scale
-        if (p.in_ssq) {
-            // ssq is [T][n_ssq]: two threads per token, each a half of the tiles
-            // as independent float4 loads, combined in a fixed order
-            const int c = threadIdx.x >> 1, hf = threadIdx.x & 1;
-            float a = 0.f;
-            if (c < nt) {
-                const float4* q = reinterpret_cast<const float4*>(p.in_ssq + static_cast<size_t>(n0 + c) * p.n_ssq);
-                const int n4 = p.n_ssq / 4, h0 = hf * ((n4 + 1) / 2), h1 = hf ? n4 : (n4 + 1) / 2;
-                float4 v[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = h0 + i < h1 ? __ldcg(q + h0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) a += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-            }
-            a += __shfl_xor_sync(0xffffffffu, a, 1);
-            if (c < nt && hf == 0) rs[c] = rsqrtf(a / static_cast<float>(p.K) + p.in_eps);
-        }
         __syncthreads();
+        const int nt = min(BN, p.T - n0);
         for (int idx = threadIdx.x; idx < 64 * nt; idx += blockDim.x) {
             const int r = idx & 63, c = idx >> 6;
             const int f = blockIdx.x * 64 + r;  // output feature
             if (blockIdx.x * BM + r < p.N) {
-                float g = xs[r * (BN + 1) + c], u = xs[(r + 64) * (BN + 1) + c];
-                if (p.in_ssq) {
-                    g *= rs[c];
-                    u *= rs[c];
-                }
+                const float g = xs[r * (BN + 1) + c], u = xs[(r + 64) * (BN + 1) + c];
                 static_cast<bf16*>(p.out)[static_cast<size_t>(n0 + c) * p.ldo + f] =
                     f2bf(__fdividef(g, 1.0f + __expf(-g)) * u);
             }
@@ -536,7 +325,6 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     if (warp == 2) tmem_dealloc(tmem, TMEM_COLS);
     if (p.trace && threadIdx.x == 0) atomicMin(&p.trace[3], ~gtimer());  // last CTA to finish its main loop + stores
-    if (p.rn_on) resid_norm_tile<BN>(p, m0, n0);
     if (p.trace && threadIdx.x == 0) atomicMin(&p.trace[2], ~gtimer());
 }
 
@@ -721,12 +509,6 @@ int gemm_trace_dump(const char* path) {
     return g_gtrace.n;
 }
 
-// HK_GEMM_L2PF=<k-blocks>: weight blocks per CTA prefetched into L2 before griddepcontrol.wait
-static int gemm_l2_prefetch_blocks() {
-    static const int v = std::getenv("HK_GEMM_L2PF") ? std::atoi(std::getenv("HK_GEMM_L2PF")) : 0;
-    return v;
-}
-
 int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* out, int ldo, const bf16* bias,
               float* workspace, size_t workspace_floats, cudaStream_t st, int force_splits, int max_splits) {
     if (T <= 0) return 0;
@@ -787,7 +569,6 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
     static const int skip_epi = std::getenv("HK_GEMM_DEBUG_SKIP_EPI") ? 1 : 0;
     GemmParams p{N, K, T, kb, kbps, via_ws ? kEpiPartial : epi, out, ldo, bias,
                  epi == kEpiPartial ? static_cast<float*>(out) : workspace, cluster ? 1 : 0, skip_epi};
-    p.l2_pf = gemm_l2_prefetch_blocks();
     p.trace = gemm_trace_slot(N, K, T, splits, mt * nt * splits);
     const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
     const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
@@ -805,95 +586,6 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
         const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 4096));
         splitk_reduce_kernel<<<blocks, 256, 0, st>>>(workspace, splits, T, N, epi, out, ldo, bias);
         HK_LAUNCHED(1);
-    }
-    return splits;
-}
-
-int gemm_bf16_resid_norm(const bf16* W, const bf16* X, int N, int K, int T, float* partial, size_t partial_floats,
-                         const ResidNormArgs& rn, cudaStream_t st) {
-    // opt-in (HK_RESID_FUSED=1): measured slower on B200 — the two counter
-    // barriers wait behind the fences on the tile's 8.4 MB partial-store burst
-    // (tail 8.5 us, 6.3 us with the barriers alone) vs ~5 us for the separate
-    // add_rmsnorm kernel + its PDL hand-off (profiles/r1_marginal_costs.txt)
-    static const bool on = std::getenv("HK_RESID_FUSED") != nullptr;
-    if (!on || T <= 0 || T > 64 || N % BM != 0 || K % BK != 0 || (N / BM) % 4 != 0 || N / BM > 64) return -1;
-    const int BN = T <= 16 ? 16 : (T <= 32 ? 32 : 64);
-    const int mt = N / BM, kb = K / BK;
-    int splits = 1;
-    if (mt * 2 <= 2 * g_num_sms) splits = std::min(8, 2 * g_num_sms / mt);
-    splits = std::min(splits, std::max(1, kb / 4));
-    while (splits & (splits - 1)) --splits;  // 2, 4 or 8: a slice of 128 / splits rows is whole float4 groups
-    if (splits < 2) return -1;
-    const int kbps = (kb + splits - 1) / splits;
-    if ((kb + kbps - 1) / kbps != splits) return -1;          // no empty split
-    if (mt * splits > 2 * g_num_sms) return -1;              // the tile's split CTAs wait for each other: co-resident
-    if (static_cast<size_t>(splits) * T * N > partial_floats) return -1;
-    GemmParams p{N, K, T, kb, kbps, kEpiPartial, partial, N, nullptr, partial, 0, 0};
-    p.rn_on = 1;
-    p.rn = rn;
-    p.trace = gemm_trace_slot(N, K, T, splits, mt * splits);
-    const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
-    const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
-    const dim3 grid(mt, 1, splits);
-    switch (BN) {
-        case 16: launch_tc<16, 4>(tw, tx, p, grid, st); break;
-        case 32: launch_tc<32, 4>(tw, tx, p, grid, st); break;
-        default: launch_tc<64, 4>(tw, tx, p, grid, st); break;
-    }
-    return splits;
-}
-
-void gemm_bf16_swiglu_scaled(const bf16* W, const bf16* X, int N, int K, int T, void* out, int ldo, const float* in_ssq,
-                             int n_ssq, float eps, cudaStream_t st) {
-    if (T <= 0) return;
-    if (K % BK != 0) throw std::runtime_error("gemm_bf16_swiglu_scaled: K must be a multiple of 64");
-    const int BN = T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256;
-    const int mt = (N + BM - 1) / BM, nt = (T + BN - 1) / BN, kb = K / BK;
-    GemmParams p{N, K, T, kb, kb, kEpiSwiGLU, out, ldo, nullptr, nullptr, 0, 0};
-    p.in_ssq = in_ssq;
-    p.n_ssq = n_ssq;
-    p.in_eps = eps;
-    p.trace = gemm_trace_slot(N, K, T, 1, mt * nt);
-    const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
-    const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
-    const dim3 grid(mt, nt, 1);
-    switch (BN) {
-        case 16: launch_tc<16, 4>(tw, tx, p, grid, st); break;
-        case 32: launch_tc<32, 4>(tw, tx, p, grid, st); break;
-        case 64: launch_tc<64, 4>(tw, tx, p, grid, st); break;
-        case 128: launch_tc<128, 4>(tw, tx, p, grid, st); break;
-        default: launch_tc<256, 4>(tw, tx, p, grid, st); break;
-    }
-}
-
-int gemm_bf16_qkv_rope(const bf16* W, const bf16* X, int N, int K, const bf16* bias, const RopeArgs& r,
-                       cudaStream_t st) {
-    const int T = r.T;
-    if (T <= 0) return 0;
-    if (r.f32 || r.hd != BM || N != (r.H + 2 * r.Hkv) * BM || K % BK != 0) return -1;
-    // opt-in (HK_QKV_FUSED=1): measured slower in the decode pipeline on B200 than
-    // L2 partials + qkv_rope_kv (c2 bench 1163 vs 1083 ms/run): the 6-CTA
-    // clusters schedule worse than independent split-K CTAs (profiles/r1_marginal_costs.txt)
-    static const bool on = std::getenv("HK_QKV_FUSED") != nullptr;
-    if (!on) return -1;
-    const int BN = T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256;
-    const int mt = N / BM, nt = (T + BN - 1) / BN, kb = K / BK;
-    int splits = 1;
-    const int slots = BN <= 64 ? 2 * g_num_sms : g_num_sms;
-    if (mt * nt * 2 <= slots) splits = std::min(8, slots / (mt * nt));
-    splits = std::min(splits, std::max(1, kb / 4));
-    const int kbps = (kb + splits - 1) / splits;
-    splits = (kb + kbps - 1) / kbps;
-    GemmParams p{N, K, T, kb, kbps, kEpiQkvRope, nullptr, N, bias, nullptr, 1, 0, r, gemm_l2_prefetch_blocks()};
-    const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
-    const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
-    dim3 grid(mt, nt, splits);
-    switch (BN) {
-        case 16: launch_tc<16, 4>(tw, tx, p, grid, st); break;
-        case 32: launch_tc<32, 4>(tw, tx, p, grid, st); break;
-        case 64: launch_tc<64, 4>(tw, tx, p, grid, st); break;
-        case 128: launch_tc<128, 4>(tw, tx, p, grid, st); break;
-        default: launch_tc<256, 4>(tw, tx, p, grid, st); break;
     }
     return splits;
 }

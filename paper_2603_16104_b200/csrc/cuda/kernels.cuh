@@ -14,8 +14,7 @@ namespace hkd {
 // kEpiSwiGLU expects W rows interleaved per 128-row tile as [64 gate | 64 up]
 // and writes silu(gate) * up as bf16 [T][N/2]; kEpiArgmax writes per-(tile,
 // token) (max, argmax) pairs [N/128][T] for argmax_reduce.
-enum : int { kEpiStoreBf16 = 0, kEpiAddF32 = 1, kEpiStoreF32 = 2, kEpiPartial = 3, kEpiSwiGLU = 4, kEpiArgmax = 5,
-       kEpiQkvRope = 6 };
+enum : int { kEpiStoreBf16 = 0, kEpiAddF32 = 1, kEpiStoreF32 = 2, kEpiPartial = 3, kEpiSwiGLU = 4, kEpiArgmax = 5 };
 extern int g_num_sms;
 extern unsigned long long g_launches;  // kernels launched by this library (all launchers count)
 
@@ -66,37 +65,6 @@ struct RopeArgs {
     int block;
 };
 void rope_kv_write(const RopeArgs& a, cudaStream_t st);
-// Residual + RMSNorm folded into a split-K GEMM (decode, T <= 64, bf16): the
-// split CTAs of a 128-row tile meet at a counter (all CTAs are co-resident:
-// mt * splits <= 2 CTAs per SM), each reduces 128/splits rows of the tile in
-// split order, adds them to the fp32 residual x, writes u = bf16(x * w) (the
-// next GEMM's input, NOT yet scaled by 1/rms) and per-token sums of squares;
-// split 0 folds them into ssq[tile][t]. Consumers scale by
-// rsqrt(sum_tiles ssq / d + eps) (qkv_rope_kv, the SwiGLU epilogue).
-struct ResidNormArgs {
-    float* x;           // [T][N] fp32 residual stream (in/out)
-    const bf16* w;      // [N] norm weight
-    bf16* u;            // [T][N] out
-    float* ssq;         // [T][N / 128] out (a token's tiles contiguous)
-    float* ssq_slice;   // scratch [T][N / 128][8]
-    int32_t* ctr;       // [N / 128][64] (two counters per tile, 128 B apart), zero between launches
-};
-// Returns the split count used (>= 2), or -1 when not applicable (caller falls
-// back to kEpiPartial + add_rmsnorm). `partial` holds splits * T * N floats.
-int gemm_bf16_resid_norm(const bf16* W, const bf16* X, int N, int K, int T, float* partial, size_t partial_floats,
-                         const ResidNormArgs& rn, cudaStream_t st);
-// The SwiGLU GEMM with its input rows scaled by rsqrt(sum_i in_ssq[t][i] / K + eps)
-// (i < n_ssq) — the consumer side of gemm_bf16_resid_norm.
-void gemm_bf16_swiglu_scaled(const bf16* W, const bf16* X, int N, int K, int T, void* out, int ldo, const float* in_ssq,
-                             int n_ssq, float eps, cudaStream_t st);
-
-// Fused QKV projection (bf16, head_dim 128): split-K CTAs of a cluster reduce
-// through DSMEM and apply bias + RoPE + the K/V page write in the epilogue
-// (the result of gemm_bf16 kEpiPartial followed by qkv_rope_kv, one kernel).
-// Returns the split count, or -1 when the shape is not supported (caller
-// falls back to the two-kernel path).
-int gemm_bf16_qkv_rope(const bf16* W, const bf16* X, int N, int K, const bf16* bias, const RopeArgs& r,
-                       cudaStream_t st);
 void swiglu(const void* gu, bool f32, int T, int F, void* out, cudaStream_t st);
 // gate/up weights are stored with rows interleaved per 128-row tile ([64 gate | 64 up]);
 // init maps the physical index back to the logical (gate | up) index of the oracle.
@@ -110,17 +78,12 @@ struct QkvArgs {
     int splits;
     const void* bias;       // [QKV] or null
     RopeArgs r;             // r.qkv receives the rotated q (and raw k, v) rows
-    const float* in_ssq = nullptr;  // input rows were u = x * w: scale by rsqrt(sum ssq / d + eps) first
-    int n_ssq = 0;
-    float eps = 0.f;
-    int d = 0;
 };
 void qkv_rope_kv(const QkvArgs& a, cudaStream_t st);
 // Split-K consumer: x[t] += sum_s part[s][t]; h[t] = rmsnorm(x[t]) * w; rows with
 // cmap[t] >= 0 are also written to hc[cmap[t]] (compact rows for the LM head).
-// pf / pf_bytes: optional L2 prefetch of the next GEMM's weights (bf16 path)
 void add_rmsnorm(const float* part, int splits, float* x, const void* w, bool f32, int T, int d, float eps, void* h,
-                 const int32_t* cmap, void* hc, cudaStream_t st, const void* pf = nullptr, size_t pf_bytes = 0);
+                 const int32_t* cmap, void* hc, cudaStream_t st);
 // ids[r] = argmax_v logits[r][v] (lowest index on ties); also slot_last[slots[r]] = ids[r]
 void argmax_rows(const float* logits, int R, int V, int32_t* ids, const int32_t* slots, int32_t* slot_last,
                  cudaStream_t st);

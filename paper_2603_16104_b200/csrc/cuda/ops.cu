@@ -229,17 +229,6 @@ __global__ void qkv_rope_kv_kernel(QkvArgs a) {
     pdl_wait();
     const RopeArgs& r = a.r;
     const int t = blockIdx.y;
-    // input rows were u = x * w (gemm_bf16_resid_norm): this token's 1 / rms
-    __shared__ float s_inv;
-    if (a.in_ssq) {
-        if (threadIdx.x < 32) {
-            float v = 0.f;
-            for (int i = threadIdx.x; i < a.n_ssq; i += 32) v += a.in_ssq[static_cast<size_t>(t) * a.n_ssq + i];
-            v = warp_sum(v);
-            if (threadIdx.x == 0) s_inv = rsqrtf(v / static_cast<float>(a.d) + a.eps);
-        }
-        __syncthreads();
-    }
     const int half = r.hd / 2;
     const int n_rot = (r.H + r.Hkv) * half;   // (i, i + half) pairs of q and k heads
     const int n_v = r.Hkv * half;             // v handled as (2j, 2j + 1) pairs
@@ -279,10 +268,6 @@ __global__ void qkv_rope_kv_kernel(QkvArgs a) {
             x0 += p0[s];
             x1 += p1[s];
         }
-    }
-    if (a.in_ssq) {
-        x0 *= s_inv;
-        x1 *= s_inv;
     }
     if (a.bias) {
         if (sizeof(T) == 4) {
@@ -406,8 +391,7 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(const float* __restric
 template <int VPT>
 __global__ void __launch_bounds__(1024) add_rmsnorm_row_kernel(const float* __restrict__ part, int splits, float* x,
                                                                const bf16* __restrict__ w, int T_, int d, float eps,
-                                                               bf16* h, const int32_t* __restrict__ cmap, bf16* hc,
-                                                               const char* pf, unsigned long long pf_bytes) {
+                                                               bf16* h, const int32_t* __restrict__ cmap, bf16* hc) {
     pdl_trigger();
     const int t = blockIdx.x;
     const int n4 = d / 4;
@@ -418,15 +402,6 @@ __global__ void __launch_bounds__(1024) add_rmsnorm_row_kernel(const float* __re
         wv[j] = i < n4 ? __ldg(reinterpret_cast<const uint2*>(w) + i) : make_uint2(0u, 0u);
     }
     pdl_wait();
-    if (pf_bytes && threadIdx.x == 0) {
-        // the next GEMM's first weight bytes into L2 while this latency-bound
-        // kernel runs (its predecessor, the previous GEMM, has finished streaming)
-        const unsigned long long per = (pf_bytes / gridDim.x + 4095) & ~4095ull;
-        const unsigned long long b0 = per * blockIdx.x, b1 = b0 + per < pf_bytes ? b0 + per : pf_bytes;
-        const uint64_t pol = policy_evict_last();
-        for (unsigned long long o = b0; o < b1; o += 32768)
-            l2_prefetch_bulk(pf + o, static_cast<uint32_t>(b1 - o < 32768 ? b1 - o : 32768), pol);
-    }
     float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(t) * d);
     const size_t pstride = static_cast<size_t>(T_) * d / 4;
     const float4* pr = reinterpret_cast<const float4*>(part) + static_cast<size_t>(t) * d / 4;
@@ -514,7 +489,7 @@ void qkv_rope_kv(const QkvArgs& a, cudaStream_t st) {
 }
 
 void add_rmsnorm(const float* part, int splits, float* x, const void* w, bool f32, int T, int d, float eps, void* h,
-                 const int32_t* cmap, void* hc, cudaStream_t st, const void* pf, size_t pf_bytes) {
+                 const int32_t* cmap, void* hc, cudaStream_t st) {
     if (!T) return;
     if (d % 4 || d > 8192 * 4) throw std::runtime_error("add_rmsnorm: d must be a multiple of 4");
     static const bool cluster_rms = std::getenv("HK_RMS_CLUSTER") != nullptr;  // A/B: the 8-CTA cluster kernel
@@ -526,14 +501,11 @@ void add_rmsnorm(const float* part, int splits, float* x, const void* w, bool f3
         bf16* hb = static_cast<bf16*>(h);
         bf16* hcb = static_cast<bf16*>(hc);
         if (vpt == 1)
-            launch_pdl(add_rmsnorm_row_kernel<1>, dim3(T), dim3(threads), 0, st, part, splits, x, wb, T, d, eps, hb, cmap, hcb,
-                       static_cast<const char*>(pf), static_cast<unsigned long long>(pf ? pf_bytes : 0));
+            launch_pdl(add_rmsnorm_row_kernel<1>, dim3(T), dim3(threads), 0, st, part, splits, x, wb, T, d, eps, hb, cmap, hcb);
         else if (vpt == 2)
-            launch_pdl(add_rmsnorm_row_kernel<2>, dim3(T), dim3(threads), 0, st, part, splits, x, wb, T, d, eps, hb, cmap, hcb,
-                       static_cast<const char*>(pf), static_cast<unsigned long long>(pf ? pf_bytes : 0));
+            launch_pdl(add_rmsnorm_row_kernel<2>, dim3(T), dim3(threads), 0, st, part, splits, x, wb, T, d, eps, hb, cmap, hcb);
         else
-            launch_pdl(add_rmsnorm_row_kernel<4>, dim3(T), dim3(threads), 0, st, part, splits, x, wb, T, d, eps, hb, cmap, hcb,
-                       static_cast<const char*>(pf), static_cast<unsigned long long>(pf ? pf_bytes : 0));
+            launch_pdl(add_rmsnorm_row_kernel<4>, dim3(T), dim3(threads), 0, st, part, splits, x, wb, T, d, eps, hb, cmap, hcb);
         HK_LAUNCHED(1);
         return;
     }
