@@ -268,14 +268,14 @@ def main():
         a_b = prof["attn_shared"]["bytes"] + prof["attn_private"]["bytes"]
         if a_ms > 0:
             ach = a_b / (a_ms / 1e3) / 1e9
-            at = traffic.get("attn_decode_kernel<4> (configs[1] decode, k~5, 148 CTAs)")
+            at = traffic.get("attn_decode_kernel<4> (configs[1] decode, k=128, 148 CTAs)")
             line["attention_roofline"] = {
                 "bound": "hbm",
                 "kernel": "attn_decode_kernel (tcgen05 prefix-shared tiles, multicast CTA pairs + mma.sync private "
                           "queue + in-kernel merge), one launch per layer",
                 "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                 "traffic": (at["dram_read_bytes"] + at["dram_write_bytes"]) if at else None,
-                "traffic_kernel": "one decode launch at k~5 (algorithmic %.0f B), ncu --set full" % at["algorithmic_bytes"]
+                "traffic_kernel": "one decode launch at k=128 (algorithmic %.0f B), ncu --set full" % at["algorithmic_bytes"]
                 if at else None,
                 "peak_source": peak_src, "algorithmic_bytes_run": a_b,
                 "note": "bytes = shared-prefix KV once per group + private KV + Q/O, per layer, summed over the run; "
