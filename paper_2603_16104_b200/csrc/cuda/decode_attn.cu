@@ -696,16 +696,20 @@ __device__ __forceinline__ void merge16(const DecodeAttnArgs& a, int pair, int n
     const int lane = threadIdx.x & 31, sub = lane & 15;
     const bool active = pair < n_pairs;
     const int row = active ? pair / a.H : 0, head = active ? pair % a.H : 0;
+    if (a.trace && threadIdx.x == 0) a.trace[static_cast<size_t>(blockIdx.x) * 24 + 18] = clock64();
     const int np = active ? a.n_parts[row] : 0;
     const size_t base = (static_cast<size_t>(row) * a.H + head) * a.max_parts;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float M = -INFINITY, L = 0.f;
     // the first batch's loads are issued together with the part count (they do
     // not depend on it; unused slots are masked): one L2 round trip per row
-    float2 ml = sub < 8 ? __ldcg(&a.part_ml[base + sub]) : make_float2(-INFINITY, 0.f);
+    // (a.any_merge = the step's max part count bounds the first batch: no loads of unused slots)
+    const int lim = a.any_merge > 1 ? min(8, a.any_merge) : 8;
+    float2 ml = sub < lim ? __ldcg(&a.part_ml[base + sub]) : make_float2(-INFINITY, 0.f);
     uint4 v[8];  // 8 bf16 dims of each of the batch's parts
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = __ldcg(reinterpret_cast<const uint4*>(part_bf16(a) + (base + k) * HD) + sub);
+    for (int k = 0; k < 8; ++k)
+        v[k] = k < lim ? __ldcg(reinterpret_cast<const uint4*>(part_bf16(a) + (base + k) * HD) + sub) : make_uint4(0u, 0u, 0u, 0u);
     for (int k0 = 0; k0 < a.max_parts; k0 += 8) {
         if (!__any_sync(full, k0 < np)) break;
         if (k0 > 0) {
@@ -742,6 +746,7 @@ __device__ __forceinline__ void merge16(const DecodeAttnArgs& a, int pair, int n
         }
         M = Mn;
     }
+    if (a.trace && threadIdx.x == 0) a.trace[static_cast<size_t>(blockIdx.x) * 24 + 19] = clock64();
     if (!active || np <= 1) return;
     const float inv = L > 0.f ? __frcp_rn(L) : 0.f;
     uint4 w4;
@@ -750,6 +755,7 @@ __device__ __forceinline__ void merge16(const DecodeAttnArgs& a, int pair, int n
     w4.z = pack2(acc[4] * inv, acc[5] * inv);
     w4.w = pack2(acc[6] * inv, acc[7] * inv);
     *reinterpret_cast<uint4*>(a.out + (static_cast<size_t>(a.dec_tok0 + row) * a.H + head) * HD + sub * 8) = w4;
+    if (a.trace && threadIdx.x == 0) a.trace[static_cast<size_t>(blockIdx.x) * 24 + 20] = clock64();
 }
 
 // Fallback merge launch (when the attention grid exceeds one CTA per SM).

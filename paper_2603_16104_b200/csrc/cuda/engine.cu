@@ -776,8 +776,12 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
                                        d_pages, d_sh, static_cast<int>(dplan.sh.size()), dplan.sh_cluster, d_pv,
                                        static_cast<int>(dplan.pv.size()), part_o, part_ml, max_parts, d_np,
                                        wk.counters, static_cast<int>(dec.size()),
-                                       static_cast<int>(std::any_of(dplan.n_parts.begin(), dplan.n_parts.end(),
-                                                                    [](int32_t v) { return v > 1; })),
+                                       [&] {
+                                           const int mx = dplan.n_parts.empty()
+                                                              ? 0
+                                                              : *std::max_element(dplan.n_parts.begin(), dplan.n_parts.end());
+                                           return mx > 1 ? mx : 0;
+                                       }(),
                                        // per-layer queue state: the queue head may be claimed before
                                        // griddepcontrol.wait, so layers never share it
                                        wk.counters + ctr_words + 4 * l, wk.counters + ctr_words + 4 * l + 1,

@@ -2,6 +2,7 @@
 #include <string>
 #include <vector>
 
+#include <algorithm>
 #include "common.cuh"
 #include "helium_b200_kernels.h"
 #include "kernels.cuh"
@@ -126,7 +127,11 @@ double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_
                               reinterpret_cast<const hkd::ShItem*>(m + o_sh), static_cast<int>(plan.sh.size()), plan.sh_cluster,
                               reinterpret_cast<const hkd::PvItem*>(m + o_pv), static_cast<int>(plan.pv.size()),
                               static_cast<float*>(bufs[1]), static_cast<float2*>(bufs[2]), kMaxParts,
-                              reinterpret_cast<const int32_t*>(m + o_np), ctr, n_rows, 1,
+                              reinterpret_cast<const int32_t*>(m + o_np), ctr, n_rows,
+                              [&] {
+                                  const int mx = plan.n_parts.empty() ? 0 : *std::max_element(plan.n_parts.begin(), plan.n_parts.end());
+                                  return mx > 1 ? mx : 0;
+                              }(),
                               ctr + static_cast<size_t>(n_rows) * Hkv,
                               ctr + static_cast<size_t>(n_rows) * Hkv + 1, ctr + static_cast<size_t>(n_rows) * Hkv + 2,
                               0, 0,

@@ -169,7 +169,7 @@ struct DecodeAttnArgs {
     const int32_t* n_parts; // [rows] partials per (row, kv head)
     int32_t* counters;      // [rows][Hkv], zero between launches
     int n_rows;             // decode rows of the step
-    int any_merge;          // some row has > 1 partial (a merge launch follows)
+    int any_merge;          // max partials of a row when > 1 (a merge follows), else 0; 1 = unknown
     int32_t* pv_next;       // private work queue head (zero between launches)
     int32_t* pv_done;       // warps / CTAs that left the queue (zero between launches)
     int32_t* grid_arrive;   // grid-wide arrival before the in-kernel merge (zero between launches)

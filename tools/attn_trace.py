@@ -61,3 +61,7 @@ for (i0, n0), (i1, n1) in zip(c1, c1[1:]):
 allc = t[t[:, 0] > 0]
 print(f"  tail: queue end {us(allc[:,12]).max():.2f}, grid barrier entered {us(allc[:,16]).min():.2f}..{us(allc[:,16]).max():.2f}, "
       f"merge start {us(allc[:,13]).min():.2f}..{us(allc[:,13]).max():.2f}, merge end {us(allc[:,17]).min():.2f}..{us(allc[:,17]).max():.2f} us")
+m = allc[(allc[:, 18] > 0) & (allc[:, 20] > 0)]
+if len(m):
+    print(f"  merge16 (thread 0, cycles): entry -> batch consumed {np.median(m[:,19]-m[:,18]):.0f} (max {np.max(m[:,19]-m[:,18]):.0f}), "
+          f"-> stored {np.median(m[:,20]-m[:,19]):.0f}; CTAs with pairs {len(m)}")
