@@ -76,6 +76,15 @@ __device__ __forceinline__ void stamp(const DecodeAttnArgs& a, int cta, int k) {
     }
 }
 
+// launch span (debug, HK_GEMM_TRACE): 0 first CTA start, 1 first wait exit, 2 ~last end
+__device__ __forceinline__ void span_mark(const DecodeAttnArgs& a, int k) {
+    if (a.span && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMin(&a.span[k], k == 2 ? ~t : t);
+    }
+}
+
 // per private item (debug trace): [claim, first page landed, done, (smid << 8) | warp]
 __device__ __forceinline__ void item_stamp(const DecodeAttnArgs& a, int item, int k) {
     if (a.trace && (threadIdx.x & 31) == 0 && item < 6000) {
@@ -295,6 +304,7 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
         const int tok_base = causal ? it.row0 : a.dec_tok0 + it.row0;  // batch token of tile row 0
         pdl_wait();  // q comes from the qkv/RoPE kernel
         pdl_trigger();
+        span_mark(a, 1);
         // causal prefill rows attend keys <= their own position
         const int prow = causal && row < nrows ? a.pos[tok_base + row / G] : 0x7fffffff;
         {
@@ -781,6 +791,7 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
     // plain stores compile to STS
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     pdl_trigger();  // the next kernel (O projection) may launch; it waits for us before reading
+    span_mark(a, 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t* ring = sm + warp * PV_ST * 8192;
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + SH_SMEM - 1024) + warp * PV_ST;
@@ -827,6 +838,7 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
             }
         }
         pdl_wait();  // q and this step's own K/V come from the qkv/RoPE kernel
+        span_mark(a, 1);
         if (warp >= DA_PV_WARPS) return;
     }
     while (nx.idx < a.n_pv) {
@@ -848,6 +860,7 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
             *a.pv_next = 0;
             *a.pv_done = 0;
         }
+        span_mark(a, 2);
         return;
     }
     // Grid-wide arrival: every CTA of this grid is resident (one per SM, and
@@ -878,6 +891,7 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
         *a.pv_done = 0;
         *a.grid_arrive = 0;
     }
+    span_mark(a, 2);
 }
 
 template <int G>

@@ -789,6 +789,9 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
                                        static_cast<bf16*>(attn), scale * 1.4426950408889634f, nullptr,
                                        l2_prefetch_o ? lw.wo : nullptr,
                                        static_cast<size_t>(d) * H * hd * esz};
+                da.span = hkd::gemm_trace_slot(
+                    -1, static_cast<int>((dplan.shared_bytes + dplan.private_bytes + prefill_bytes) / 1024),
+                    static_cast<int>(dec.size()), static_cast<int>(dplan.sh.size()), 0);
                 // one launch: decode tiles + private queue + prefill tiles
                 ck = clock.begin(dec.empty() ? 3 : 1, st);
                 if (dbl("attn")) hkd::decode_attention(da, wk.tm_kv, st);

@@ -478,11 +478,13 @@ struct GemmTrace {
     std::vector<std::array<int, 5>> meta;  // N, K, T, splits, grid CTAs
 };
 GemmTrace g_gtrace;
+}  // namespace
+
 unsigned long long* gemm_trace_slot(int N, int K, int T, int splits, int ctas) {
     static const bool on = std::getenv("HK_GEMM_TRACE") != nullptr;
     if (!on) return nullptr;
     if (!g_gtrace.d) {
-        g_gtrace.cap = 1 << 16;
+        g_gtrace.cap = 1 << 18;
         HK_CUDA(cudaMalloc(&g_gtrace.d, static_cast<size_t>(g_gtrace.cap) * 4 * 8));
         HK_CUDA(cudaMemset(g_gtrace.d, 0xff, static_cast<size_t>(g_gtrace.cap) * 4 * 8));
     }
@@ -490,7 +492,6 @@ unsigned long long* gemm_trace_slot(int N, int K, int T, int splits, int ctas) {
     g_gtrace.meta.push_back({N, K, T, splits, ctas});
     return g_gtrace.d + 4 * static_cast<size_t>(g_gtrace.n++);
 }
-}  // namespace
 
 int gemm_trace_dump(const char* path) {
     if (!g_gtrace.d) return 0;

@@ -31,6 +31,9 @@ void gemm_bf16_streamk(const bf16* W, const bf16* X, int N, int K, int T, int ep
 bool gemm_streamk_enabled();
 // debug: write the HK_GEMM_TRACE launch spans as CSV; returns the launch count
 int gemm_trace_dump(const char* path);
+// debug (HK_GEMM_TRACE): a span slot [first CTA start, first wait exit, ~last end, ~last main-loop end]
+// for one launch; N = -1 marks a decode-attention launch (K = its algorithmic KB)
+unsigned long long* gemm_trace_slot(int N, int K, int T, int splits, int ctas);
 // allocate the stream-K workspace/counters ahead of any CUDA-graph capture
 void gemm_streamk_reserve(int max_tiles, int max_bn);
 // ids[t] = argmax over the n_tiles (max, idx) partials of kEpiArgmax (lowest index wins ties)
@@ -180,6 +183,7 @@ struct DecodeAttnArgs {
     unsigned long long* trace;  // optional [n_sh + n_pv][8] %globaltimer stamps per CTA phase (null = off)
     const void* l2_prefetch;    // optional: bytes the next kernel streams (O-projection weights), pulled
     size_t l2_prefetch_bytes;   // into L2 by otherwise idle warps while HBM is under-used
+    unsigned long long* span = nullptr;  // debug (HK_GEMM_TRACE): launch span slot, see gemm_trace_slot
 };
 // Host planning of one step's decode rows. Rows of a group are consecutive
 // and share `shared_pages` leading pages of their block tables.

@@ -226,7 +226,9 @@ __global__ void swiglu_interleaved_kernel(const float* __restrict__ gu, int F, f
 template <typename T>
 __global__ void qkv_rope_kv_kernel(QkvArgs a) {
     pdl_trigger();
-    pdl_wait();
+    // everything but the split-K partials (step metadata, page ids, RoPE
+    // table, bias) is loaded before griddepcontrol.wait: only the partial
+    // loads remain on the critical path after the QKV GEMM
     const RopeArgs& r = a.r;
     const int t = blockIdx.y;
     const int half = r.hd / 2;
@@ -254,6 +256,18 @@ __global__ void qkv_rope_kv_kernel(QkvArgs a) {
         c0 = (r.H + r.Hkv) * r.hd + 2 * jj;
         c1 = c0 + 1;
     }
+    float b0 = 0.f, b1 = 0.f;
+    if (a.bias) {
+        if (sizeof(T) == 4) {
+            b0 = static_cast<const float*>(a.bias)[c0];
+            b1 = static_cast<const float*>(a.bias)[c1];
+        } else {
+            b0 = bf2f(static_cast<const bf16*>(a.bias)[c0]);
+            b1 = bf2f(static_cast<const bf16*>(a.bias)[c1]);
+        }
+    }
+    const float2 cs = j < n_rot ? r.rope[static_cast<size_t>(pos) * half + (j % half)] : make_float2(1.f, 0.f);
+    pdl_wait();
     float x0 = 0.f, x1 = 0.f;
     for (int s0 = 0; s0 < a.splits; s0 += 8) {
         float p0[8], p1[8];
@@ -270,13 +284,8 @@ __global__ void qkv_rope_kv_kernel(QkvArgs a) {
         }
     }
     if (a.bias) {
-        if (sizeof(T) == 4) {
-            x0 += static_cast<const float*>(a.bias)[c0];
-            x1 += static_cast<const float*>(a.bias)[c1];
-        } else {
-            x0 += bf2f(static_cast<const bf16*>(a.bias)[c0]);
-            x1 += bf2f(static_cast<const bf16*>(a.bias)[c1]);
-        }
+        x0 += b0;
+        x1 += b1;
     }
     if (j < n_rot) {
         // round to the storage type first: the oracle rotates the stored (bf16) qkv
@@ -284,7 +293,6 @@ __global__ void qkv_rope_kv_kernel(QkvArgs a) {
         x0 = ld(&s0);
         x1 = ld(&s1);
         const int i = (j % half);
-        const float2 cs = r.rope[static_cast<size_t>(pos) * half + i];
         const float o1 = x0 * cs.x - x1 * cs.y;
         const float o2 = x1 * cs.x + x0 * cs.y;
         const T q1 = cvt<T>(o1), q2 = cvt<T>(o2);
