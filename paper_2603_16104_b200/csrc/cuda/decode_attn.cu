@@ -66,6 +66,10 @@ __device__ __forceinline__ int arrive_acq_rel(int32_t* ctr) {
     return old;
 }
 
+// per-chunk clock64 stamps of thread 0 (softmax) and the MMA issuer, chunks < 8 (debug trace)
+__device__ __forceinline__ void cstamp(const DecodeAttnArgs& a, int c, int k) {
+    if (a.trace && c < 8) a.trace[16384 + static_cast<size_t>(blockIdx.x) * 48 + c * 6 + k] = clock64();
+}
 __device__ __forceinline__ void stamp(const DecodeAttnArgs& a, int cta, int k) {
     if (a.trace && threadIdx.x == 0) {
         unsigned long long t;
@@ -129,12 +133,13 @@ __device__ __forceinline__ void prefetch_next_weights(const DecodeAttnArgs& a) {
 //                     column half = warp / 4): scale, row max (exchanged
 //                     through smem), lazy O rescale, exp2, P (bf16) into the
 //                     A-operand tile, then the epilogue and arrival counters.
-// smem (1024-aligned): sQ [2][128][64] | 2 x (sK [2][128][64] | sV) | sP [2][128][64] | barriers | exchange
+// smem (1024-aligned): sQ [2][128][64] | 3 x sK [2][128][64] | 2 x sV | barriers | exchange (P lives in TMEM)
 constexpr int SQ_BYTES = ROWS * HD * 2;   // 32 KB
 constexpr int SKV_BYTES = KC * HD * 2;    // 32 KB (K or V of one chunk)
 constexpr int SH_THREADS = 320;
+constexpr int KST = 3;  // K ring depth of a shared tile (V ring: 2)
 constexpr int SH_MAX_PAGES = 1024;        // pages of one tile item (16K keys)
-constexpr int SH_SMEM = 1024 + SQ_BYTES + 2 * 2 * SKV_BYTES + ROWS * KC * 2 + 256 + 7 * ROWS * 4 + (ROWS + 4) * 4 +
+constexpr int SH_SMEM = 1024 + SQ_BYTES + (KST + 2) * SKV_BYTES + 256 + 7 * ROWS * 4 + (ROWS + 4) * 4 +
                         SH_MAX_PAGES * 4;
 
 __device__ __forceinline__ uint32_t sw128(int row, int chunk16) {  // byte offset inside a [rows][64] SW128 block
@@ -144,6 +149,16 @@ __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+// (2^a, 2^b) with one ex2.approx.f16x2: two exponentials per MUFU op (f16
+// arguments <= 8 under the lazy rescale; p is rounded to bf16 for the MMA)
+__device__ __forceinline__ void ex2_pair(float a, float b, float& pa, float& pb) {
+    uint32_t h, e;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
+    asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
+    asm("{.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;}"
+        : "=f"(pa), "=f"(pb)
+        : "r"(e));
 }
 // 2^x on the FMA/ALU pipes: 2^floor(x) * p(frac(x)), p a degree-3 minimax
 // polynomial for 2^f on [0, 1) (max rel. error ~9e-5, well inside the bf16
@@ -159,23 +174,27 @@ __device__ __forceinline__ float ex2_poly(float x) {
 template <int G>
 __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const DecodeAttnArgs& a, uint8_t* sm) {
     uint8_t* sQ = sm;
-    uint8_t* sKV = sm + SQ_BYTES;  // stage b: K at b*2*SKV_BYTES, V at +SKV_BYTES
-    uint8_t* sP = sKV + 4 * SKV_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + ROWS * KC * 2);
+    // K ring of 3 stages, then a V ring of 2 (P lives in tensor memory, so its
+    // 32 KB of shared memory became the third K stage: K(c + 3) is requested as
+    // soon as S(c) has read K(c), hiding the ~2 us loaded HBM latency)
+    uint8_t* sKV = sm + SQ_BYTES;
+    auto sK = [&](int c) { return sKV + (c % KST) * SKV_BYTES; };
+    auto sV = [&](int c) { return sKV + KST * SKV_BYTES + (c & 1) * SKV_BYTES; };
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + (KST + 2) * SKV_BYTES);
     // K and V of a chunk have their own barriers: K(c + 2) streams in as soon as
     // S(c) has read K(c), long before PV(c) frees V(c)
-    uint64_t* k_full = bars;        // [2] K chunk landed (TMA tx)
-    uint64_t* k_empty = bars + 2;   // [2] K chunk consumed (S commit, both CTAs of the pair)
-    uint64_t* s_full = bars + 4;    // [2] S buffer written (MMA commit)
-    uint64_t* s_free = bars + 6;    // [2] S buffer read (256 softmax threads)
-    uint64_t* p_full = bars + 8;    // P written (256 softmax threads)
-    uint64_t* o_done = bars + 9;    // PV complete (MMA commit)
-    uint64_t* q_full = bars + 10;   // Q tile written (256 softmax threads)
-    uint64_t* v_full = bars + 11;   // [2] V chunk landed
-    uint64_t* v_empty = bars + 13;  // [2] V chunk consumed (PV commit, both CTAs)
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+    uint64_t* k_full = bars;        // [KST] K chunk landed (TMA tx)
+    uint64_t* k_empty = bars + 3;   // [KST] K chunk consumed (S commit, both CTAs of the pair)
+    uint64_t* s_full = bars + 6;    // [2] S buffer written (MMA commit)
+    uint64_t* s_free = bars + 8;    // [2] S buffer read (256 softmax threads)
+    uint64_t* p_full = bars + 10;   // P written to TMEM (256 softmax threads)
+    uint64_t* o_done = bars + 11;   // PV complete (MMA commit)
+    uint64_t* q_full = bars + 12;   // Q tile written (256 softmax threads)
+    uint64_t* v_full = bars + 13;   // [2] V chunk landed
+    uint64_t* v_empty = bars + 15;  // [2] V chunk consumed (PV commit, both CTAs)
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 20);
 
-    float* red = reinterpret_cast<float*>(sm + SQ_BYTES + 4 * SKV_BYTES + ROWS * KC * 2 + 256);  // [2][128] x 2
+    float* red = reinterpret_cast<float*>(sm + SQ_BYTES + (KST + 2) * SKV_BYTES + 256);  // [2][128] x 2
     int* flags = reinterpret_cast<int*>(red + 7 * ROWS);  // [ROWS] tokens this CTA merges, [ROWS] count
     int* spg = flags + ROWS + 4;                            // page ids of this item
 
@@ -188,9 +207,11 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
 
     if (tid == 0) {
         tma_prefetch_desc(&tm_kv);
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < KST; ++b) {
             mbar_init(&k_full[b], 1);
             mbar_init(&k_empty[b], 2);  // the MMA issuers of both CTAs of the pair
+        }
+        for (int b = 0; b < 2; ++b) {
             mbar_init(&v_full[b], 1);
             mbar_init(&v_empty[b], 2);
             mbar_init(&s_full[b], 1);
@@ -201,7 +222,7 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
         mbar_init(q_full, 256);
         fence_barrier_init();
     }
-    if (warp == 8) tmem_alloc(tslot, 512);  // S0 [0,128) | S1 [128,256) | O [256,384)
+    if (warp == 8) tmem_alloc(tslot, 512);  // S0 [0,128) | S1 [128,256) | O [256,384) | P [384,448)
     tc_fence_before();
     // the pair's peer multicasts K/V into this CTA's stages and arrives on its
     // barriers: both CTAs' barriers must be initialised first
@@ -224,11 +245,12 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
             // page once from HBM and multicasts it (the shared prefix is read
             // once for all 2 x 128 rows of this kv head)
             auto load = [&](int c, int v) {
-                const int b = c & 1;
+                const int ns = v ? 2 : KST;  // ring depth
+                const int b = c % ns;
                 uint64_t* full = v ? &v_full[b] : &k_full[b];
-                if (c >= 2) mbar_wait(v ? &v_empty[b] : &k_empty[b], ((c >> 1) - 1) & 1);
+                if (c >= ns) mbar_wait(v ? &v_empty[b] : &k_empty[b], ((c / ns) - 1) & 1);
                 const int np = min(8, it.npages - c * 8);
-                uint8_t* dst = sKV + b * 2 * SKV_BYTES + v * SKV_BYTES;
+                uint8_t* dst = v ? sV(c) : sK(c);
                 mbar_expect_tx(full, static_cast<uint32_t>(np) * 2 * 2048);
                 for (int i = crank; i < np; i += 2) {
                     const int rk = a.layer_row0 + (spg[c * 8 + i] * 2 * a.Hkv + it.kvh) * PG + v * rows_per_head;
@@ -249,29 +271,32 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
         pdl_wait();
         pdl_trigger();
         if (lane == 0) {
-            const uint32_t q0 = smem_u32(sQ), p0 = smem_u32(sP);
+            const uint32_t q0 = smem_u32(sQ);
             auto issue_pv = [&](int j) {
                 mbar_wait(p_full, j & 1);
                 mbar_wait(&v_full[j & 1], (j >> 1) & 1);
                 tc_fence_after();
+                cstamp(a, j, 5);
                 const int np = min(8, it.npages - j * 8);
-                const uint32_t v0 = smem_u32(sKV + (j & 1) * 2 * SKV_BYTES + SKV_BYTES);
+                const uint32_t v0 = smem_u32(sV(j));
                 const uint32_t idesc = umma_idesc_bf16(ROWS, HD) | (1u << 16);  // B = V, MN-major
+                // A = P straight from tensor memory: 16 keys = 8 columns per k-step
                 for (int kk = 0; kk < np; ++kk)
-                    umma_bf16(tmem + 256, umma_desc_sw128(p0 + (kk >> 2) * (ROWS * 128) + (kk & 3) * 32),
-                              umma_desc_sw128_lbo(v0 + kk * 2048, SKV_BYTES / 2, 1024), idesc,
-                              (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16_ts(tmem + 256, tmem + 384 + kk * 8,
+                                 umma_desc_sw128_lbo(v0 + kk * 2048, SKV_BYTES / 2, 1024), idesc,
+                                 (j > 0 || kk > 0) ? 1u : 0u);
                 umma_commit(o_done);
                 umma_commit_mc(&v_empty[j & 1], 3);  // V stage free in both CTAs once both PVs are done
             };
             auto issue_s = [&](int c) {
                 const int b = c & 1;
-                mbar_wait(&k_full[b], (c >> 1) & 1);
+                mbar_wait(&k_full[c % KST], (c / KST) & 1);
                 if (c >= 2) mbar_wait(&s_free[b], ((c >> 1) - 1) & 1);
                 tc_fence_after();
+                cstamp(a, c, 4);
                 const int nk = min(8, it.npages - c * 8) * PG;
                 const uint32_t idesc = umma_idesc_bf16(ROWS, nk);
-                const uint32_t k0 = smem_u32(sKV + b * 2 * SKV_BYTES);
+                const uint32_t k0 = smem_u32(sK(c));
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * (SKV_BYTES / 2) + (kk & 3) * 32;
@@ -279,7 +304,7 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                               umma_desc_sw128(k0 + off), idesc, kk > 0 ? 1u : 0u);
                 }
                 umma_commit(&s_full[b]);
-                umma_commit_mc(&k_empty[b], 3);  // K stage free in both CTAs once both S are done
+                umma_commit_mc(&k_empty[c % KST], 3);  // K stage free in both CTAs once both S are done
             };
             mbar_wait(q_full, 0);
             issue_s(0);
@@ -338,6 +363,7 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
             mbar_wait(&s_full[b], (c >> 1) & 1);
             tc_fence_after();
             if (c == 0) stamp(a, blockIdx.x, 7);
+            if (threadIdx.x == 0) cstamp(a, c, 0);
             // raw scores (the softmax scale is folded into the exp2 argument)
             float s[64];
             {
@@ -376,17 +402,19 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
             float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const float p0 = ex2(fmaf(s[2 * j], a.sl2, nm));
-                const float p1 = ex2(fmaf(s[2 * j + 1], a.sl2, nm));
+                float p0, p1;
+                ex2_pair(fmaf(s[2 * j], a.sl2, nm), fmaf(s[2 * j + 1], a.sl2, nm), p0, p1);
                 ls[j & 3] += p0 + p1;
                 pk[j] = pack2(p0, p1);
             }
             l_half += (ls[0] + ls[1]) + (ls[2] + ls[3]);
             // PV(c-1) must be done before O is rescaled or P rewritten
+            if (threadIdx.x == 0) cstamp(a, c, 1);
             if (c > 0) {
                 mbar_wait(o_done, (c - 1) & 1);
                 tc_fence_after();
             }
+            if (threadIdx.x == 0) cstamp(a, c, 2);
             // tcgen05.ld/st are warp-collective: a warp rescales together
             if (c > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll
@@ -400,14 +428,13 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                 }
                 tmem_wait_st();
             }
-#pragma unroll
-            for (int j8 = 0; j8 < 8; ++j8)
-                *reinterpret_cast<uint4*>(sP + half * (ROWS * 128) + sw128(row, j8)) =
-                    make_uint4(pk[4 * j8], pk[4 * j8 + 1], pk[4 * j8 + 2], pk[4 * j8 + 3]);
-            fence_proxy_async();
+            // P (bf16 pairs, key-major) into its TMEM columns: the PV MMA reads A from there
+            tmem_st32u(t_lane + 384 + half * 32, pk);
+            tmem_wait_st();
             tc_fence_before();
             mbar_arrive(p_full);
             if (c == 0) stamp(a, blockIdx.x, 8);
+            if (threadIdx.x == 0) cstamp(a, c, 3);
         }
         mbar_wait(o_done, (nch - 1) & 1);
         tc_fence_after();
