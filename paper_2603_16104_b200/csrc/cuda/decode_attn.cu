@@ -68,7 +68,7 @@ __device__ __forceinline__ int arrive_acq_rel(int32_t* ctr) {
 
 // per-chunk clock64 stamps of thread 0 (softmax) and the MMA issuer, chunks < 8 (debug trace)
 __device__ __forceinline__ void cstamp(const DecodeAttnArgs& a, int c, int k) {
-    if (a.trace && c < 8) a.trace[16384 + static_cast<size_t>(blockIdx.x) * 48 + c * 6 + k] = clock64();
+    if (a.trace && c < 8) a.trace[16384 + static_cast<size_t>(blockIdx.x) * 64 + c * 8 + k] = clock64();
 }
 __device__ __forceinline__ void stamp(const DecodeAttnArgs& a, int cta, int k) {
     if (a.trace && threadIdx.x == 0) {
@@ -149,16 +149,6 @@ __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
-}
-// (2^a, 2^b) with one ex2.approx.f16x2: two exponentials per MUFU op (f16
-// arguments <= 8 under the lazy rescale; p is rounded to bf16 for the MMA)
-__device__ __forceinline__ void ex2_pair(float a, float b, float& pa, float& pb) {
-    uint32_t h, e;
-    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
-    asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
-    asm("{.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;}"
-        : "=f"(pa), "=f"(pb)
-        : "r"(e));
 }
 // 2^x on the FMA/ALU pipes: 2^floor(x) * p(frac(x)), p a degree-3 minimax
 // polynomial for 2^f on [0, 1) (max rel. error ~9e-5, well inside the bf16
@@ -385,7 +375,9 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
             float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
             float* xm = red_mx + (c & 1) * 2 * ROWS;  // double-buffered half-row maxima
             xm[half * ROWS + row] = mx;
+            if (threadIdx.x == 0) cstamp(a, c, 6);
             named_bar(1, 256);
+            if (threadIdx.x == 0) cstamp(a, c, 7);
             mx = fmaxf(xm[row], xm[ROWS + row]) * a.sl2;  // log2 domain
             // lazy rescale (exact: O and l always refer to m_run; p <= 2^8 between
             // rescales). The exponentials only need the new running max, so they
@@ -402,8 +394,8 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
             float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                float p0, p1;
-                ex2_pair(fmaf(s[2 * j], a.sl2, nm), fmaf(s[2 * j + 1], a.sl2, nm), p0, p1);
+                const float p0 = ex2(fmaf(s[2 * j], a.sl2, nm));
+                const float p1 = ex2(fmaf(s[2 * j + 1], a.sl2, nm));
                 ls[j & 3] += p0 + p1;
                 pk[j] = pack2(p0, p1);
             }

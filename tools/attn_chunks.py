@@ -28,8 +28,8 @@ lib.hkx_decode_attention_trace(C.c_void_p(buf.data_ptr()))
 run(case)
 lib.hkx_decode_attention_trace(None)
 t = buf.cpu().numpy().astype(np.float64)
-ch = t[16384:16384 + 148 * 48].reshape(148, 8, 6)[:n_sh]
-names = ["S ready", "exps", "PV(c-1) waited", "P stored", "S issued", "PV issued"]
+ch = t[16384:16384 + 148 * 64].reshape(148, 8, 8)[:n_sh]
+names = ["S ready", "exps", "PV(c-1) waited", "P stored", "S issued", "PV issued", "max done", "bar passed"]
 base = ch[:, 0, 4][:, None]
 print("median cycles relative to S(0) issue, per chunk (rows) x event (cols):")
 print("      " + " ".join(f"{n:>15s}" for n in names))
@@ -37,4 +37,4 @@ for c in range(8):
     vals = ch[:, c, :] - base
     if np.all(ch[:, c, 0] == 0):
         break
-    print(f"c={c}: " + " ".join(f"{np.median(vals[:, e]):15.0f}" for e in range(6)))
+    print(f"c={c}: " + " ".join(f"{np.median(vals[:, e]):15.0f}" for e in range(8)))
