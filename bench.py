@@ -180,8 +180,15 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize(device)
 
+    # exchange 2: plans whose calls wait on other workers' calls replay the
+    # whole control plane on every rank and broadcast generated ids (NCCL)
+    out_ex = None
+    if ws > 1 and helios.needs_output_exchange(blob, sc):
+        from paper_2603_16104_b200 import exchange
+        out_ex = exchange.make_output_exchange("cuda")
+
     def one_run():
-        m = helios.simulate(blob, sc, engine=eng, only_worker=only)
+        m = helios.simulate(blob, sc, engine=eng, only_worker=only, exchange=out_ex)
         return m, eng.stats()
 
     for _ in range(args.warmup):
@@ -241,7 +248,8 @@ def main():
                    "l2": "inputs > L2: 15 GB of weights streamed every decode iteration",
                    "pin_precompute_ms_per_step": pin_ms / args.steps,
                    "pin_exchange": {0: "local prefill", 1: "prefill + NCCL broadcast source",
-                                    2: "NCCL broadcast receiver"}[pin_role]},
+                                    2: "NCCL broadcast receiver"}[pin_role],
+                   "output_exchange": out_ex is not None},
         "e2e": {"value": decode / wall_s, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": launches,

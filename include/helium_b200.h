@@ -91,6 +91,17 @@ typedef struct hk_kvcache hk_kvcache;
  * flags: bit0 = verify device trie lookups against the host tree. */
 hk_run* hk_simulate(const uint8_t* plan, size_t plan_len, const hk_sim_config* cfg, hk_engine* engine,
                     uint32_t flags);
+/* Cross-worker dependencies with one process per GPU (SURVEY.md §8(e)
+ * exchange 2). With only_worker >= 0 (flags bits 8+) and fn set, every process
+ * replays the control plane of ALL workers (the reference's lock-step loop,
+ * simulator.cpp:287-380) and runs the LLM body only for its own worker; at
+ * every completion of every worker, in the same order in all processes,
+ * fn(user, worker, op, query, tokens, n) is called: the owning process passes
+ * the n generated ids, the others fill `tokens`. Metrics, call rows and
+ * outputs then cover the whole workflow. fn returns 0 on success. */
+typedef int (*hk_output_exchange_fn)(void* user, int worker, int op, int query, uint64_t* tokens, uint64_t n);
+hk_run* hk_simulate_ex(const uint8_t* plan, size_t plan_len, const hk_sim_config* cfg, hk_engine* engine,
+                       uint32_t flags, hk_output_exchange_fn fn, void* user);
 int hk_run_metrics(const hk_run* run, hk_metrics* out);
 /* per-worker vectors of SimMetrics: which 0 = pinned_tokens, 1 = evicted_tokens,
  * 2 = pin_compute_tokens. Returns the count; copies min(count, cap). */

@@ -58,6 +58,8 @@ class EngineStatsC(C.Structure):
                 ("step_tokens", C.c_uint64), ("attn_bytes", C.c_double)]
 
 
+# cross-worker output exchange: int fn(void* user, int worker, int op, int query, uint64_t* tokens, uint64_t n)
+OutputExchangeFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.c_uint64)
 # K6 pin exchange callback: int fn(void* user, int worker, void* device_buf, uint64_t bytes)
 PinExchangeFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_uint64)
 
@@ -66,6 +68,8 @@ _SIGS = {
     "hk_last_error": (C.c_char_p, []),
     "hk_abi_version": (C.c_int, []),
     "hk_simulate": (C.c_void_p, [u8p, C.c_size_t, C.POINTER(SimConfigC), C.c_void_p, C.c_uint32]),
+    "hk_simulate_ex": (C.c_void_p, [u8p, C.c_size_t, C.POINTER(SimConfigC), C.c_void_p, C.c_uint32,
+                                    OutputExchangeFn, C.c_void_p]),
     "hk_run_metrics": (C.c_int, [C.c_void_p, C.POINTER(MetricsC)]),
     "hk_run_worker_stat": (C.c_size_t, [C.c_void_p, C.c_int, u64p, C.c_size_t]),
     "hk_run_report": (C.c_size_t, [C.c_void_p, C.c_int, C.c_char_p, C.c_size_t]),

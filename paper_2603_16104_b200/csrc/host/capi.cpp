@@ -60,6 +60,11 @@ int hk_abi_version(void) { return HK_ABI_VERSION; }
 
 hk_run* hk_simulate(const uint8_t* plan, size_t plan_len, const hk_sim_config* cfg, hk_engine* engine,
                     uint32_t flags) {
+    return hk_simulate_ex(plan, plan_len, cfg, engine, flags, nullptr, nullptr);
+}
+
+hk_run* hk_simulate_ex(const uint8_t* plan, size_t plan_len, const hk_sim_config* cfg, hk_engine* engine,
+                       uint32_t flags, hk_output_exchange_fn fn, void* user) {
     return guard(
         [&]() -> hk_run* {
             hk::Plan p = hk::parse_plan(plan, plan_len);
@@ -68,6 +73,13 @@ hk_run* hk_simulate(const uint8_t* plan, size_t plan_len, const hk_sim_config* c
             hk::ExecOptions eo;
             eo.verify_device_lookup = (flags & 1u) != 0;
             eo.only_worker = static_cast<int>((flags >> 8) & 0xFFFFu) - 1;
+            if (fn) {
+                eo.exchange = [fn, user](int w, const hk::CallId& c, hk::TokenSeq& t) {
+                    if (fn(user, w, static_cast<int>(c.op), c.query, t.data(), t.size()) != 0)
+                        throw std::runtime_error("simulate: output exchange failed for worker " + std::to_string(w) +
+                                                 " call op " + std::to_string(c.op) + " q " + std::to_string(c.query));
+                };
+            }
             if (engine) {
                 std::unique_ptr<hk::LlmBody> body = hk::make_device_body(engine, p, sc);
                 run->m = hk::simulate(p, sc, *body, eo);

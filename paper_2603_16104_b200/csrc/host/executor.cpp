@@ -54,7 +54,10 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
     // call of another worker (then its timeline is independent of the others).
     const int only = opts.only_worker;
     if (only >= static_cast<int>(W)) throw std::runtime_error("simulate: only_worker out of range");
-    if (only >= 0) {
+    // replay: every worker's control plane runs here, outputs of other workers
+    // arrive through opts.exchange (cross-worker dependencies allowed)
+    const bool replay = only >= 0 && static_cast<bool>(opts.exchange);
+    if (only >= 0 && !replay) {
         std::map<CallId, int> wof;
         for (std::size_t w = 0; w < W; ++w)
             for (const CallId& c : plan.sigma[w]) wof[c] = static_cast<int>(w);
@@ -68,6 +71,8 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
             }
     }
     auto active = [&](std::size_t w) { return only < 0 || static_cast<int>(w) == only; };
+    // host control plane of worker w runs in this process
+    auto simulated = [&](std::size_t w) { return replay || active(w); };
 
     Evaluator ev(plan, cfg.seed, cfg.stochastic, /*strict_llm=*/true);
 
@@ -82,12 +87,12 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
         const SimWorkerConfig& wc = cfg.workers[w];
         caches.push_back(std::make_unique<KvTree>(wc.capacity, wc.block));
         pools.push_back(std::make_unique<PagePool>(paged && active(w) ? body.pages_per_worker(static_cast<int>(w)) : 0));
-        if (paged) {
+        if (paged && active(w)) {
             caches[w]->set_page_pool(pools[w].get());
             caches[w]->journaling = body.device_lookup();
         }
         budgets[w] = wc.prefill_budget > 0 ? wc.prefill_budget : std::max<std::size_t>(wc.capacity / 8, wc.block);
-        if (cfg.proactive_pin && active(w)) {
+        if (cfg.proactive_pin && simulated(w)) {
             const auto budget = static_cast<std::size_t>(cfg.pin_capacity_frac * static_cast<double>(wc.capacity));
             std::vector<TokenSeq> pins = static_pin_prefixes(plan, static_cast<int>(w), wc.block, cfg.pin_threshold, budget);
             std::vector<std::vector<int>> pin_pages;
@@ -105,7 +110,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                 pin_pages.push_back(std::move(pages));
                 first_new.push_back(fn);
             }
-            if (paged) body.precompute_pins(static_cast<int>(w), pins, pin_pages, first_new);
+            if (paged && active(w)) body.precompute_pins(static_cast<int>(w), pins, pin_pages, first_new);
         }
         m.pinned_tokens.push_back(caches[w]->pinned_tokens());
     }
@@ -139,6 +144,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
         completing.clear();
         for (std::size_t w = 0; w < W; ++w)
             for (auto& lcp : live[w]) {
+                if (!active(w)) break;  // (replay: other workers' calls are host-only)
                 LiveCall& lc = *lcp;
                 if (lc.out_len > 0 && lc.remaining() == 0 && lc.prefill_done_iter < iter && lc.decoded + 1 == lc.out_len)
                     completing.emplace_back(static_cast<int>(w), &lc);
@@ -146,9 +152,12 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
         body.begin_iteration(iter, completing);
 
         for (std::size_t w = 0; w < W; ++w) {
-            if (!active(w)) continue;
+            if (!simulated(w)) continue;
+            const bool dev = active(w);            // this worker's body (device) runs here
+            const bool wpaged = paged && dev;
+            const bool dlook = dev && body.device_lookup();
             KvTree& cache = *caches[w];
-            PagePool* pool = paged ? pools[w].get() : nullptr;
+            PagePool* pool = wpaged ? pools[w].get() : nullptr;
             if (pool) pool->flush_deferred();
             SimIterRow row;
             row.iter = iter;
@@ -168,7 +177,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
             while (!stop) {
                 std::vector<std::size_t> cand;
                 std::vector<TokenSeq> prompts;
-                const std::size_t max_batch = body.device_lookup() ? 1024 : 1;
+                const std::size_t max_batch = dlook ? 1024 : 1;
                 std::size_t scan = qi;
                 for (; scan < plan.sigma[w].size() && cand.size() < max_batch; ++scan) {
                     if (admitted[w][scan]) continue;
@@ -179,7 +188,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                 }
                 if (cand.empty()) break;
                 std::vector<std::vector<int>> paths;
-                if (body.device_lookup()) {
+                if (dlook) {
                     if (backlog[w] >= budgets[w]) break;
                     body.sync_trie(static_cast<int>(w), cache);
                     std::vector<const TokenSeq*> pp;
@@ -204,7 +213,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                                                cfg.seed, cfg.stochastic);
                     lc.hold = ++holdc;
                     std::vector<int> path;
-                    if (body.device_lookup()) {
+                    if (dlook) {
                         path = paths[k];
                         if (opts.verify_device_lookup) {
                             std::vector<int> hp;
@@ -233,8 +242,8 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                     m.prompt_tokens += lc.prompt.size();
                     m.cache_served_tokens += lc.done;
                     m.calls.push_back(cr);
-                    body.on_admit(static_cast<int>(w), lc);
-                    if (lc.remaining() == 0 && lc.out_len > 0 && paged) {
+                    if (dev) body.on_admit(static_cast<int>(w), lc);
+                    if (lc.remaining() == 0 && lc.out_len > 0 && wpaged) {
                         // Fully cached prompt: the model still needs the logits of
                         // the last prompt position to produce output token 1. Re-run
                         // that position without rewriting its (shared) KV.
@@ -253,7 +262,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                 }
                 if (k < cand.size()) break;
                 qi = scan;
-                if (!body.device_lookup()) {
+                if (!dlook) {
                     // host path admits one candidate at a time; continue scanning
                     if (scan >= plan.sigma[w].size()) break;
                 }
@@ -267,7 +276,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                 if (left == 0) break;
                 if (lc.remaining() == 0) continue;
                 const std::size_t chunk = std::min(left, lc.remaining());
-                if (paged) {
+                if (wpaged) {
                     ensure_pages(lc, lc.done + chunk, cache.block(), pool);
                     StepPlan::Seg s;
                     s.call = &lc;
@@ -296,7 +305,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                     ++lc.decoded;
                     ++row.decode_tokens;
                     ++m.decode_tokens;
-                    if (paged) {
+                    if (wpaged) {
                         // decode #k feeds output token k at position |prompt|+k-1
                         const std::size_t pos = lc.prompt.size() + lc.decoded - 1;
                         ensure_pages(lc, pos + 1, cache.block(), pool);
@@ -313,7 +322,14 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                 }
                 const double len_out = ev.profile_len_out(lc.id.op);
                 const bool det = ev.deterministic(lc.id.op);
-                TokenSeq out = lc.out_len > 0 ? body.take_output(static_cast<int>(w), lc, len_out, det) : TokenSeq{};
+                TokenSeq out;
+                if (dev) {
+                    out = lc.out_len > 0 ? body.take_output(static_cast<int>(w), lc, len_out, det) : TokenSeq{};
+                    if (replay && lc.out_len > 0) opts.exchange(static_cast<int>(w), lc.id, out);  // send
+                } else if (lc.out_len > 0) {
+                    out.assign(lc.out_len, 0);
+                    opts.exchange(static_cast<int>(w), lc.id, out);  // receive from the owning process
+                }
                 if (out.size() != lc.out_len) throw std::logic_error("simulate: output length drifted from plan");
                 ev.put_llm_output(lc.id.op, static_cast<std::size_t>(lc.id.query), out);
                 m.call_outputs[lc.id] = out;
@@ -327,7 +343,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                         if (pg >= 0 && !pool->is_tree(pg)) pool->release(pg);
                     lc.pages.clear();
                 }
-                body.on_finish(static_cast<int>(w), lc);
+                if (dev) body.on_finish(static_cast<int>(w), lc);
                 leaf_done[static_cast<std::size_t>(lc.leaf)] = 1;
                 SimCallRow& cr = m.calls[lc.row];
                 cr.prefill_done_iter = lc.prefill_done_iter;
@@ -336,7 +352,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                 lc.finished = true;
                 ++completed;
             }
-            if (paged && !sp.segs.empty()) body.run_step(sp);
+            if (wpaged && !sp.segs.empty()) body.run_step(sp);
             // finished calls stay alive until their step was issued (segs point at them)
             live[w].erase(std::remove_if(live[w].begin(), live[w].end(),
                                          [](const std::unique_ptr<LiveCall>& lc) { return lc->finished; }),
@@ -352,7 +368,7 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
     m.hit_rate_pct = m.prompt_tokens > 0
                          ? 100.0 * static_cast<double>(m.cache_served_tokens) / static_cast<double>(m.prompt_tokens)
                          : 0.0;
-    if (only < 0) {
+    if (only < 0 || replay) {
         m.outputs = ev.output_values();
     } else {
         // one-worker mode: only outputs whose llm calls all ran here

@@ -9,6 +9,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <set>
@@ -371,6 +372,14 @@ class SyntheticBody : public LlmBody {
 struct ExecOptions {
     bool verify_device_lookup = false;  // also walk the host tree and compare paths
     int only_worker = -1;  // >=0: this process owns one worker's device (others replayed)
+    // Cross-worker dependencies with one process per worker (SURVEY §8(e)
+    // exchange 2): with only_worker >= 0 and `exchange` set, every process
+    // replays the host control plane of ALL workers and drives the body only
+    // for its own; at every completion of every worker (in the same order on
+    // all processes) exchange(worker, call, tokens) is called — the owning
+    // process passes the generated ids, the others receive them (tokens is
+    // pre-sized to the call's output length).
+    std::function<void(int worker, const CallId& call, TokenSeq& tokens)> exchange;
 };
 
 SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const ExecOptions& opts = {});

@@ -1,4 +1,6 @@
-"""K6: pinned-prefix replication across ranks (exchange 1).
+"""Exchanges between the ranks of a multi-GPU run.
+
+K6, exchange 1 — pinned-prefix replication across ranks.
 
 The reference pins the same static prefix on every worker that runs >= 2
 calls under it (static_pin_prefixes + pin insert, simulator.cpp:132-199,
@@ -79,3 +81,25 @@ def enable_pin_broadcast(engine, pins: List[List[int]], src: int = 0, device: st
     role = 1 if dist.get_rank(group) == src else 2
     engine.set_pin_exchange(role, make_broadcast_fn(src, device, group))
     return role
+
+
+# --------------------------------------------------------------- exchange 2
+def make_output_exchange(device: str = "cpu", group=None):
+    """Cross-worker dependencies with one process per GPU (exchange 2): the
+    callback for helios.simulate(..., only_worker=rank, exchange=fn). Rank r
+    owns schedule worker r; at each completion of worker w the owner's output
+    ids are broadcast from rank w (host ids only, a few KB). Every rank calls
+    it in the same order because every rank replays the same control plane."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(worker: int, op: int, query: int, tokens):
+        t = torch.from_numpy(tokens.view(np.int64))  # shares memory with the executor's buffer
+        if device == "cpu":
+            dist.broadcast(t, src=worker, group=group)
+        else:
+            d = t.to(device)
+            dist.broadcast(d, src=worker, group=group)
+            t.copy_(d.cpu())
+
+    return fn

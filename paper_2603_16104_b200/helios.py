@@ -170,7 +170,7 @@ def _call_outputs(h) -> Dict[tuple, List[int]]:
 
 
 def simulate(plan: bytes, cfg: SimConfig, engine=None, verify_lookup: bool = False,
-             only_worker: int = -1) -> SimMetrics:
+             only_worker: int = -1, exchange=None) -> SimMetrics:
     """simulate() (simulator.hpp:128-130) on a flattened HKPLAN01 plan.
 
     engine=None runs the synthetic LLM body (reference mode S); an Engine runs
@@ -178,14 +178,34 @@ def simulate(plan: bytes, cfg: SimConfig, engine=None, verify_lookup: bool = Fal
     schedule (one process per GPU; exact when that worker has no cross-worker
     dependency). Raises RuntimeError with the reference's messages
     ("simulate: ...") on invalid schedules/configs.
+
+    exchange (with only_worker >= 0): fn(worker, op, query, tokens: np.ndarray
+    uint64 view) called at every completion of every worker in the same order
+    in all processes — the owner's array holds the generated ids, the others
+    must fill theirs (exchange.make_output_exchange broadcasts over
+    torch.distributed). Cross-worker dependencies are then served and the
+    metrics cover the whole workflow (SURVEY.md §8(e) exchange 2).
     """
     lib = _lib.load()
     buf = (C.c_uint8 * len(plan)).from_buffer_copy(plan)
     c = cfg.to_c()
     flags = (1 if verify_lookup else 0) | ((only_worker + 1) << 8)
-    h = lib.hk_simulate(buf, len(plan), C.byref(c), engine.handle if engine is not None else None, flags)
+    err = []
+    if exchange is not None:
+        def _cb(_user, worker, op, query, toks, n):
+            try:
+                exchange(int(worker), int(op), int(query), np.ctypeslib.as_array(toks, shape=(int(n),)))
+                return 0
+            except Exception as e:  # re-raised below as the cause
+                err.append(e)
+                return 1
+        cb = _lib.OutputExchangeFn(_cb)
+        h = lib.hk_simulate_ex(buf, len(plan), C.byref(c), engine.handle if engine is not None else None, flags,
+                               cb, None)
+    else:
+        h = lib.hk_simulate(buf, len(plan), C.byref(c), engine.handle if engine is not None else None, flags)
     if not h:
-        cause = engine.take_pin_exchange_error() if engine is not None else None
+        cause = err[0] if err else (engine.take_pin_exchange_error() if engine is not None else None)
         raise RuntimeError(_lib.last_error()) from cause
     try:
         mc = _lib.MetricsC()
@@ -214,6 +234,19 @@ def sim_calls_csv(m: SimMetrics) -> str:
 
 def sim_trace_csv(m: SimMetrics) -> str:
     return m.trace_csv
+
+
+def needs_output_exchange(plan: bytes, cfg: SimConfig) -> bool:
+    """True when some call of the schedule waits on a call of another worker,
+    i.e. one-process-per-worker runs need simulate(..., exchange=...)."""
+    for w in range(len(cfg.workers)):
+        try:
+            simulate(plan, cfg, only_worker=w)  # synthetic body: host control plane only
+        except RuntimeError as e:
+            if "cross-worker dependency" in str(e):
+                return True
+            raise
+    return False
 
 
 def worker_pins(plan: bytes, cfg: SimConfig, worker: int) -> List[List[int]]:

@@ -96,5 +96,19 @@ def main():
     emit("t_press", wf, i, p, dict(s, pin_threshold=64), "8 branches, 256-token prefix, 1K cache (eviction)")
 
 
+def main_cross_worker():
+    """Multi-worker plans whose calls wait on calls of another worker (SURVEY
+    §8(e) exchange 2): the tiny map-reduce and the reflect workload on 2 workers."""
+    wf, i, p, s = wl.c1_tiny_mapred()
+    emit("c1_w2", wf, i, p, dict(s, workers=2, collect_trace=True), "configs[0] map-reduce on 2 workers (cross-worker deps)")
+    gen, s = wl.c3_reflect_spec()
+    wft, it, pt = refpy.generate_workload(gen)
+    emit("c3_w2", json.loads(wft), json.loads(it), json.loads(pt), dict(s, workers=2),
+         "configs[2] reflect on 2 workers (cross-worker deps)", full_outputs=False)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "cross_worker":
+        main_cross_worker()
+    else:
+        main()
