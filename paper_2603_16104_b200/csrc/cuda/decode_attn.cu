@@ -346,7 +346,6 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
         float m_run = -INFINITY, l_half = 0.f;
         float* red_mx = red;             // [2 chunk parity][2][128] row maxima halves
         float* red_l = red + 5 * ROWS;   // [2][128]
-        float* red_m = red + 4 * ROWS;   // [128] final m_run
         for (int c = 0; c < nch; ++c) {
             const int b = c & 1;
             const int nk = min(8, it.npages - c * 8) * PG;
