@@ -93,3 +93,11 @@ def test_only_worker_without_exchange_still_rejects_cross_worker_plans():
     sc = wl.sim_config_from_meta(meta)
     with pytest.raises(RuntimeError, match="cross-worker dependency"):
         helios.simulate(blob, sc, only_worker=0)
+
+
+def test_needs_output_exchange_detects_cross_worker_plans():
+    from paper_2603_16104_b200 import helios
+    from paper_2603_16104_b200 import workloads as wl
+    for name, want in (("c1_w2", True), ("c3_w2", True), ("c2x2", False), ("c4_w2", False), ("c1", False)):
+        blob, meta = wl.load_plan(name)
+        assert helios.needs_output_exchange(blob, wl.sim_config_from_meta(meta)) is want, name
