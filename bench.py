@@ -125,6 +125,43 @@ def run_reference(args, ws, rank):
     print(json.dumps(line))
 
 
+def inpipeline_spans(eng, one_run):
+    """Bytes-weighted GB/s of the decode GEMMs and of the decode attention over
+    one whole run, from per-launch spans (wait exit -> last CTA end)."""
+    import csv
+    import tempfile
+    from paper_2603_16104_b200 import _lib
+    lib = _lib.load()
+    lib.hk_engine_set_graphs(eng.handle, 0)
+    lib.hkx_span_trace(1)
+    try:
+        one_run()
+        with tempfile.NamedTemporaryFile(suffix=".csv", delete=False) as f:
+            path = f.name
+        lib.hkx_gemm_trace_dump(path.encode())
+    finally:
+        lib.hkx_span_trace(0)
+        lib.hk_engine_set_graphs(eng.handle, 1)
+    acc = {"gemm": [0.0, 0.0, 0], "attn": [0.0, 0.0, 0]}
+    with open(path) as fh:
+        for r in csv.DictReader(fh):
+            n, k, t = int(r["N"]), int(r["K"]), int(r["T"])
+            wd, en = int(r["wait_done"]), int(r["end"])
+            if wd >= (1 << 63) or en <= wd:
+                continue
+            if n == -1 and t > 0:
+                fam, b = "attn", k * 1024.0
+            elif n > 0 and t <= 64:
+                fam, b = "gemm", float(n) * k * 2
+            else:
+                continue
+            acc[fam][0] += b
+            acc[fam][1] += (en - wd) * 1e-9
+            acc[fam][2] += 1
+    os.unlink(path)
+    return {f: {"achieved": v[0] / v[1] / 1e9 if v[1] > 0 else None, "launches": v[2]} for f, v in acc.items()}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -230,6 +267,13 @@ def main():
         prof_stats = eng.stats()
         eng.profile(False)
 
+    # in-pipeline spans (not timed): one run with PDL but without CUDA graphs and
+    # without event brackets; every decode GEMM / attention launch records its
+    # first griddepcontrol.wait exit and last CTA end (%globaltimer)
+    spans = None
+    if not args.no_profile and rank == 0:
+        spans = inpipeline_spans(eng, one_run)
+
     if rank != 0:
         eng.close()
         if ws > 1:
@@ -271,6 +315,12 @@ def main():
                             if gu else None,
                             "peak_source": peak_src,
                             "share_of_step": g["ms"] / (prof_stats["pin_ms"] + prof_stats["iter_ms"])}
+        if spans and spans["gemm"]["achieved"]:
+            line["roofline"]["inpipeline"] = {
+                "achieved": spans["gemm"]["achieved"], "frac": spans["gemm"]["achieved"] / hbm,
+                "launches": spans["gemm"]["launches"],
+                "method": "decode split-K GEMMs (T <= 64): weight bytes / (last CTA end - first griddepcontrol.wait "
+                          "exit), %globaltimer, one run with PDL and no CUDA graphs / events"}
         # prefix-shared decode attention = shared-prefix items + private-suffix items + merge
         a_ms = prof["attn_shared"]["ms"] + prof["attn_private"]["ms"] + prof["attn_merge"]["ms"]
         a_b = prof["attn_shared"]["bytes"] + prof["attn_private"]["bytes"]
@@ -288,6 +338,12 @@ def main():
                 "peak_source": peak_src, "algorithmic_bytes_run": a_b,
                 "note": "bytes = shared-prefix KV once per group + private KV + Q/O, per layer, summed over the run; "
                         "time = CUDA events around each launch in one profiled run (no PDL overlap)"}
+            if spans and spans["attn"]["achieved"]:
+                line["attention_roofline"]["inpipeline"] = {
+                    "achieved": spans["attn"]["achieved"], "frac": spans["attn"]["achieved"] / hbm,
+                    "launches": spans["attn"]["launches"],
+                    "method": "same algorithmic bytes / (last CTA end - first griddepcontrol.wait exit) per launch, "
+                              "%globaltimer, one run with PDL and no CUDA graphs / events"}
         line["kernel_ms_per_step"] = {k: v["ms"] for k, v in prof.items()}
     if not args.no_cpu_baseline:
         from oracle.cpu_sample import decode_step_sample

@@ -200,6 +200,8 @@ int hk_engine_reset(hk_engine* e);
  * fn returns 0 on success; non-zero fails hk_simulate with "simulate: ...". */
 typedef int (*hk_pin_exchange_fn)(void* user, int worker, void* device_buf, uint64_t bytes);
 int hk_engine_set_pin_exchange(hk_engine* e, int role, hk_pin_exchange_fn fn, void* user);
+/* CUDA-graph replay of repeated step shapes (default on; off for launch-level tracing) */
+int hk_engine_set_graphs(hk_engine* e, int on);
 
 /* K1 block pool: page-granular gather / scatter / copy on the device.
  * dst/src are device pointers of n * page_bytes bytes. */

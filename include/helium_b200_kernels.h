@@ -50,6 +50,9 @@ int hkx_prefill_attention(const void* qkv, const void* kv, int n_pages, int n_to
 int hkx_decode_attention_trace(void* device_buf);
 /* debug: dump the HK_GEMM_TRACE per-launch spans (first CTA start, wait exit, last end) as CSV */
 int hkx_gemm_trace_dump(const char* path);
+/* debug: start (on = 1, clearing earlier spans) or stop span tracing of the
+ * GEMM / decode-attention launches (run without CUDA graphs: hk_engine_set_graphs) */
+int hkx_span_trace(int on);
 /* Algorithmic bytes of that call: shared KV once per group + private KV + q and o. */
 double hkx_decode_attention_bytes(int n_rows, int H, int Hkv, const int32_t* offs, const int32_t* pos,
                                   const int32_t* group_rows, const int32_t* group_shared_pages, int n_groups);

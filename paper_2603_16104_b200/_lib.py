@@ -97,6 +97,7 @@ _SIGS = {
     "hk_engine_page_bytes": (C.c_size_t, [C.c_void_p]),
     "hk_engine_reset": (C.c_int, [C.c_void_p]),
     "hk_engine_set_pin_exchange": (C.c_int, [C.c_void_p, C.c_int, PinExchangeFn, C.c_void_p]),
+    "hk_engine_set_graphs": (C.c_int, [C.c_void_p, C.c_int]),
     "hk_pool_gather": (C.c_int, [C.c_void_p, C.c_int, i32p, C.c_size_t, C.c_void_p]),
     "hk_pool_scatter": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, i32p, C.c_size_t]),
     "hk_pool_copy": (C.c_int, [C.c_void_p, C.c_int, i32p, i32p, C.c_size_t]),
@@ -114,6 +115,7 @@ _SIGS = {
                                           i32p, i32p, C.c_int, C.c_void_p, C.c_int]),
     "hkx_decode_attention_trace": (C.c_int, [C.c_void_p]),
     "hkx_gemm_trace_dump": (C.c_int, [C.c_char_p]),
+    "hkx_span_trace": (C.c_int, [C.c_int]),
     "hkx_prefill_attention": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i32p,
                                         C.c_int, C.c_void_p]),
     "hkx_decode_attention_bytes": (C.c_double, [C.c_int, C.c_int, C.c_int, i32p, i32p, i32p, i32p, C.c_int]),

@@ -1165,6 +1165,10 @@ hk_engine* hk_engine_create(const hk_model_config* m, const hk_engine_config* c)
 
 void hk_engine_destroy(hk_engine* e) { delete e; }
 
+int hk_engine_set_graphs(hk_engine* e, int on) {
+    return guarded([&] { e->use_graphs = on != 0 && std::getenv("HK_NO_GRAPHS") == nullptr; });
+}
+
 int hk_engine_set_pin_exchange(hk_engine* e, int role, hk_pin_exchange_fn fn, void* user) {
     return guarded([&] {
         if (role < 0 || role > 2) throw std::runtime_error("hk_engine_set_pin_exchange: role must be 0, 1 or 2");

@@ -480,9 +480,17 @@ struct GemmTrace {
 GemmTrace g_gtrace;
 }  // namespace
 
+bool g_span_trace = std::getenv("HK_GEMM_TRACE") != nullptr;  // also hkx_span_trace(1)
+
+void span_trace_reset(bool on) {
+    g_span_trace = on;
+    g_gtrace.n = 0;
+    g_gtrace.meta.clear();
+    if (g_gtrace.d) HK_CUDA(cudaMemset(g_gtrace.d, 0xff, static_cast<size_t>(g_gtrace.cap) * 4 * 8));
+}
+
 unsigned long long* gemm_trace_slot(int N, int K, int T, int splits, int ctas) {
-    static const bool on = std::getenv("HK_GEMM_TRACE") != nullptr;
-    if (!on) return nullptr;
+    if (!g_span_trace) return nullptr;
     if (!g_gtrace.d) {
         g_gtrace.cap = 1 << 18;
         HK_CUDA(cudaMalloc(&g_gtrace.d, static_cast<size_t>(g_gtrace.cap) * 4 * 8));

@@ -178,6 +178,15 @@ double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_
 
 /* Phase timestamps (%globaltimer ns) of the next hkx_decode_attention calls:
  * [n_sh + n_pv CTAs][8] into a device buffer of `words` u64 (NULL = off). */
+int hkx_span_trace(int on) {
+    try {
+        hkd::span_trace_reset(on != 0);
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
 int hkx_gemm_trace_dump(const char* path) {
     try {
         return hkd::gemm_trace_dump(path);
