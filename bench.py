@@ -271,7 +271,7 @@ def main():
     # without event brackets; every decode GEMM / attention launch records its
     # first griddepcontrol.wait exit and last CTA end (%globaltimer)
     spans = None
-    if not args.no_profile and rank == 0:
+    if not args.no_profile:  # every rank runs it: the runs' exchanges are collectives
         spans = inpipeline_spans(eng, one_run)
 
     if rank != 0:
