@@ -13,6 +13,9 @@ transfer runs NVLink peer to peer; 256 MiB for C2's prefix at Llama shape.
 The exchange is only enabled when every rank's worker pins exactly the same
 token sequences (checked with an all-gather of a digest): a worker with a
 different prefix (e.g. C4's per-operator overlap) keeps computing its own.
+
+Exchange 2 — generated ids of calls other workers depend on
+(make_output_exchange, used with helios.simulate(..., exchange=...)).
 """
 from __future__ import annotations
 
