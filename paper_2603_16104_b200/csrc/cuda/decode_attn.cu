@@ -32,6 +32,7 @@
 // the shared kernel waits for the private grid only before exiting, so the
 // next kernel's griddepcontrol.wait covers both.
 #include <algorithm>
+#include <array>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
@@ -1098,6 +1099,9 @@ double plan_prefill_attention(const std::vector<PrefillSegIn>& segs, int H, int 
     const int G = H / Hkv;
     const int rb = ROWS / G;
     double bytes = 0;
+    // tile pairs are emitted longest first: with more pairs than SMs the CTAs
+    // run in waves in launch order, so the short early-causal pairs fill the tail
+    std::vector<std::array<ShItem, 2>> pairs;
     for (const auto& sg : segs) {
         const int nrb = (sg.count + rb - 1) / rb;
         for (int h = 0; h < Hkv; ++h)
@@ -1107,9 +1111,10 @@ double plan_prefill_attention(const std::vector<PrefillSegIn>& segs, int H, int 
                 const int last_tok = std::min(sg.count, (j + 2) * rb) - 1;
                 const int npages = (sg.start + last_tok) / PG + 1;
                 if (npages > SH_MAX_PAGES) throw std::runtime_error("prefill attention: context too long for a tile");
+                std::array<ShItem, 2> pr{};
                 for (int q = 0; q < 2; ++q) {
                     const int r0 = std::min((j + q) * rb, sg.count);
-                    ShItem it{};
+                    ShItem& it = pr[static_cast<size_t>(q)];
                     it.row0 = sg.tok0 + r0;
                     it.ntok = std::max(0, std::min(rb, sg.count - r0));
                     it.kvh = h;
@@ -1118,10 +1123,16 @@ double plan_prefill_attention(const std::vector<PrefillSegIn>& segs, int H, int 
                     it.npages = npages;
                     it.rank = -1;
                     it.flags = 1;
-                    plan.sh.push_back(it);
                 }
+                pairs.push_back(pr);
             }
         bytes += (static_cast<double>(sg.start) + sg.count) * Hkv * 2.0 * HD * 2 + 2.0 * sg.count * H * HD * 2;
+    }
+    std::stable_sort(pairs.begin(), pairs.end(),
+                     [](const std::array<ShItem, 2>& x, const std::array<ShItem, 2>& y) { return x[0].npages > y[0].npages; });
+    for (const auto& pr : pairs) {
+        plan.sh.push_back(pr[0]);
+        plan.sh.push_back(pr[1]);
     }
     return bytes;
 }
