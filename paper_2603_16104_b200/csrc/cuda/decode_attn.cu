@@ -243,10 +243,21 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
                 const int np = min(8, it.npages - c * 8);
                 uint8_t* dst = v ? sV(c) : sK(c);
                 mbar_expect_tx(full, static_cast<uint32_t>(np) * 2 * 2048);
-                for (int i = crank; i < np; i += 2) {
-                    const int rk = a.layer_row0 + (spg[c * 8 + i] * 2 * a.Hkv + it.kvh) * PG + v * rows_per_head;
+                if (c * 8 + np <= it.mc_pages) {
+                    // pages common to the pair: each CTA fetches every other one and multicasts
+                    for (int i = crank; i < np; i += 2) {
+                        const int rk = a.layer_row0 + (spg[c * 8 + i] * 2 * a.Hkv + it.kvh) * PG + v * rows_per_head;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) tma_load_2d_mc(dst + h * SKV_BYTES / 2 + i * 2048, &tm_kv, full, h * 64, rk, 3);
+                        for (int h = 0; h < 2; ++h)
+                            tma_load_2d_mc(dst + h * SKV_BYTES / 2 + i * 2048, &tm_kv, full, h * 64, rk, 3);
+                    }
+                } else {
+                    // this CTA's own pages (e.g. a call's suffix next to its partner's)
+                    for (int i = 0; i < np; ++i) {
+                        const int rk = a.layer_row0 + (spg[c * 8 + i] * 2 * a.Hkv + it.kvh) * PG + v * rows_per_head;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) tma_load_2d(dst + h * SKV_BYTES / 2 + i * 2048, &tm_kv, full, h * 64, rk);
+                    }
                 }
             };
             // K runs one chunk ahead of V (V(c) is needed a softmax later than K(c))
@@ -1053,6 +1064,7 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
                         it.ptab = rows[static_cast<size_t>(g.row0)].ptab;
                         it.page0 = k * cpc * 8;
                         it.npages = std::min(cpc * 8, shared_pages - it.page0);
+                        it.mc_pages = it.npages;  // both row blocks read the group's shared pages
                         it.rank = k;  // partial index
                         plan.sh.push_back(it);
                     }
@@ -1095,38 +1107,63 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
     }
 }
 
-double plan_prefill_attention(const std::vector<PrefillSegIn>& segs, int H, int Hkv, DecodePlan& plan) {
+double plan_prefill_attention(const std::vector<PrefillSegIn>& segs, int H, int Hkv, DecodePlan& plan,
+                              const int32_t* arena) {
     const int G = H / Hkv;
     const int rb = ROWS / G;
     double bytes = 0;
     // tile pairs are emitted longest first: with more pairs than SMs the CTAs
     // run in waves in launch order, so the short early-causal pairs fill the tail
     std::vector<std::array<ShItem, 2>> pairs;
-    for (const auto& sg : segs) {
+    auto item = [&](const PrefillSegIn& sg, int r0, int h, int npages) {
+        ShItem it{};
+        it.row0 = sg.tok0 + r0;
+        it.ntok = std::max(0, std::min(rb, sg.count - r0));
+        it.kvh = h;
+        it.ptab = sg.ptab;
+        it.page0 = 0;
+        it.npages = npages;
+        it.mc_pages = npages;
+        it.rank = -1;
+        it.flags = 1;
+        return it;
+    };
+    auto pages_of = [&](const PrefillSegIn& sg) { return (sg.start + sg.count - 1) / PG + 1; };
+    for (size_t si = 0; si < segs.size(); ++si) {
+        const PrefillSegIn& sg = segs[si];
         const int nrb = (sg.count + rb - 1) / rb;
+        bytes += (static_cast<double>(sg.start) + sg.count) * Hkv * 2.0 * HD * 2 + 2.0 * sg.count * H * HD * 2;
+        if (pages_of(sg) > SH_MAX_PAGES) throw std::runtime_error("prefill attention: context too long for a tile");
+        // two single-tile segments under a common prefix (the calls of one
+        // operator after its pinned system prompt) share a pair: the common
+        // pages are multicast, each CTA loads its own suffix pages
+        if (arena && nrb == 1 && si + 1 < segs.size()) {
+            const PrefillSegIn& sb = segs[si + 1];
+            const int na = pages_of(sg), nb = pages_of(sb);
+            if ((sb.count + rb - 1) / rb == 1 && na == nb) {
+                int common = 0;
+                while (common < na && arena[sg.ptab + common] == arena[sb.ptab + common]) ++common;
+                if (common >= 8) {
+                    for (int h = 0; h < Hkv; ++h) {
+                        std::array<ShItem, 2> pr{item(sg, 0, h, na), item(sb, 0, h, na)};
+                        pr[0].mc_pages = pr[1].mc_pages = common;
+                        pairs.push_back(pr);
+                    }
+                    bytes += (static_cast<double>(sb.start) + sb.count) * Hkv * 2.0 * HD * 2 + 2.0 * sb.count * H * HD * 2;
+                    ++si;
+                    continue;
+                }
+            }
+        }
         for (int h = 0; h < Hkv; ++h)
             for (int j = 0; j < nrb + (nrb & 1); j += 2) {
                 // a CTA pair shares the pages of its later row block (causal mask
                 // trims the earlier one); an odd block count gets an empty partner
                 const int last_tok = std::min(sg.count, (j + 2) * rb) - 1;
                 const int npages = (sg.start + last_tok) / PG + 1;
-                if (npages > SH_MAX_PAGES) throw std::runtime_error("prefill attention: context too long for a tile");
-                std::array<ShItem, 2> pr{};
-                for (int q = 0; q < 2; ++q) {
-                    const int r0 = std::min((j + q) * rb, sg.count);
-                    ShItem& it = pr[static_cast<size_t>(q)];
-                    it.row0 = sg.tok0 + r0;
-                    it.ntok = std::max(0, std::min(rb, sg.count - r0));
-                    it.kvh = h;
-                    it.ptab = sg.ptab;
-                    it.page0 = 0;
-                    it.npages = npages;
-                    it.rank = -1;
-                    it.flags = 1;
-                }
-                pairs.push_back(pr);
+                pairs.push_back({item(sg, std::min(j * rb, sg.count), h, npages),
+                                 item(sg, std::min((j + 1) * rb, sg.count), h, npages)});
             }
-        bytes += (static_cast<double>(sg.start) + sg.count) * Hkv * 2.0 * HD * 2 + 2.0 * sg.count * H * HD * 2;
     }
     std::stable_sort(pairs.begin(), pairs.end(),
                      [](const std::array<ShItem, 2>& x, const std::array<ShItem, 2>& y) { return x[0].npages > y[0].npages; });

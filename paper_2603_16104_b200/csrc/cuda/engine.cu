@@ -631,7 +631,7 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
             hkd::plan_decode_attention(drows, dgroups, H, Hkv, max_parts, hkd::g_num_sms, dplan);
             nparts = dplan.n_parts;
         }
-        prefill_bytes = hkd::plan_prefill_attention(psegs, H, Hkv, dplan);  // appended after the decode tiles
+        prefill_bytes = hkd::plan_prefill_attention(psegs, H, Hkv, dplan, pages.data());  // after the decode tiles
     }
     const int S = static_cast<int>(srows.size());
     if (S > maxS) throw std::runtime_error("engine: too many sampled rows in one step");

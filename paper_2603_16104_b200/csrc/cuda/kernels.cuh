@@ -146,6 +146,8 @@ struct ShItem {
     int rank;    // partial index (decode items)
     int flags;   // bit0: causal prefill item — row0 is a batch token, keys <= the row's
                  // position, the normalised bf16 output is written directly
+    int mc_pages;  // leading pages identical in both CTAs of the pair: those chunks are
+                   // fetched once and multicast, later chunks are loaded by each CTA itself
 };
 struct PvItem {
     int row;     // decode row
@@ -214,7 +216,11 @@ struct PrefillSegIn {
     int start;  // position of the first token
     int ptab;   // block table offset in the arena
 };
-double plan_prefill_attention(const std::vector<PrefillSegIn>& segs, int H, int Hkv, DecodePlan& plan);
+// arena (optional): the host page-id arena the segments' ptab offsets index;
+// with it, single-tile segments that share leading pages (calls under one
+// pinned prefix) are paired with each other instead of with an empty tile
+double plan_prefill_attention(const std::vector<PrefillSegIn>& segs, int H, int Hkv, DecodePlan& plan,
+                              const int32_t* arena = nullptr);
 // tm_kv: the worker's whole pool as a [L*P*2*Hkv*16][128] bf16 tensor map, box {64, 16}.
 void decode_attention(const DecodeAttnArgs& a, const CUtensorMap& tm_kv, cudaStream_t st);
 
