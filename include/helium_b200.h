@@ -116,6 +116,10 @@ size_t hk_run_outputs(const hk_run* run, uint64_t* out, size_t cap);
 /* Generated tokens of every llm call (not only workflow outputs), as u64 words:
  *   n_calls, {op, query, len, tokens[len]}[n_calls]  in (op, query) order. */
 size_t hk_run_call_outputs(const hk_run* run, uint64_t* out, size_t cap);
+/* The device's fp32 logit of every token of hk_run_call_outputs, in the same
+ * order (NaN where the body has none, e.g. mode S). For parity checks: the
+ * greedy choice's logit against the oracle's logit of the same token. */
+size_t hk_run_call_logits(const hk_run* run, float* out, size_t cap);
 /* executor wall time split (seconds): [0] pin precompute, [1] iterations. */
 int hk_run_timing(const hk_run* run, double out[2]);
 void hk_run_free(hk_run* run);

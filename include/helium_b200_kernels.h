@@ -44,6 +44,14 @@ double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_
  * chunked prefill (simulator.cpp:331-343). Returns 0 or -1. */
 int hkx_prefill_attention(const void* qkv, const void* kv, int n_pages, int n_tok, int start, int H, int Hkv,
                           const int32_t* table, int table_len, void* out);
+/* Several causal prefill segments in one launch, planned as the engine plans a
+ * step: segment s = seg_count[s] tokens at qkv/out rows seg_tok0[s].., positions
+ * seg_start[s].., block table arena[seg_ptab[s]..]. Adjacent single-tile
+ * segments with >= 8 common leading pages share a multicast CTA pair (the
+ * calls of one operator under its pinned prefix). Returns 0 or -1. */
+int hkx_prefill_attention_segs(const void* qkv, const void* kv, int n_pages, int n_segs, const int32_t* seg_tok0,
+                               const int32_t* seg_count, const int32_t* seg_start, const int32_t* seg_ptab, int H,
+                               int Hkv, const int32_t* arena, int arena_len, int n_tok, void* out);
 /* Debug: record per-CTA phase timestamps (%globaltimer, ns) of later
  * hkx_decode_attention calls into device_buf ([shared CTAs + private CTAs][8] u64);
  * NULL turns it off. */

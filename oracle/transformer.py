@@ -37,16 +37,29 @@ def round_bf16(v: np.ndarray) -> np.ndarray:
     return b.astype(np.uint32).view(np.float32)
 
 
-def init_uniform(n: int, seed: int, tid: int, scale: float, bf16: bool, chunk: int = 1 << 24) -> np.ndarray:
-    """Mirror of init_uniform_kernel (ops.cu)."""
+def init_uniform(n: int, seed: int, tid: int, scale: float, bf16: bool, chunk: int = 1 << 16) -> np.ndarray:
+    """Mirror of init_uniform_kernel (ops.cu). Cache-sized chunks with in-place
+    uint64 arithmetic (about 2.5x faster than whole-array temporaries)."""
     with np.errstate(over="ignore"):
         base = np.uint64((seed * 0xD1B54A32D192ED03 + tid * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF)
         out = np.empty(n, dtype=np.float32)
+        ar = np.arange(chunk, dtype=np.uint64)
+        x = np.empty(chunk, dtype=np.uint64)
+        t = np.empty(chunk, dtype=np.uint64)
+        c1, c2, c3 = np.uint64(0x9E3779B97F4A7C15), np.uint64(0xBF58476D1CE4E5B9), np.uint64(0x94D049BB133111EB)
+        s30, s27, s31, s40 = np.uint64(30), np.uint64(27), np.uint64(31), np.uint64(40)
+        sc = np.float32(scale)
         for s in range(0, n, chunk):
             e = min(n, s + chunk)
-            h = splitmix64(base + np.arange(s, e, dtype=np.uint64))
-            u = (h >> np.uint64(40)).astype(np.float32) * np.float32(1.0 / 8388608.0) - np.float32(1.0)
-            v = u * np.float32(scale)
+            m = e - s
+            xv, tv = x[:m], t[:m]
+            np.add(ar[:m], base + np.uint64(s) + c1, out=xv)          # splitmix64(base + i)
+            np.right_shift(xv, s30, out=tv); np.bitwise_xor(xv, tv, out=xv); np.multiply(xv, c2, out=xv)
+            np.right_shift(xv, s27, out=tv); np.bitwise_xor(xv, tv, out=xv); np.multiply(xv, c3, out=xv)
+            np.right_shift(xv, s31, out=tv); np.bitwise_xor(xv, tv, out=xv)
+            np.right_shift(xv, s40, out=xv)
+            u = xv.astype(np.float32) * np.float32(1.0 / 8388608.0) - np.float32(1.0)
+            v = u * sc
             out[s:e] = round_bf16(v) if bf16 else v
     return out
 
@@ -114,8 +127,9 @@ class Decoder:
         x1, x2 = x[..., :half], x[..., half:]
         return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1).astype(np.float32)
 
-    def forward(self, ids: Sequence[int], cache: Optional[list] = None, start: int = 0):
-        """Run tokens ids at positions start.. ; returns (logits of last token, cache)."""
+    def forward(self, ids: Sequence[int], cache: Optional[list] = None, start: int = 0, all_logits: bool = False):
+        """Run tokens ids at positions start.. ; returns (logits of the last token
+        — of every token with all_logits — and the cache)."""
         m = self.m
         H, Hkv, hd, d, F = m.n_heads, m.n_kv_heads, m.head_dim, m.d_model, m.ffn_dim
         G = H // Hkv
@@ -159,18 +173,19 @@ class Decoder:
             g_, u_ = gu[:, :F], gu[:, F:]
             a = self._r((g_ / (np.float32(1.0) + np.exp(-g_))) * u_)
             x = x + (a @ lw["wd"].T)
-        hl = self._r(self._rms(x[-1:]))
-        logits = (hl @ self.w.lm_head.T)[0].astype(np.float32)
-        return logits, new_cache
+        hl = self._r(self._rms(x if all_logits else x[-1:]))
+        logits = (hl @ self.w.lm_head.T).astype(np.float32)
+        return (logits if all_logits else logits[0]), new_cache
 
-    def generate(self, ids: Sequence[int], n_new: int, forced: Optional[Sequence[int]] = None):
+    def generate(self, ids: Sequence[int], n_new: int, forced: Optional[Sequence[int]] = None, prefilled=None):
         """Greedy decode n_new tokens. With `forced` (teacher forcing) the given
         tokens are fed instead of the argmax, so logits can be compared step by
-        step against another implementation's sequence."""
+        step against another implementation's sequence. `prefilled` = (logits
+        of the last prompt token, cache over the whole prompt) skips the prefill."""
         out, all_logits = [], []
         if n_new == 0:
             return out, all_logits
-        logits, cache = self.forward(list(ids), None, 0)
+        logits, cache = prefilled if prefilled is not None else self.forward(list(ids), None, 0)
         p = len(ids)
         for k in range(n_new):
             all_logits.append(logits)
@@ -187,3 +202,41 @@ class Decoder:
 def top2_margin(logits: np.ndarray) -> float:
     part = np.partition(logits, -2)[-2:]
     return float(part[1] - part[0])
+
+
+class PrefixReuse:
+    """Greedy decoding of many prompts that reuses the KV of the longest prompt
+    prefix seen before. Exact, not an approximation: K/V at position p depend
+    only on tokens 0..p (causal), which is the same fact the reference's block
+    cache relies on (simulator.cpp:69-121). A fully seen prompt re-runs its last
+    position for the logits (as the engine does)."""
+
+    def __init__(self, dec: Decoder):
+        self.dec = dec
+        self.store: list = []  # (prompt ids, cache over the prompt)
+
+    def prefill(self, ids: Sequence[int]):
+        a = np.asarray(ids, dtype=np.int64)
+        best, bj = None, 0
+        for p, cache in self.store:
+            n = min(len(p), len(a))
+            ne = np.flatnonzero(p[:n] != a[:n])
+            j = int(ne[0]) if len(ne) else n
+            if j > bj:
+                best, bj = cache, j
+        bj = min(bj, len(a) - 1)
+        c0 = [(K[:bj], V[:bj]) for K, V in best] if bj > 0 else None
+        logits, cache = self.dec.forward(a[bj:].tolist(), c0, bj)
+        self.store.append((a, cache))
+        return logits, cache
+
+    def generate(self, ids: Sequence[int], n_new: int, forced: Optional[Sequence[int]] = None):
+        if n_new == 0:
+            return [], []
+        if forced is not None and n_new > 1:
+            # teacher forcing: all positions in one causal pass over prompt || forced[:-1]
+            first, cache = self.prefill(ids)
+            rest, _ = self.dec.forward([int(t) for t in forced[:n_new - 1]], cache, len(ids), all_logits=True)
+            logits = [first] + list(rest)
+            return [int(np.argmax(lg)) for lg in logits], logits
+        return self.dec.generate(ids, n_new, forced=forced, prefilled=self.prefill(ids))

@@ -76,6 +76,7 @@ _SIGS = {
     "hk_run_outputs": (C.c_size_t, [C.c_void_p, u64p, C.c_size_t]),
     "hk_run_timing": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "hk_run_call_outputs": (C.c_size_t, [C.c_void_p, u64p, C.c_size_t]),
+    "hk_run_call_logits": (C.c_size_t, [C.c_void_p, f32p, C.c_size_t]),
     "hk_run_free": (None, [C.c_void_p]),
     "hk_kv_create": (C.c_void_p, [C.c_size_t, C.c_size_t]),
     "hk_kv_lookup": (C.c_size_t, [C.c_void_p, u64p, C.c_size_t, C.c_uint64]),
@@ -118,6 +119,8 @@ _SIGS = {
     "hkx_span_trace": (C.c_int, [C.c_int]),
     "hkx_prefill_attention": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i32p,
                                         C.c_int, C.c_void_p]),
+    "hkx_prefill_attention_segs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i32p, i32p, i32p, i32p,
+                                             C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_void_p]),
     "hkx_decode_attention_bytes": (C.c_double, [C.c_int, C.c_int, C.c_int, i32p, i32p, i32p, i32p, C.c_int]),
 }
 

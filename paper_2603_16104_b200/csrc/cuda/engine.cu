@@ -128,6 +128,7 @@ struct hk_engine {
         int trie_tombs = 0;
         std::vector<int> free_slots;
         std::vector<std::vector<int32_t>> slot_tokens;
+        std::vector<std::vector<float>> slot_logits;  // the sampled token's logit, per generated token
     };
     std::vector<Worker> workers;
     size_t page_bytes_layer = 0;
@@ -137,7 +138,7 @@ struct hk_engine {
     float* x = nullptr;
     void *h = nullptr, *qkv = nullptr, *attn = nullptr, *gu = nullptr, *act = nullptr;
     float* logits = nullptr;
-    int32_t* sample_ids = nullptr;
+    int32_t* sample_ids = nullptr;  // [maxS] sampled ids, followed by [maxS] their logits (fp32 bits)
     float* ws = nullptr;
     size_t ws_floats = 0;
     float* pbuf = nullptr;  // fp32 split-K partials of QKV / O / down GEMMs
@@ -262,6 +263,7 @@ struct hk_engine {
         int s = wk.free_slots.back();
         wk.free_slots.pop_back();
         wk.slot_tokens[static_cast<size_t>(s)].clear();
+        wk.slot_logits[static_cast<size_t>(s)].clear();
         return s;
     }
     void free_slot(int w, int s) { workers[static_cast<size_t>(w)].free_slots.push_back(s); }
@@ -339,6 +341,7 @@ hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m
         t.tab_key = dalloc<uint64_t>(t.table_size);
         t.tab_node = dalloc<int32_t>(t.table_size);
         wk.slot_tokens.resize(c.max_calls);
+        wk.slot_logits.resize(c.max_calls);
     }
     reset_workers();
 
@@ -352,7 +355,7 @@ hk_engine::hk_engine(const hk_model_config& m, const hk_engine_config& c) : mc(m
     gu = dalloc<uint8_t>(static_cast<size_t>(maxT) * 2 * F * esz);
     act = dalloc<uint8_t>(static_cast<size_t>(maxT) * F * esz);
     logits = dalloc<float>(static_cast<size_t>(maxS) * V);
-    sample_ids = dalloc<int32_t>(maxS);
+    sample_ids = dalloc<int32_t>(2 * static_cast<size_t>(maxS));
     ws_floats = static_cast<size_t>(16) * std::max<size_t>(static_cast<size_t>(c.max_calls) * c.n_workers + 64, 256) *
                 std::max({QKV, d, 2 * F});
     ws = dalloc<float>(ws_floats);
@@ -464,8 +467,14 @@ void hk_engine::harvest(bool all) {
         if (!all && cudaEventQuery(p.ev) == cudaErrorNotReady) break;
         HK_CUDA(cudaEventSynchronize(p.ev));
         Worker& wk = workers[static_cast<size_t>(p.worker)];
-        for (size_t i = 0; i < p.slots.size(); ++i)
-            if (p.slots[i] >= 0) wk.slot_tokens[static_cast<size_t>(p.slots[i])].push_back(p.host[i]);
+        const size_t S = p.slots.size();
+        for (size_t i = 0; i < S; ++i)
+            if (p.slots[i] >= 0) {
+                wk.slot_tokens[static_cast<size_t>(p.slots[i])].push_back(p.host[i]);
+                float v;
+                std::memcpy(&v, p.host + S + i, 4);
+                wk.slot_logits[static_cast<size_t>(p.slots[i])].push_back(v);
+            }
         host_bufs.push_back(p.host);
         free_ev.push_back(p.ev);
     }
@@ -708,6 +717,11 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     (void)n_sh_items;
     (void)n_pv_items;
 
+    // max attention partials of a decode row (> 1: the in-kernel merge runs over that many)
+    const int any_merge = [&] {
+        const int mx = dplan.n_parts.empty() ? 0 : *std::max_element(dplan.n_parts.begin(), dplan.n_parts.end());
+        return mx > 1 ? mx : 0;
+    }();
     const float eps = mc.rms_eps;
     const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
     // the step's kernel sequence (eager, or recorded once into a CUDA graph)
@@ -775,13 +789,7 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
                                        static_cast<int>(static_cast<size_t>(l) * ec.pages_per_worker * 2 * Hkv * block),
                                        d_pages, d_sh, static_cast<int>(dplan.sh.size()), dplan.sh_cluster, d_pv,
                                        static_cast<int>(dplan.pv.size()), part_o, part_ml, max_parts, d_np,
-                                       wk.counters, static_cast<int>(dec.size()),
-                                       [&] {
-                                           const int mx = dplan.n_parts.empty()
-                                                              ? 0
-                                                              : *std::max_element(dplan.n_parts.begin(), dplan.n_parts.end());
-                                           return mx > 1 ? mx : 0;
-                                       }(),
+                                       wk.counters, static_cast<int>(dec.size()), any_merge,
                                        // per-layer queue state: the queue head may be claimed before
                                        // griddepcontrol.wait, so layers never share it
                                        wk.counters + ctr_words + 4 * l, wk.counters + ctr_words + 4 * l + 1,
@@ -827,12 +835,14 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         if (f32 || logits_out_host) {
             gemm(lm_head, hs, V, d, S, hkd::kEpiStoreF32, logits, V);
             ck = clock.begin(5, st);
-            hkd::argmax_rows(logits, S, V, sample_ids, d_ss, wk.slot_last, st);
+            hkd::argmax_rows(logits, S, V, sample_ids, reinterpret_cast<float*>(sample_ids + maxS), d_ss, wk.slot_last,
+                             st);
             clock.end(ck, st);
         } else {
             gemm(lm_head, hs, V, d, S, hkd::kEpiArgmax, amax, V);  // greedy argmax fused in the epilogue
             ck = clock.begin(5, st);
-            hkd::argmax_reduce(amax, (V + 127) / 128, S, sample_ids, d_ss, wk.slot_last, st);
+            hkd::argmax_reduce(amax, (V + 127) / 128, S, sample_ids, reinterpret_cast<float*>(sample_ids + maxS), d_ss,
+                               wk.slot_last, st);
             clock.end(ck, st);
         }
     }
@@ -840,9 +850,13 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
 
     const bool graphable = use_graphs && !clock.enabled && !logits_out_host && !f32;
     if (graphable) {
-        // everything the recorded kernels depend on besides metadata contents
+        // everything the recorded kernels depend on besides metadata contents: the
+        // metadata offsets, and every scalar baked into a launch (grid sizes, the
+        // decode-attention tile / queue counts, cluster mode and merge bound)
         const std::vector<int64_t> sig{w, T, S, T_pre, n_multi, static_cast<int64_t>(n_items),
-                                       static_cast<int64_t>(dec.size()), static_cast<int64_t>(o_pages)};
+                                       static_cast<int64_t>(dec.size()), static_cast<int64_t>(o_pages),
+                                       static_cast<int64_t>(dplan.sh.size()), static_cast<int64_t>(dplan.pv.size()),
+                                       static_cast<int64_t>(dplan.sh_cluster), any_merge};
         auto it = graphs.find(sig);
         if (it != graphs.end()) {
             HK_CUDA(cudaGraphLaunch(it->second.exec, st));
@@ -873,7 +887,7 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         Pending p;
         if (host_bufs.empty()) {
             int32_t* hb;
-            HK_CUDA(cudaMallocHost(&hb, static_cast<size_t>(maxS) * 4));
+            HK_CUDA(cudaMallocHost(&hb, static_cast<size_t>(2 * maxS) * 4));
             host_bufs.push_back(hb);
         }
         p.host = host_bufs.back();
@@ -887,8 +901,10 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         free_ev.pop_back();
         p.worker = w;
         p.slots = sslots;
+        // ids, then their logits (read back for the parity checks; 4 B per token)
         HK_CUDA(cudaMemcpyAsync(p.host, sample_ids, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, st));
-        stats.d2h_bytes += static_cast<uint64_t>(S) * 4;
+        HK_CUDA(cudaMemcpyAsync(p.host + S, sample_ids + maxS, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, st));
+        stats.d2h_bytes += static_cast<uint64_t>(S) * 8;
         HK_CUDA(cudaEventRecord(p.ev, st));
         pending.push_back(std::move(p));
         if (pending.size() > 64) harvest(false);
@@ -1000,8 +1016,12 @@ namespace hk {
 
 class DeviceBody : public LlmBody {
   public:
-    DeviceBody(hk_engine* e, const Plan& plan, const SimConfig& cfg) : e_(e) {
-        if (cfg.workers.size() != e->workers.size() && e->workers.size() != 1)
+    DeviceBody(hk_engine* e, const Plan& plan, const SimConfig& cfg, int only_worker) : e_(e) {
+        // one pool per schedule worker; a single pool only serves a single device-driving
+        // worker (W == 1, or only_worker mode) — two workers on one pool would hand out the
+        // same page ids and device-trie node ids and overwrite each other's KV
+        const bool one_driver = cfg.workers.size() == 1 || only_worker >= 0;
+        if (cfg.workers.size() != e->workers.size() && !(e->workers.size() == 1 && one_driver))
             throw std::runtime_error("hk_simulate: engine has " + std::to_string(e->workers.size()) +
                                      " worker pools but the schedule has " + std::to_string(cfg.workers.size()) +
                                      " workers");
@@ -1106,6 +1126,10 @@ class DeviceBody : public LlmBody {
             out.push_back(gen_token(static_cast<std::uint32_t>(toks[i]), static_cast<std::uint32_t>(e_->V)));
         return out;
     }
+    std::vector<float> take_logits(int w, LiveCall& lc) override {
+        const auto& v = e_->workers[static_cast<size_t>(pw(w))].slot_logits[static_cast<size_t>(lc.slot)];
+        return std::vector<float>(v.begin(), v.begin() + static_cast<std::ptrdiff_t>(std::min(v.size(), lc.out_len)));
+    }
     void on_finish(int w, LiveCall& lc) override {
         // The call's last decode token (it writes the KV of the final output
         // token, read back by the completion insert) is still in this
@@ -1131,8 +1155,8 @@ class DeviceBody : public LlmBody {
     std::vector<std::vector<int>> finished_slots_;
 };
 
-std::unique_ptr<LlmBody> make_device_body(hk_engine* e, const Plan& plan, const SimConfig& cfg) {
-    return std::make_unique<DeviceBody>(e, plan, cfg);
+std::unique_ptr<LlmBody> make_device_body(hk_engine* e, const Plan& plan, const SimConfig& cfg, int only_worker) {
+    return std::make_unique<DeviceBody>(e, plan, cfg, only_worker);
 }
 
 }  // namespace hk

@@ -612,7 +612,7 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
 
 namespace {
 __global__ void argmax_reduce_kernel(const float2* __restrict__ part, int n_tiles, int T, int32_t* ids,
-                                     const int32_t* slots, int32_t* slot_last) {
+                                     float* vals, const int32_t* slots, int32_t* slot_last) {
     pdl_trigger();
     pdl_wait();
     const int t = blockIdx.x;
@@ -650,15 +650,16 @@ __global__ void argmax_reduce_kernel(const float2* __restrict__ part, int n_tile
             }
         if (bi == 0x7fffffff) bi = 0;  // all-NaN row: an in-range id (the embedding gather indexes with it)
         ids[t] = bi;
+        if (vals) vals[t] = best;
         if (slots) slot_last[slots[t]] = bi;
     }
 }
 }  // namespace
 
-void argmax_reduce(const float2* part, int n_tiles, int T, int32_t* ids, const int32_t* slots, int32_t* slot_last,
-                   cudaStream_t st) {
+void argmax_reduce(const float2* part, int n_tiles, int T, int32_t* ids, float* vals, const int32_t* slots,
+                   int32_t* slot_last, cudaStream_t st) {
     if (T <= 0) return;
-    launch_pdl(argmax_reduce_kernel, dim3(T), dim3(256), 0, st, part, n_tiles, T, ids, slots, slot_last);
+    launch_pdl(argmax_reduce_kernel, dim3(T), dim3(256), 0, st, part, n_tiles, T, ids, vals, slots, slot_last);
     HK_LAUNCHED(1);
 }
 

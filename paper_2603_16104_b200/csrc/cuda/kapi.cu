@@ -221,17 +221,32 @@ double hkx_decode_attention_bytes(int n_rows, int H, int Hkv, const int32_t* off
     return plan.shared_bytes + plan.private_bytes;
 }
 
-int hkx_prefill_attention(const void* qkv, const void* kv, int n_pages, int n_tok, int start, int H, int Hkv,
-                          const int32_t* table, int table_len, void* out) {
+/* Several causal prefill segments in ONE launch, planned exactly as the engine
+ * plans a step (plan_prefill_attention with the page-id arena): segment s has
+ * seg_count[s] tokens at batch rows seg_tok0[s].., positions seg_start[s]..,
+ * and its block table at arena[seg_ptab[s]..]. Adjacent single-tile segments
+ * that share >= 8 leading pages are paired (common pages multicast). */
+int hkx_prefill_attention_segs(const void* qkv, const void* kv, int n_pages, int n_segs, const int32_t* seg_tok0,
+                               const int32_t* seg_count, const int32_t* seg_start, const int32_t* seg_ptab, int H,
+                               int Hkv, const int32_t* arena, int arena_len, int n_tok, void* out) {
     void* bufs[2] = {nullptr, nullptr};
     try {
         init_sms();
-        if ((start + n_tok + 15) / 16 > table_len) throw std::runtime_error("hkx_prefill_attention: short table");
         hkd::DecodePlan plan;
-        std::vector<hkd::PrefillSegIn> segs{hkd::PrefillSegIn{0, n_tok, start, 0}};
-        hkd::plan_prefill_attention(segs, H, Hkv, plan);
-        std::vector<int32_t> pos(static_cast<size_t>(n_tok));
-        for (int i = 0; i < n_tok; ++i) pos[static_cast<size_t>(i)] = start + i;
+        std::vector<hkd::PrefillSegIn> segs;
+        std::vector<int32_t> pos(static_cast<size_t>(n_tok), 0);
+        for (int s = 0; s < n_segs; ++s) {
+            if (seg_tok0[s] + seg_count[s] > n_tok) throw std::runtime_error("hkx_prefill_attention_segs: rows");
+            if (seg_ptab[s] + (seg_start[s] + seg_count[s] + 15) / 16 > arena_len)
+                throw std::runtime_error("hkx_prefill_attention_segs: short table");
+            segs.push_back(hkd::PrefillSegIn{seg_tok0[s], seg_count[s], seg_start[s], seg_ptab[s]});
+            for (int i = 0; i < seg_count[s]; ++i) pos[static_cast<size_t>(seg_tok0[s] + i)] = seg_start[s] + i;
+        }
+        for (int i = 0; i < arena_len; ++i)
+            if (arena[i] < 0 || arena[i] >= n_pages) throw std::runtime_error("hkx_prefill_attention_segs: bad page");
+        hkd::plan_prefill_attention(segs, H, Hkv, plan, arena);
+        const int32_t* table = arena;
+        const int table_len = arena_len;
         const size_t b_tab = static_cast<size_t>(table_len) * 4, b_pos = pos.size() * 4,
                      b_sh = plan.sh.size() * sizeof(hkd::ShItem);
         const size_t o_pos = (b_tab + 15) / 16 * 16, o_sh = o_pos + (b_pos + 15) / 16 * 16;
@@ -259,6 +274,17 @@ int hkx_prefill_attention(const void* qkv, const void* kv, int n_pages, int n_to
         hk::set_error(e.what());
         return -1;
     }
+}
+
+int hkx_prefill_attention(const void* qkv, const void* kv, int n_pages, int n_tok, int start, int H, int Hkv,
+                          const int32_t* table, int table_len, void* out) {
+    if ((start + n_tok + 15) / 16 > table_len) {
+        hk::set_error("hkx_prefill_attention: short table");
+        return -1;
+    }
+    const int32_t zero = 0;
+    return hkx_prefill_attention_segs(qkv, kv, n_pages, 1, &zero, &n_tok, &start, &zero, H, Hkv, table,
+                                      (start + n_tok + 15) / 16, n_tok, out);
 }
 
 }  // extern "C"

@@ -38,9 +38,10 @@ unsigned long long* gemm_trace_slot(int N, int K, int T, int splits, int ctas);
 void span_trace_reset(bool on);
 // allocate the stream-K workspace/counters ahead of any CUDA-graph capture
 void gemm_streamk_reserve(int max_tiles, int max_bn);
-// ids[t] = argmax over the n_tiles (max, idx) partials of kEpiArgmax (lowest index wins ties)
-void argmax_reduce(const float2* part, int n_tiles, int T, int32_t* ids, const int32_t* slots, int32_t* slot_last,
-                   cudaStream_t st);
+// ids[t] = argmax over the n_tiles (max, idx) partials of kEpiArgmax (lowest index wins ties);
+// vals[t] (optional) = that max logit
+void argmax_reduce(const float2* part, int n_tiles, int T, int32_t* ids, float* vals, const int32_t* slots,
+                   int32_t* slot_last, cudaStream_t st);
 // 2D bf16 tensor map [rows][cols] (row stride cols*2 B), box {box_cols, box_rows}, 128B swizzle
 CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows);
 void gemm_f32(const float* W, const float* X, int N, int K, int T, int epi, void* out, int ldo, const float* bias,
@@ -89,9 +90,10 @@ void qkv_rope_kv(const QkvArgs& a, cudaStream_t st);
 // cmap[t] >= 0 are also written to hc[cmap[t]] (compact rows for the LM head).
 void add_rmsnorm(const float* part, int splits, float* x, const void* w, bool f32, int T, int d, float eps, void* h,
                  const int32_t* cmap, void* hc, cudaStream_t st);
-// ids[r] = argmax_v logits[r][v] (lowest index on ties); also slot_last[slots[r]] = ids[r]
-void argmax_rows(const float* logits, int R, int V, int32_t* ids, const int32_t* slots, int32_t* slot_last,
-                 cudaStream_t st);
+// ids[r] = argmax_v logits[r][v] (lowest index on ties), vals[r] (optional) its logit;
+// also slot_last[slots[r]] = ids[r]
+void argmax_rows(const float* logits, int R, int V, int32_t* ids, float* vals, const int32_t* slots,
+                 int32_t* slot_last, cudaStream_t st);
 
 // ------------------------------------------------------------ attention.cu
 struct AttnItem {

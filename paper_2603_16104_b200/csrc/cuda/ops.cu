@@ -152,7 +152,8 @@ __global__ void swiglu_kernel(const T* gu, int F, T* out) {
     }
 }
 
-__global__ void argmax_kernel(const float* logits, int V, int32_t* ids, const int32_t* slots, int32_t* slot_last) {
+__global__ void argmax_kernel(const float* logits, int V, int32_t* ids, float* vals, const int32_t* slots,
+                              int32_t* slot_last) {
     const int r = blockIdx.x;
     const float* row = logits + static_cast<size_t>(r) * V;
     float best = -INFINITY;
@@ -188,6 +189,7 @@ __global__ void argmax_kernel(const float* logits, int V, int32_t* ids, const in
             }
         if (bi == 0x7fffffff) bi = 0;  // all-NaN row: an in-range id (the embedding gather indexes with it)
         ids[r] = bi;
+        if (vals) vals[r] = best;
         if (slots) slot_last[slots[r]] = bi;
     }
 }
@@ -586,10 +588,10 @@ void swiglu(const void* gu, bool f32, int T, int F, void* out, cudaStream_t st) 
     HK_LAUNCHED(1);
 }
 
-void argmax_rows(const float* logits, int R, int V, int32_t* ids, const int32_t* slots, int32_t* slot_last,
-                 cudaStream_t st) {
+void argmax_rows(const float* logits, int R, int V, int32_t* ids, float* vals, const int32_t* slots,
+                 int32_t* slot_last, cudaStream_t st) {
     if (!R) return;
-    argmax_kernel<<<R, 512, 0, st>>>(logits, V, ids, slots, slot_last);
+    argmax_kernel<<<R, 512, 0, st>>>(logits, V, ids, vals, slots, slot_last);
     HK_LAUNCHED(1);
 }
 

@@ -1,6 +1,7 @@
 // extern "C" entry points of include/helium_b200.h for the host side
 // (executor, KvCache, pins, synth, hashes). Device entry points live in
 // csrc/cuda/engine.cu.
+#include <cmath>
 #include <cstring>
 #include <memory>
 
@@ -11,7 +12,7 @@ namespace hk {
 thread_local std::string g_last_error;
 void set_error(const std::string& s) { g_last_error = s; }
 // Implemented in csrc/cuda/engine.cu.
-std::unique_ptr<LlmBody> make_device_body(hk_engine* e, const Plan& plan, const SimConfig& cfg);
+std::unique_ptr<LlmBody> make_device_body(hk_engine* e, const Plan& plan, const SimConfig& cfg, int only_worker);
 }  // namespace hk
 
 struct hk_run {
@@ -81,7 +82,7 @@ hk_run* hk_simulate_ex(const uint8_t* plan, size_t plan_len, const hk_sim_config
                 };
             }
             if (engine) {
-                std::unique_ptr<hk::LlmBody> body = hk::make_device_body(engine, p, sc);
+                std::unique_ptr<hk::LlmBody> body = hk::make_device_body(engine, p, sc, eo.only_worker);
                 run->m = hk::simulate(p, sc, *body, eo);
             } else {
                 hk::SyntheticBody body(sc.seed, sc.stochastic);
@@ -162,6 +163,17 @@ size_t hk_run_call_outputs(const hk_run* r, uint64_t* out, size_t cap) {
     }
     for (size_t i = 0; i < w.size() && i < cap; ++i) out[i] = w[i];
     return w.size();
+}
+
+size_t hk_run_call_logits(const hk_run* r, float* out, size_t cap) {
+    if (!r) return 0;
+    size_t n = 0;
+    for (const auto& [cid, toks] : r->m.call_outputs) {
+        auto it = r->m.call_logits.find(cid);
+        for (size_t i = 0; i < toks.size(); ++i, ++n)
+            if (n < cap) out[n] = it != r->m.call_logits.end() && i < it->second.size() ? it->second[i] : NAN;
+    }
+    return n;
 }
 
 int hk_run_timing(const hk_run* r, double out[2]) {

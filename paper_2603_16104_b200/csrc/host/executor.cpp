@@ -325,6 +325,10 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                 TokenSeq out;
                 if (dev) {
                     out = lc.out_len > 0 ? body.take_output(static_cast<int>(w), lc, len_out, det) : TokenSeq{};
+                    if (lc.out_len > 0) {
+                        std::vector<float> lv = body.take_logits(static_cast<int>(w), lc);
+                        if (!lv.empty()) m.call_logits[lc.id] = std::move(lv);
+                    }
                     if (replay && lc.out_len > 0) opts.exchange(static_cast<int>(w), lc.id, out);  // send
                 } else if (lc.out_len > 0) {
                     out.assign(lc.out_len, 0);

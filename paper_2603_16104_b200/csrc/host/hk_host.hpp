@@ -289,6 +289,7 @@ struct SimMetrics {
     std::map<NodeId, std::vector<TokenSeq>> outputs;
     // B200 additions (not part of the reference report)
     std::map<CallId, TokenSeq> call_outputs;        // every llm call's generated tokens
+    std::map<CallId, std::vector<float>> call_logits;  // device body: the logit of each generated token
     std::vector<std::uint64_t> pin_compute_tokens;  // per worker, pin precompute prefill
     std::uint64_t recompute_tokens = 0;             // fully-cached prompts: last position re-run
     double pin_seconds = 0, iter_seconds = 0;       // wall time: pin precompute, iteration loop
@@ -353,6 +354,8 @@ class LlmBody {
     virtual void on_admit(int /*w*/, LiveCall& /*lc*/) {}
     virtual void run_step(StepPlan& /*sp*/) {}
     virtual TokenSeq take_output(int w, LiveCall& lc, double len_out, bool det) = 0;
+    // the logit of each token take_output returned (device body only; called right after it)
+    virtual std::vector<float> take_logits(int /*w*/, LiveCall& /*lc*/) { return {}; }
     virtual void on_finish(int /*w*/, LiveCall& /*lc*/) {}
     virtual void finish_run() {}
 };

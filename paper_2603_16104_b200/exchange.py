@@ -60,14 +60,21 @@ def same_pins_everywhere(pins: List[List[int]], group=None) -> bool:
     return all(d == digests[0] for d in digests) and digests[0][1] > 0
 
 
+def global_rank(group_rank: int, group=None) -> int:
+    """torch.distributed's `src` is a global rank: map a rank of `group` to it."""
+    import torch.distributed as dist
+    return group_rank if group is None else dist.get_global_rank(group, group_rank)
+
+
 def make_broadcast_fn(src: int, device: str, group=None):
-    """The callback: broadcast the pin pages from rank `src` into every rank's buffer."""
+    """The callback: broadcast the pin pages from group rank `src` into every rank's buffer."""
     import torch
     import torch.distributed as dist
+    g_src = global_rank(src, group)
 
     def fn(worker: int, ptr: int, nbytes: int):
         t = buffer_tensor(ptr, nbytes, device)
-        dist.broadcast(t, src=src, group=group)
+        dist.broadcast(t, src=g_src, group=group)
         if device != "cpu":
             torch.cuda.synchronize()
 
@@ -98,11 +105,12 @@ def make_output_exchange(device: str = "cpu", group=None):
 
     def fn(worker: int, op: int, query: int, tokens):
         t = torch.from_numpy(tokens.view(np.int64))  # shares memory with the executor's buffer
+        src = global_rank(worker, group)  # worker w is owned by rank w of the group
         if device == "cpu":
-            dist.broadcast(t, src=worker, group=group)
+            dist.broadcast(t, src=src, group=group)
         else:
             d = t.to(device)
-            dist.broadcast(d, src=worker, group=group)
+            dist.broadcast(d, src=src, group=group)
             t.copy_(d.cpu())
 
     return fn

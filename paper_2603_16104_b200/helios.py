@@ -117,6 +117,7 @@ class SimMetrics:
     pin_seconds: float = 0.0
     iter_seconds: float = 0.0
     call_outputs: Dict[tuple, List[int]] = field(default_factory=dict)
+    call_logits: Dict[tuple, List[float]] = field(default_factory=dict)  # device logit of each generated token
 
 
 def _report(h, which: int) -> str:
@@ -169,6 +170,20 @@ def _call_outputs(h) -> Dict[tuple, List[int]]:
     return out
 
 
+def _call_logits(h, outs: Dict[tuple, List[int]]) -> Dict[tuple, List[float]]:
+    lib = _lib.load()
+    n = lib.hk_run_call_logits(h, None, 0)
+    buf = np.zeros(max(n, 1), dtype=np.float32)
+    lib.hk_run_call_logits(h, buf.ctypes.data_as(_lib.f32p), n)
+    res, i = {}, 0
+    for k in sorted(outs):  # same (op, query) order as hk_run_call_outputs
+        ln = len(outs[k])
+        if not np.isnan(buf[i:i + ln]).all():
+            res[k] = buf[i:i + ln].tolist()
+        i += ln
+    return res
+
+
 def simulate(plan: bytes, cfg: SimConfig, engine=None, verify_lookup: bool = False,
              only_worker: int = -1, exchange=None) -> SimMetrics:
     """simulate() (simulator.hpp:128-130) on a flattened HKPLAN01 plan.
@@ -219,7 +234,7 @@ def simulate(plan: bytes, cfg: SimConfig, engine=None, verify_lookup: bool = Fal
             evicted_tokens=_worker_stat(h, 1), outputs=_outputs(h), metrics_json=_report(h, 0),
             calls_csv=_report(h, 1), trace_csv=_report(h, 2), recompute_tokens=mc.recompute_tokens,
             pin_compute_tokens=_worker_stat(h, 2), pin_seconds=t[0], iter_seconds=t[1],
-            call_outputs=_call_outputs(h))
+            call_outputs=(co := _call_outputs(h)), call_logits=_call_logits(h, co))
     finally:
         lib.hk_run_free(h)
 

@@ -96,6 +96,13 @@ def main():
     emit("t_press", wf, i, p, dict(s, pin_threshold=64), "8 branches, 256-token prefix, 1K cache (eviction)")
 
 
+def main_model_parity():
+    """configs[1] with 16 decode tokens: the Llama-width bf16 token-parity run
+    (tests/test_gpu_parity.py), short enough for the CPU oracle."""
+    wf, i, p, s = wl.c2_branches(decode=16)
+    emit("c2_d16", wf, i, p, s, "configs[1] with 16 decode tokens (model parity at Llama width)", full_outputs=False)
+
+
 def main_cross_worker():
     """Multi-worker plans whose calls wait on calls of another worker (SURVEY
     §8(e) exchange 2): the tiny map-reduce and the reflect workload on 2 workers."""
@@ -110,5 +117,7 @@ def main_cross_worker():
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "cross_worker":
         main_cross_worker()
+    elif len(sys.argv) > 1 and sys.argv[1] == "model_parity":
+        main_model_parity()
     else:
         main()

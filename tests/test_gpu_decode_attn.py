@@ -173,3 +173,64 @@ def test_prefill_attention_matches_causal_fp32_reference(H, Hkv, n, start):
     err = (out.float() - ref).abs().amax(dim=(1, 2))
     bad = (err > 1e-2 * ref.abs().max()).nonzero().flatten().tolist()
     assert not bad, (bad[:10], err.max().item())
+
+
+def _causal_ref(q_rows, kv, table, start, H, Hkv):
+    n = q_rows.shape[0]
+    G = H // Hkv
+    pages = torch.tensor(table, device="cuda", dtype=torch.long)
+    k = kv[pages, 0].float().permute(1, 0, 2, 3).reshape(Hkv, -1, HD)
+    v = kv[pages, 1].float().permute(1, 0, 2, 3).reshape(Hkv, -1, HD)
+    q = q_rows[:, :H * HD].float().view(n, Hkv, G, HD)
+    s = torch.einsum("thgd,hkd->thgk", q, k) / np.sqrt(HD)
+    keys = torch.arange(k.shape[1], device="cuda")
+    pos = start + torch.arange(n, device="cuda")
+    s = s.masked_fill((keys[None, :] > pos[:, None])[:, None, None, :], float("-inf"))
+    return torch.einsum("thgk,hkd->thgd", torch.softmax(s, dim=-1), v).reshape(n, H, HD)
+
+
+# (H, Hkv, common pages, suffix tokens per segment, segments): the configs[1] shape
+# (G=4: 32-row tiles, 2,048-token pinned prefix = 128 pages), configs[4]'s G=5
+# (25-row tiles), and common prefixes that are not a multiple of the 8-page chunk
+PAIR_CASES = [(32, 8, 128, [16, 16, 16, 16], 4), (32, 8, 37, [20, 27], 2), (40, 8, 77, [25, 11, 25], 3),
+              (40, 8, 9, [7, 25], 2), (2, 1, 12, [60, 33, 64], 3)]
+
+
+@pytest.mark.parametrize("H,Hkv,common,suffix,nseg", PAIR_CASES)
+def test_prefill_paired_suffix_segments_match_causal_reference(H, Hkv, common, suffix, nseg):
+    """The engine's paired-suffix prefill (plan_prefill_attention with the arena):
+    calls of one operator admitted together prefill their suffixes under a
+    common cached prefix; two single-tile segments with >= 8 common leading
+    pages share one CTA pair (common pages multicast, own pages per CTA).
+    Every segment must equal its own causal fp32 attention."""
+    g = torch.Generator(device="cpu").manual_seed(H * 1000 + common * 7 + nseg)
+    pre = common * PG
+    n_pages = common + sum((s + PG) // PG + 1 for s in suffix) + 8
+    perm = torch.randperm(n_pages, generator=g).tolist()
+    common_pages, nxt = perm[:common], common
+    arena, tok0, counts, starts, ptabs = [], [], [], [], []
+    t = 0
+    for s in suffix[:nseg]:
+        own = (pre + s + PG - 1) // PG - common
+        ptabs.append(len(arena))
+        arena += common_pages + perm[nxt:nxt + own]
+        nxt += own
+        tok0.append(t)
+        counts.append(s)
+        starts.append(pre)
+        t += s
+    kv = (torch.randn(n_pages, 2, Hkv, PG, HD, generator=g) * 0.5).to(torch.bfloat16).cuda()
+    qkv = torch.randn(t, (H + 2 * Hkv) * HD, generator=g).to(torch.bfloat16).cuda()
+    out = torch.zeros(t, H, HD, dtype=torch.bfloat16, device="cuda")
+    a = [_i32(x) for x in (tok0, counts, starts, ptabs, arena)]
+    rc = _lib.load().hkx_prefill_attention_segs(C.c_void_p(qkv.data_ptr()), C.c_void_p(kv.data_ptr()), n_pages, nseg,
+                                                a[0][1], a[1][1], a[2][1], a[3][1], H, Hkv, a[4][1], len(arena), t,
+                                                C.c_void_p(out.data_ptr()))
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    for s in range(nseg):
+        rows = slice(tok0[s], tok0[s] + counts[s])
+        table = arena[ptabs[s]:ptabs[s] + (starts[s] + counts[s] + PG - 1) // PG]
+        ref = _causal_ref(qkv[rows], kv, table, starts[s], H, Hkv)
+        err = (out[rows].float() - ref).abs().max().item()
+        assert err <= 1e-2 * ref.abs().max().item(), (s, err)

@@ -153,13 +153,18 @@ def test_pool_gather_scatter_copy():
 
 # -------------------------------------------------------------- transformer
 def _check_generation(model, prompt, n_new, rel_tol, eng_cfg=None):
-    from oracle.transformer import Decoder, top2_margin
+    """hk_generate with full logits vs the oracle teacher-forced on the device's
+    ids: every logit within rel_tol of max |logit|; a device choice that is not
+    the oracle's argmax must sit inside the measured error band (oracle gap <=
+    2 x the largest logit error of the run). Returns the exact-match count."""
+    from oracle.transformer import Decoder
     eng = Engine(model, eng_cfg or EngineConfig(pages_per_worker=256, max_calls=8, max_step_tokens=1024,
                                                 max_ctx_tokens=4096))
     toks, logits = eng.generate(prompt, n_new, want_logits=True)
     eng.close()
     dec = Decoder(model, max_pos=4096)
     ref_toks, ref_logits = dec.generate(prompt, n_new, forced=list(toks))
+    delta = max(float(np.abs(gl - rl).max()) for gl, rl in zip(logits, ref_logits))
     exact = 0
     for k in range(n_new):
         rl, gl = ref_logits[k], logits[k]
@@ -168,8 +173,7 @@ def _check_generation(model, prompt, n_new, rel_tol, eng_cfg=None):
         if ref_toks[k] == toks[k]:
             exact += 1
         else:
-            # only a near-tie of the oracle's top two may flip
-            assert top2_margin(rl) < 4 * rel_tol * np.abs(rl).max(), (k, toks[k], ref_toks[k])
+            assert rl[ref_toks[k]] - rl[toks[k]] <= 2 * delta, (k, toks[k], ref_toks[k])
     return exact
 
 
@@ -194,3 +198,43 @@ def test_generate_llama_shape_reduced_depth_matches_oracle():
     prompt = rng.integers(0, m.vocab, size=150).tolist()
     exact = _check_generation(m, prompt, 6, 1e-2)
     assert exact >= 5
+
+
+@pytest.mark.parametrize("T", [1, 17, 64])
+def test_lm_head_streamk_argmax_at_llama_vocab(T):
+    """The LM head of every decode step: V = 128,256 (1,002 vocab tiles >= one
+    wave of 148 SMs, T <= 64) routes to the stream-K kernel (gemm_sk_kernel,
+    gemm.cu gemm_bf16) with the fused (max, argmax) epilogue. Checked against a
+    torch fp32 matmul of the same bf16 operands: every tile's max within 1e-5
+    relative, its index exact where the tile's top two are not a near-tie, and
+    the row argmax over the tiles equal to torch's; plus run-to-run determinism."""
+    lib = _lib.load()
+    V, K = 128256, 4096
+    g = torch.Generator(device="cuda").manual_seed(1000 + T)
+    W = ((torch.rand(V, K, device="cuda", generator=g) * 2 - 1) * (3.0 / K) ** 0.5).to(torch.bfloat16)
+    X = (torch.rand(T, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    ref = X.float() @ W.float().t()
+    nt = (V + 127) // 128
+    part = torch.zeros(nt, T, 2, device="cuda")
+    assert lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(part), V, K, T, 5, None, 0, None) == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    pad = torch.full((T, nt * 128 - V), -float("inf"), device="cuda")
+    lv = torch.cat([ref, pad], dim=1).view(T, nt, 128)
+    mx, ix = lv.max(dim=-1)
+    scale = ref.abs().max().item()
+    assert (part[..., 0].t() - mx).abs().max().item() <= 1e-5 * scale
+    idx = part[..., 1].contiguous().view(torch.int32).t().long()
+    top2 = lv.topk(2, dim=-1).values
+    clear = (top2[..., 0] - top2[..., 1]) > 1e-4 * scale
+    assert torch.equal(idx[clear], (ix + torch.arange(nt, device="cuda") * 128)[clear])
+    # row argmax over the tile partials (what argmax_reduce computes) == torch's
+    best = part[..., 0].t().argmax(dim=1)
+    rows = torch.arange(T, device="cuda")
+    dev_ids = idx[rows, best]
+    top2r = ref.topk(2, dim=1).values
+    clear_r = (top2r[:, 0] - top2r[:, 1]) > 1e-4 * scale
+    assert torch.equal(dev_ids[clear_r], ref.argmax(dim=1)[clear_r])
+    part2 = torch.zeros_like(part)
+    assert lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(part2), V, K, T, 5, None, 0, None) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(part, part2)
