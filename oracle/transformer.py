@@ -14,6 +14,7 @@ fp32 here; the device's accumulation order differs, hence the tolerances
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
@@ -37,20 +38,17 @@ def round_bf16(v: np.ndarray) -> np.ndarray:
     return b.astype(np.uint32).view(np.float32)
 
 
-def init_uniform(n: int, seed: int, tid: int, scale: float, bf16: bool, chunk: int = 1 << 16) -> np.ndarray:
-    """Mirror of init_uniform_kernel (ops.cu). Cache-sized chunks with in-place
-    uint64 arithmetic (about 2.5x faster than whole-array temporaries)."""
+def _init_range(out: np.ndarray, lo: int, hi: int, base: np.uint64, scale: float, bf16: bool, chunk: int) -> None:
+    """splitmix64 counter init of out[lo:hi] in cache-sized chunks, in-place uint64 arithmetic."""
     with np.errstate(over="ignore"):
-        base = np.uint64((seed * 0xD1B54A32D192ED03 + tid * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF)
-        out = np.empty(n, dtype=np.float32)
         ar = np.arange(chunk, dtype=np.uint64)
         x = np.empty(chunk, dtype=np.uint64)
         t = np.empty(chunk, dtype=np.uint64)
         c1, c2, c3 = np.uint64(0x9E3779B97F4A7C15), np.uint64(0xBF58476D1CE4E5B9), np.uint64(0x94D049BB133111EB)
         s30, s27, s31, s40 = np.uint64(30), np.uint64(27), np.uint64(31), np.uint64(40)
         sc = np.float32(scale)
-        for s in range(0, n, chunk):
-            e = min(n, s + chunk)
+        for s in range(lo, hi, chunk):
+            e = min(hi, s + chunk)
             m = e - s
             xv, tv = x[:m], t[:m]
             np.add(ar[:m], base + np.uint64(s) + c1, out=xv)          # splitmix64(base + i)
@@ -61,6 +59,23 @@ def init_uniform(n: int, seed: int, tid: int, scale: float, bf16: bool, chunk: i
             u = xv.astype(np.float32) * np.float32(1.0 / 8388608.0) - np.float32(1.0)
             v = u * sc
             out[s:e] = round_bf16(v) if bf16 else v
+
+
+def init_uniform(n: int, seed: int, tid: int, scale: float, bf16: bool, chunk: int = 1 << 16) -> np.ndarray:
+    """Mirror of init_uniform_kernel (ops.cu): w[i] = scale * ((splitmix64(base + i) >> 40) * 2^-23 - 1),
+    base = seed * C1 + tid * C2. Large tensors are filled by all host threads
+    (numpy releases the GIL inside these ufuncs)."""
+    base = np.uint64((seed * 0xD1B54A32D192ED03 + tid * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF)
+    out = np.empty(n, dtype=np.float32)
+    workers = min(os.cpu_count() or 1, 32)
+    if n < (1 << 22) or workers == 1:
+        _init_range(out, 0, n, base, scale, bf16, chunk)
+        return out
+    from concurrent.futures import ThreadPoolExecutor
+    step = -(-n // workers)
+    step = -(-step // chunk) * chunk
+    with ThreadPoolExecutor(workers) as ex:
+        list(ex.map(lambda lo: _init_range(out, lo, min(n, lo + step), base, scale, bf16, chunk), range(0, n, step)))
     return out
 
 
@@ -157,15 +172,15 @@ class Decoder:
             S = K.shape[0]
             o = np.empty((T, H, hd), np.float32)
             kpos = np.arange(S)
+            mask = kpos[None, None, :] > pos[:, None, None]
             for g in range(Hkv):
-                qg = q[:, g * G:(g + 1) * G, :]                        # T,G,hd
-                sc = np.einsum("tgd,sd->tgs", qg, K[:, g, :]) * scale  # T,G,S
-                mask = kpos[None, None, :] > pos[:, None, None]
+                qg = q[:, g * G:(g + 1) * G, :].reshape(T * G, hd)          # (T G), hd
+                sc = (qg @ K[:, g, :].T).reshape(T, G, S) * scale           # T,G,S (BLAS)
                 sc = np.where(mask, -np.inf, sc)
                 sc = sc - sc.max(axis=-1, keepdims=True)
                 p = np.exp(sc)
                 p = p / p.sum(axis=-1, keepdims=True)
-                o[:, g * G:(g + 1) * G, :] = np.einsum("tgs,sd->tgd", p.astype(np.float32), Vv[:, g, :])
+                o[:, g * G:(g + 1) * G, :] = (p.astype(np.float32).reshape(T * G, S) @ Vv[:, g, :]).reshape(T, G, hd)
             o = self._r(o.reshape(T, H * hd))
             x = x + (o @ lw["wo"].T)
             h = self._r(self._rms(x))

@@ -47,9 +47,11 @@ struct KernelClock {
         int fam;
         double bytes;
     };
-    static constexpr int kFamilies = 8;
+    static constexpr int kFamilies = 9;
+    // gemm: weight-streaming GEMMs (<= 192 rows, bytes = weights + inputs); gemm_prefill:
+    // tensor-bound GEMMs (> 192 rows, "bytes" = FLOPs)
     const char* names[kFamilies] = {"gemm", "attn_shared", "attn_private", "attn_prefill",
-                                    "attn_merge", "small", "trie", "kvcopy"};
+                                    "attn_merge", "small", "trie", "kvcopy", "gemm_prefill"};
     double ms[kFamilies] = {0};
     double bytes[kFamilies] = {0};
     uint64_t launches[kFamilies] = {0};
@@ -733,6 +735,7 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     // schedule is unchanged) to measure what a perfect fusion of it could save
     static const std::string skip_env = std::getenv("HK_DEBUG_SKIP") ? std::getenv("HK_DEBUG_SKIP") : "";
     auto skip = [&](const char* fam) { return !skip_env.empty() && skip_env.find(fam) != std::string::npos && !dec.empty(); };
+    hkd::g_trace_prefill_rows = T_pre;
     auto enqueue = [&]() {
     int ck = clock.begin(5, st);
     hkd::embed(embed, f32, d, d_ids, d_slots, wk.slot_last, T, x, st);
@@ -740,7 +743,8 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     clock.end(ck, st, static_cast<double>(T) * d * (esz + 4));
     // GEMMs into fp32 split-K partials (consumers reduce them), or fused epilogues
     auto gemm = [&](const void* W, const void* X, int N, int K, int rows, int epi, void* out, int ldo) -> int {
-        const int c = clock.begin(0, st);
+        const bool tensor_bound = rows > 192;
+        const int c = clock.begin(tensor_bound ? 8 : 0, st);
         int sp = 1;
         if (f32) {
             hkd::gemm_f32(static_cast<const float*>(W), static_cast<const float*>(X), N, K, rows,
@@ -750,7 +754,7 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
             sp = hkd::gemm_bf16(static_cast<const bf16*>(W), static_cast<const bf16*>(X), N, K, rows, epi, out, ldo,
                                 nullptr, ws, ws_floats, st, 0, max_sp);
         }
-        clock.end(c, st, static_cast<double>(N) * K * esz + static_cast<double>(rows) * K * esz);
+        clock.end(c, st, tensor_bound ? 2.0 * N * K * rows : static_cast<double>(N) * K * esz + static_cast<double>(rows) * K * esz);
         return sp;
     };
     for (int l = 0; l < L; ++l) {

@@ -486,12 +486,13 @@ namespace {
 struct GemmTrace {
     unsigned long long* d = nullptr;
     int n = 0, cap = 0;
-    std::vector<std::array<int, 5>> meta;  // N, K, T, splits, grid CTAs
+    std::vector<std::array<int, 6>> meta;  // N, K, T, splits, grid CTAs, prefill rows of the step
 };
 GemmTrace g_gtrace;
 }  // namespace
 
 bool g_span_trace = std::getenv("HK_GEMM_TRACE") != nullptr;  // also hkx_span_trace(1)
+int g_trace_prefill_rows = 0;
 
 void span_trace_reset(bool on) {
     g_span_trace = on;
@@ -508,7 +509,7 @@ unsigned long long* gemm_trace_slot(int N, int K, int T, int splits, int ctas) {
         HK_CUDA(cudaMemset(g_gtrace.d, 0xff, static_cast<size_t>(g_gtrace.cap) * 4 * 8));
     }
     if (g_gtrace.n >= g_gtrace.cap) return nullptr;
-    g_gtrace.meta.push_back({N, K, T, splits, ctas});
+    g_gtrace.meta.push_back({N, K, T, splits, ctas, g_trace_prefill_rows});
     return g_gtrace.d + 4 * static_cast<size_t>(g_gtrace.n++);
 }
 
@@ -519,11 +520,11 @@ int gemm_trace_dump(const char* path) {
     HK_CUDA(cudaMemcpy(h.data(), g_gtrace.d, h.size() * 8, cudaMemcpyDeviceToHost));
     FILE* f = std::fopen(path, "w");
     if (!f) return -1;
-    std::fprintf(f, "slot,N,K,T,splits,ctas,start,wait_done,end,mainloop_end\n");
+    std::fprintf(f, "slot,N,K,T,splits,ctas,start,wait_done,end,mainloop_end,prefill_rows\n");
     for (int i = 0; i < g_gtrace.n; ++i) {
         const auto& m = g_gtrace.meta[static_cast<size_t>(i)];
-        std::fprintf(f, "%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu\n", i, m[0], m[1], m[2], m[3], m[4], h[4 * i], h[4 * i + 1],
-                     ~h[4 * i + 2], ~h[4 * i + 3]);
+        std::fprintf(f, "%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d\n", i, m[0], m[1], m[2], m[3], m[4], h[4 * i],
+                     h[4 * i + 1], ~h[4 * i + 2], ~h[4 * i + 3], m[5]);
     }
     std::fclose(f);
     return g_gtrace.n;

@@ -34,6 +34,7 @@ int gemm_trace_dump(const char* path);
 // debug (HK_GEMM_TRACE): a span slot [first CTA start, first wait exit, ~last end, ~last main-loop end]
 // for one launch; N = -1 marks a decode-attention launch (K = its algorithmic KB)
 unsigned long long* gemm_trace_slot(int N, int K, int T, int splits, int ctas);
+extern int g_trace_prefill_rows;  // recorded with every trace slot: prefill rows of the step being enqueued
 // (re)start span tracing (clears the slots); on = false stops it
 void span_trace_reset(bool on);
 // allocate the stream-K workspace/counters ahead of any CUDA-graph capture

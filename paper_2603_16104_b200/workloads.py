@@ -208,3 +208,29 @@ def sim_config_from_meta(meta: dict):
         proactive_pin=sc["proactive_pin"], pin_threshold=sc["pin_threshold"],
         pin_capacity_frac=sc["pin_capacity_frac"], seed=sc["seed"], stochastic=sc["stochastic"],
         collect_trace=sc.get("collect_trace", False), max_iterations=sc.get("max_iterations", 0))
+
+
+def engine_sizing(blob: bytes, sc) -> dict:
+    """Engine limits for a plan, from the executor's own synthetic-mode run
+    (mode S: the reference's control plane with synth_llm_output, no device):
+    the most calls live in one iteration on one worker, the longest call
+    context (prompt + output), and the most private (uncached prompt + output)
+    tokens of a call."""
+    from .helios import simulate
+    m = simulate(blob, sc)
+    rows = [list(map(int, r.split(","))) for r in m.calls_csv.strip().split("\n")[1:]]
+    # op,query,worker,admitted_iter,prefill_done_iter,completed_iter,prompt_tokens,cached_tokens,output_tokens
+    events = {}
+    for r in rows:
+        events.setdefault(r[2], []).append((r[3], 1))
+        events[r[2]].append((r[5] + 1, -1))
+    max_live = 0
+    for ev in events.values():
+        live = 0
+        for _, dlt in sorted(ev):
+            live += dlt
+            max_live = max(max_live, live)
+    return {"max_live": max_live,
+            "max_ctx": max((r[6] + r[8] for r in rows), default=0),
+            "max_private": max((r[6] - r[7] + r[8] for r in rows), default=0),
+            "decode_tokens": m.decode_tokens}
