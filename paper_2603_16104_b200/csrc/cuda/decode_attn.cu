@@ -1,36 +1,39 @@
-// K3b: prefix-shared paged decode attention (bf16), the attention of every
+// K3b: prefix-shared paged decode attention (bf16) — the attention of every
 // decode token of one (iteration, worker) step of the reference's simulate()
-// loop (simulator.cpp:347-374: one token per running call per iteration).
+// loop (simulator.cpp:347-374: one token per running call per iteration) —
+// and, on the same tile path, the causal prefill of K3a (:331-343).
 //
-// Decode rows that share a block-table prefix (branches of one shared prompt,
-// e.g. the 2,048-token pinned system prompt of configs[1]) form a group. Per
-// layer and kv head the group's rows are (token, q-head) pairs — G = H / Hkv
-// of them per token — so 128/G tokens fill one 128-row tcgen05 tile:
+// ONE persistent launch per layer (attn_decode_kernel<G>): one CTA per SM,
+// 320 threads, CTAs paired in clusters of 2.
 //
-//   shared item  (attn_shared_tc_kernel): S = Q K^T and O = P V on the tensor
-//                cores for 128 rows x a range of shared pages. K/V pages are
-//                staged by TMA (128B swizzle) straight from the paged pool,
-//                Q is written swizzled by the CTA, S and O live in TMEM, the
-//                softmax warps read S with tcgen05.ld (one thread per row) and
-//                write P (bf16) back to shared memory as the A operand of PV;
-//                V is consumed MN-major, as it lies in the page. The shared KV
-//                is read once for all rows of the tile instead of once per row.
-//   private item (attn_private_kernel): one token x one kv head over its own
-//                pages (prompt suffix + generated tokens): a GEMV-shaped flash
-//                loop on the CUDA cores, whole 4 KB K and V page halves staged
-//                by 1D bulk async copies (cp.async.bulk) into an 8-deep
-//                mbarrier ring, 8 lanes x 16 dims per key, 8-lane shuffles.
-//
-// The shared items that split one tile's pages form a thread-block cluster:
-// they exchange row maxima and reduce their O tiles through distributed shared
-// memory, so a tile leaves ONE flash partial (m, l, unnormalised o; log2
-// domain) per row however many SMs streamed its pages. Private items leave
-// one partial each. A per-(decode row, kv head) arrival counter picks the last
-// contributor, which merges the row's partials and writes the bf16 attention
-// output — there is no separate merge launch. The private kernel runs first and lets
-// the shared kernel launch as soon as every private CTA has started (PDL);
-// the shared kernel waits for the private grid only before exiting, so the
-// next kernel's griddepcontrol.wait covers both.
+//   shared items  decode rows that share a block-table prefix (the branches
+//                 of one pinned system prompt, e.g. configs[1]'s 2,048 tokens)
+//                 are (token, q-head) pairs of one kv head — 128/G tokens fill
+//                 a 128-row tcgen05 tile. A tile's prefix pages are split over
+//                 S CTAs (planner: ~64 shared CTAs for a <= 2K prefix). Warp 9
+//                 streams K/V straight from the paged pool with TMA (128B
+//                 swizzle, a 3-stage K ring and a 2-stage V ring, started
+//                 before griddepcontrol.wait: old pages do not depend on this
+//                 step); the two tiles of a kv head form the CTA pair and each
+//                 page is fetched once and multicast into both. Warp 8 issues
+//                 S = Q K^T into two TMEM buffers and O += P V with P read
+//                 from TMEM; 8 softmax warps (two threads per row) do the
+//                 online softmax with a lazy O rescale. Output: the row
+//                 normalised to bf16 + (m, l), one partial per item.
+//   private items every decode row's own pages (prompt suffix + generated
+//                 tokens) per kv head, as key ranges sized for one round on
+//                 the free warps; each warp pulls items from a global queue,
+//                 feeds itself a 3-deep TMA page ring and runs mma.sync
+//                 m16n8k16 with swapped operands (keys / head dims are the
+//                 16-row M side, the G q-heads the 8-wide N side).
+//   merge         after a grid-wide arrival (all CTAs co-resident: grid <=
+//                 SMs), every SM merges rows (merge16: w_p = l_p 2^(m_p - M));
+//                 a row with a single item is written directly. A grid larger
+//                 than the SM count falls back to a separate merge launch.
+//   prefill tiles causal tiles (rows = prompt tokens x G heads, keys [0, pos])
+//                 paired so the later row block's pages serve both CTAs; two
+//                 single-tile segments under a common prefix share a pair
+//                 (common pages multicast, own pages per CTA).
 #include <algorithm>
 #include <array>
 #include <cfloat>
@@ -56,16 +59,6 @@ constexpr int ROWS = 128;     // MMA rows of a shared item
 // w_p with w_p = l_p 2^(m_p - max m).
 
 __device__ __forceinline__ bf16* part_bf16(const DecodeAttnArgs& a) { return reinterpret_cast<bf16*>(a.part_o); }
-
-// Arrival on a (row, kv head) counter: release orders this thread's partial
-// stores (after a warp/CTA barrier, those of its peers too, by cumulativity)
-// before the increment; acquire makes the other contributors' partials
-// visible to the thread that arrives last.
-__device__ __forceinline__ int arrive_acq_rel(int32_t* ctr) {
-    int old;
-    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
-    return old;
-}
 
 // per-chunk clock64 stamps of thread 0 (softmax) and the MMA issuer, chunks < 8 (debug trace)
 __device__ __forceinline__ void cstamp(const DecodeAttnArgs& a, int c, int k) {
@@ -151,17 +144,6 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// 2^x on the FMA/ALU pipes: 2^floor(x) * p(frac(x)), p a degree-3 minimax
-// polynomial for 2^f on [0, 1) (max rel. error ~9e-5, well inside the bf16
-// rounding P gets next); x = -inf gives 0.
-__device__ __forceinline__ float ex2_poly(float x) {
-    x = fmaxf(x, -127.f);
-    const float xi = floorf(x);
-    const float f = x - xi;
-    const float p = fmaf(f, fmaf(f, fmaf(f, 0.077119089663028717f, 0.227564394474029541f), 0.695146143436431885f), 1.0f);
-    return __int_as_float(__float_as_int(p) + (static_cast<int>(xi) << 23));
-}
-
 template <int G>
 __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const DecodeAttnArgs& a, uint8_t* sm) {
     uint8_t* sQ = sm;

@@ -487,7 +487,6 @@ void hk_engine::harvest(bool all) {
 void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     Worker& wk = workers[static_cast<size_t>(w)];
     const int block = static_cast<int>(ec.block_tokens);
-    const int G = H / Hkv;
 
     // order: prefill/recompute segs first, decode segs grouped by table prefix
     std::vector<int> pre, dec;
