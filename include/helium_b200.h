@@ -139,6 +139,13 @@ void hk_kv_destroy(hk_kvcache* c);
  * (lens_cap). Returns the number of pins, or -1. */
 int64_t hk_static_pin_prefixes(const uint8_t* plan, size_t plan_len, int worker, size_t block, size_t threshold,
                                size_t budget_tokens, uint64_t* tokens, size_t cap, uint64_t* lens, size_t lens_cap);
+/* The plan's TRT shared-prefix groups (trt.cpp:489-530), one per llm call in
+ * (op, query) order: the deepest call-tree ancestor whose whole root path is
+ * static text (-1: none) and that static path's token length. The decode
+ * planner groups prefix-shared attention rows by it. Returns the call count
+ * (copies min(count, cap)) or -1. */
+int64_t hk_plan_call_groups(const uint8_t* plan, size_t plan_len, int64_t* op, int32_t* query, int32_t* group,
+                            uint64_t* tokens, size_t cap);
 
 /* --------------------------------------------------------- LLM body (synth) */
 /* synth_llm_len / synth_llm_output (evaluator.hpp:29-32). */

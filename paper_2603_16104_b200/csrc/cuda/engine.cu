@@ -246,6 +246,8 @@ struct hk_engine {
         int slot = -1;
         int start = 0, count = 0;
         bool from_prompt = true, write_kv = true, sample = false;
+        int group = -1;        // TRT static group (decode): Plan::static_group of the call's leaf
+        int group_pages = 0;   // full pages of that group's static prefix
         const std::vector<int>* table = nullptr;
         const std::vector<uint64_t>* prompt = nullptr;  // host tokens (Token space)
         const std::vector<uint32_t>* ids = nullptr;     // or raw vocab ids
@@ -488,16 +490,26 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     Worker& wk = workers[static_cast<size_t>(w)];
     const int block = static_cast<int>(ec.block_tokens);
 
-    // order: prefill/recompute segs first, decode segs grouped by table prefix
-    std::vector<int> pre, dec;
-    for (int i = 0; i < static_cast<int>(segs.size()); ++i) (segs[i].from_prompt ? pre : dec).push_back(i);
+    // order: prefill/recompute segs first, then decode segs: rows of a TRT
+    // static group (the plan's call-level tree, trt.cpp:489-530) together, in
+    // admission order; rows without one are grouped by block-table prefix
+    std::vector<int> pre, dec, dec_free;
+    for (int i = 0; i < static_cast<int>(segs.size()); ++i) {
+        if (segs[i].from_prompt)
+            pre.push_back(i);
+        else
+            (segs[i].group >= 0 ? dec : dec_free).push_back(i);
+    }
     auto full_pages = [&](const SegIn& s) { return (s.start) / block; };  // pages strictly before the decode token
-    std::sort(dec.begin(), dec.end(), [&](int a, int b) {
+    std::stable_sort(dec.begin(), dec.end(), [&](int a, int b) { return segs[a].group < segs[b].group; });
+    std::sort(dec_free.begin(), dec_free.end(), [&](int a, int b) {
         const auto& ta = *segs[a].table;
         const auto& tb = *segs[b].table;
         const int na = full_pages(segs[a]), nb = full_pages(segs[b]);
         return std::lexicographical_compare(ta.begin(), ta.begin() + na, tb.begin(), tb.begin() + nb);
     });
+    const size_t n_trt_rows = dec.size();
+    dec.insert(dec.end(), dec_free.begin(), dec_free.end());
     std::vector<int> order = pre;
     order.insert(order.end(), dec.begin(), dec.end());
 
@@ -575,15 +587,33 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     while (gi < dec.size()) {
         size_t gj = gi + 1;
         int lcp = full_pages(segs[dec[gi]]);
-        while (gj < dec.size()) {
-            const auto& a = *segs[dec[gi]].table;
-            const auto& b = *segs[dec[gj]].table;
-            int n = std::min(lcp, full_pages(segs[dec[gj]]));
-            int k = 0;
-            while (k < n && a[static_cast<size_t>(k)] == b[static_cast<size_t>(k)]) ++k;
-            if (k < 4) break;  // require at least one shared 64-key tile
-            lcp = k;
-            ++gj;
+        if (gi < n_trt_rows) {
+            // TRT group: the members are known from the plan; the shared pages are the
+            // group's static prefix, trimmed to what the members' tables really share
+            // (a prefix block evicted and recomputed privately is not shared)
+            const int g = segs[dec[gi]].group;
+            lcp = std::min(lcp, segs[dec[gi]].group_pages);
+            while (gj < n_trt_rows && segs[dec[gj]].group == g) {
+                const auto& a = *segs[dec[gi]].table;
+                const auto& b = *segs[dec[gj]].table;
+                const int n = std::min(lcp, full_pages(segs[dec[gj]]));
+                int k = 0;
+                while (k < n && a[static_cast<size_t>(k)] == b[static_cast<size_t>(k)]) ++k;
+                lcp = k;
+                ++gj;
+            }
+            if (lcp < 4) lcp = 0;  // under one 64-key tile: no shared part
+        } else {
+            while (gj < dec.size()) {
+                const auto& a = *segs[dec[gi]].table;
+                const auto& b = *segs[dec[gj]].table;
+                int n = std::min(lcp, full_pages(segs[dec[gj]]));
+                int k = 0;
+                while (k < n && a[static_cast<size_t>(k)] == b[static_cast<size_t>(k)]) ++k;
+                if (k < 4) break;  // require at least one shared 64-key tile
+                lcp = k;
+                ++gj;
+            }
         }
         const int members = static_cast<int>(gj - gi);
         const int shared_pages = members > 1 ? lcp : 0;
@@ -1109,6 +1139,8 @@ class DeviceBody : public LlmBody {
             in.from_prompt = s.from_prompt;
             in.write_kv = s.write_kv;
             in.sample = s.sample;
+            in.group = s.group;
+            in.group_pages = static_cast<int>(s.group_tokens / static_cast<std::size_t>(e_->ec.block_tokens));
             in.table = &s.table;
             in.prompt = &s.call->prompt;
             segs.push_back(in);

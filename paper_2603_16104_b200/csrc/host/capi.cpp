@@ -221,6 +221,26 @@ int64_t hk_static_pin_prefixes(const uint8_t* plan, size_t plan_len, int worker,
         int64_t{-1});
 }
 
+int64_t hk_plan_call_groups(const uint8_t* plan, size_t plan_len, int64_t* op, int32_t* query, int32_t* group,
+                            uint64_t* tokens, size_t cap) {
+    return guard(
+        [&]() -> int64_t {
+            hk::Plan p = hk::parse_plan(plan, plan_len);
+            size_t i = 0;
+            for (const auto& [cid, leaf] : p.leaf_index) {
+                if (i < cap) {
+                    op[i] = cid.op;
+                    query[i] = cid.query;
+                    group[i] = p.static_group[static_cast<size_t>(leaf)];
+                    tokens[i] = p.static_group_tokens[static_cast<size_t>(leaf)];
+                }
+                ++i;
+            }
+            return static_cast<int64_t>(i);
+        },
+        int64_t{-1});
+}
+
 size_t hk_synth_llm_len(const uint64_t* p, size_t n, double len_out, int det, uint64_t seed, int stochastic) {
     return guard([&]() { return hk::synth_llm_len(hk::TokenSeq(p, p + n), len_out, det != 0, seed, stochastic != 0); },
                  size_t{0});

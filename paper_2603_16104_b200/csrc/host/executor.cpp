@@ -208,6 +208,8 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                     LiveCall& lc = *lcp;
                     lc.id = call;
                     lc.leaf = plan.leaf(call.op, call.query);
+                    lc.group = plan.static_group[static_cast<std::size_t>(lc.leaf)];
+                    lc.group_tokens = plan.static_group_tokens[static_cast<std::size_t>(lc.leaf)];
                     lc.prompt = std::move(prompts[k]);
                     lc.out_len = synth_llm_len(lc.prompt, ev.profile_len_out(call.op), ev.deterministic(call.op),
                                                cfg.seed, cfg.stochastic);
@@ -315,6 +317,8 @@ SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const
                         s.count = 1;
                         s.from_prompt = false;
                         s.sample = lc.decoded < lc.out_len;
+                        s.group = lc.group;
+                        s.group_tokens = lc.group_tokens;
                         s.table = lc.pages;
                         sp.segs.push_back(std::move(s));
                     }

@@ -91,6 +91,14 @@ struct Plan {
     std::vector<int> leaves;
     std::map<CallId, int> leaf_index;
     std::vector<std::vector<CallId>> sigma;
+    // Shared-prefix groups from the call-level TRT (trt.cpp:489-530), per tree
+    // node: for a leaf, the deepest ancestor whose whole root path is static
+    // text (-1: none) and the token length of that static path. Leaves with
+    // the same group share those prompt tokens, hence (when cached) the same
+    // KV pages: the decode-attention planner takes its prefix-shared groups
+    // from here instead of rediscovering them from block tables every step.
+    std::vector<int> static_group;
+    std::vector<std::size_t> static_group_tokens;
 
     const Token* span_ptr(std::int64_t s) const { return pool.data() + spans.at(static_cast<std::size_t>(s)).first; }
     std::size_t span_len(std::int64_t s) const { return spans.at(static_cast<std::size_t>(s)).second; }
@@ -309,6 +317,8 @@ struct LiveCall {
     std::size_t row = 0;
     bool finished = false;
     int slot = -1;            // device-side call slot
+    int group = -1;           // TRT static group of the call's leaf (Plan::static_group)
+    std::size_t group_tokens = 0;
     std::vector<int> pages;   // physical page per 16-token block (prompt + output)
     std::size_t remaining() const { return prompt.size() - done; }
 };
@@ -323,6 +333,8 @@ struct StepPlan {
         bool from_prompt = true; // token ids come from prompt (else last sampled)
         bool write_kv = true;    // false for the recomputed last position of a fully cached prompt
         bool sample = false;     // produce the next token from the last position
+        int group = -1;          // TRT static group (decode segs): rows of one group share its prefix pages
+        std::size_t group_tokens = 0;
         std::vector<int> table;  // block table snapshot taken when the seg was planned
     };
     int worker = 0;

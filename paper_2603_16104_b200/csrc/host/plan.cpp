@@ -119,6 +119,35 @@ Plan parse_plan(const std::uint8_t* data, std::size_t n) {
         }
     }
     if (!r.done()) fail("plan: trailing bytes");
+    // TRT static groups (see Plan::static_group)
+    p.static_group.assign(p.tree.size(), -1);
+    p.static_group_tokens.assign(p.tree.size(), 0);
+    std::vector<int> leaves_under(p.tree.size(), 0);
+    for (int lf : p.leaves)
+        for (int v = lf; v >= 0; v = p.tree[static_cast<std::size_t>(v)].parent) ++leaves_under[static_cast<std::size_t>(v)];
+    for (int lf : p.leaves) {
+        // the deepest branching node (>= 2 calls below it) whose root path is all static text
+        std::size_t toks = 0, best_toks = 0;
+        int best = -1;
+        for (int v : p.path_from_root(p.tree[static_cast<std::size_t>(lf)].parent)) {
+            const TreeNode& t = p.tree[static_cast<std::size_t>(v)];
+            bool all_static = true;
+            for (const TreePart& pt : t.parts) {
+                if (!pt.is_static) {
+                    all_static = false;
+                    break;
+                }
+                toks += p.span_len(pt.v);
+            }
+            if (!all_static) break;
+            if (leaves_under[static_cast<std::size_t>(v)] >= 2 && toks > 0) {
+                best = v;
+                best_toks = toks;
+            }
+        }
+        p.static_group[static_cast<std::size_t>(lf)] = best;
+        p.static_group_tokens[static_cast<std::size_t>(lf)] = best_toks;
+    }
     return p;
 }
 

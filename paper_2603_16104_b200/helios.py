@@ -324,3 +324,18 @@ def vocab_of(token: int, vocab: int) -> int:
 
 def gen_token(vid: int, vocab: int) -> int:
     return _lib.load().hk_gen_token(vid, vocab)
+
+
+def plan_call_groups(plan: bytes) -> Dict[tuple, tuple]:
+    """{(op, query): (trt group node, static prefix tokens)} (hk_plan_call_groups)."""
+    lib = _lib.load()
+    buf = (C.c_uint8 * len(plan)).from_buffer_copy(plan)
+    n = lib.hk_plan_call_groups(buf, len(plan), None, None, None, None, 0)
+    if n < 0:
+        raise RuntimeError(_lib.last_error())
+    op = (C.c_int64 * max(n, 1))()
+    q = (C.c_int32 * max(n, 1))()
+    g = (C.c_int32 * max(n, 1))()
+    t = (C.c_uint64 * max(n, 1))()
+    lib.hk_plan_call_groups(buf, len(plan), op, q, g, t, n)
+    return {(op[i], q[i]): (g[i], t[i]) for i in range(n)}

@@ -404,3 +404,24 @@ def test_cabi_exports_every_declared_symbol():
     assert not missing, missing
     assert set(_lib.EXPORTED) >= declared
     assert lib.hk_abi_version() == 1
+
+
+def test_plan_trt_static_groups_match_the_shared_prompt_structure():
+    """§8(f)4: the decode-attention planner takes its prefix-shared groups from the
+    plan's call-level TRT (trt.cpp:489-530): the deepest branching node whose root
+    path is all static text. configs[1]: the 64 branches share the 2,048-token
+    pinned system prompt; configs[4]: 128 branches share 8,192 tokens; configs[0]:
+    the 4 maps share 512 tokens and the reducer has no group of size > 1."""
+    from collections import Counter
+    groups = {}
+    for n in ("c1", "c2", "c4_w1", "c5"):
+        blob, _ = wl.load_plan(n)
+        groups[n] = Counter(helios.plan_call_groups(blob).values())
+    (g2, n2), = groups["c2"].items()
+    assert g2[1] == 2048 and n2 == 64
+    (g5, n5), = groups["c5"].items()
+    assert g5[1] == 8192 and n5 == 128
+    assert sorted(groups["c1"].values()) == [1, 4] and max(groups["c1"], key=groups["c1"].get)[1] == 512
+    # C4': one group of 64 calls per operator; static prefixes grow with the overlap ratio
+    assert sorted(groups["c4_w1"].values()) == [64] * 8
+    assert sorted(t for _, t in groups["c4_w1"])[-1] >= 0.9 * 1024 - 2
