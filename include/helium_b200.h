@@ -139,6 +139,13 @@ void hk_kv_destroy(hk_kvcache* c);
  * (lens_cap). Returns the number of pins, or -1. */
 int64_t hk_static_pin_prefixes(const uint8_t* plan, size_t plan_len, int worker, size_t block, size_t threshold,
                                size_t budget_tokens, uint64_t* tokens, size_t cap, uint64_t* lens, size_t lens_cap);
+/* Opt-in call-level partition — DIVERGES from the reference,
+ * which places whole operators (partition_workflow, scheduler.cpp:59-115): the
+ * plan's calls of every operator are dealt round-robin over `workers` (each
+ * worker keeps the plan's schedule order), so one operator's branches can
+ * run on several GPUs. Writes the new HKPLAN01 blob; returns its byte size
+ * (copies min(size, cap) bytes; out may be NULL) or -1. */
+int64_t hk_plan_partition_calls(const uint8_t* plan, size_t plan_len, int workers, uint8_t* out, size_t cap);
 /* The plan's TRT shared-prefix groups (trt.cpp:489-530), one per llm call in
  * (op, query) order: the deepest call-tree ancestor whose whole root path is
  * static text (-1: none) and that static path's token length. The decode

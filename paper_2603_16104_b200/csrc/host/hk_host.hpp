@@ -99,6 +99,7 @@ struct Plan {
     // from here instead of rediscovering them from block tables every step.
     std::vector<int> static_group;
     std::vector<std::size_t> static_group_tokens;
+    std::size_t sigma_offset = 0;  // byte offset of the schedule section in the blob
 
     const Token* span_ptr(std::int64_t s) const { return pool.data() + spans.at(static_cast<std::size_t>(s)).first; }
     std::size_t span_len(std::int64_t s) const { return spans.at(static_cast<std::size_t>(s)).second; }
@@ -110,6 +111,8 @@ struct Plan {
 };
 
 Plan parse_plan(const std::uint8_t* data, std::size_t n);
+// opt-in call-level partition of a plan over `workers` (diverges from the reference)
+std::vector<std::uint8_t> partition_calls(const std::uint8_t* data, std::size_t n, int workers);
 
 // -------------------------------------------------------------- evaluator
 class Evaluator {

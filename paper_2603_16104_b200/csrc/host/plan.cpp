@@ -36,6 +36,7 @@ class Reader {
         return static_cast<std::size_t>(c);
     }
     bool done() const { return pos_ == n_; }
+    std::size_t pos() const { return pos_; }
 
   private:
     const std::uint8_t* d_;
@@ -107,6 +108,7 @@ Plan parse_plan(const std::uint8_t* data, std::size_t n) {
             p.leaf_index[CallId{t.op, t.query}] = static_cast<int>(k);
         }
     }
+    p.sigma_offset = r.pos();
     std::size_t nw = r.count();
     p.sigma.resize(nw);
     for (auto& wq : p.sigma) {
@@ -149,6 +151,36 @@ Plan parse_plan(const std::uint8_t* data, std::size_t n) {
         p.static_group_tokens[static_cast<std::size_t>(lf)] = best_toks;
     }
     return p;
+}
+
+// Call-level partition (opt-in). DIVERGES from the reference,
+// whose partition_workflow places whole operators on workers (scheduler.cpp:
+// 59-115), so a one-operator workflow (configs[1]) can only ever use one
+// worker there. Here every operator's calls are dealt round-robin over
+// `workers` in the plan's schedule order (which each worker keeps); the
+// blob's value graph and call tree are unchanged, only the schedule section
+// (the blob's tail) is rewritten.
+std::vector<std::uint8_t> partition_calls(const std::uint8_t* data, std::size_t n, int workers) {
+    if (workers < 1) fail("partition_calls: workers must be positive");
+    Plan p = parse_plan(data, n);
+    std::vector<std::vector<CallId>> sigma(static_cast<std::size_t>(workers));
+    std::map<NodeId, int> next;
+    for (const auto& wq : p.sigma)
+        for (const CallId& c : wq) sigma[static_cast<std::size_t>(next[c.op]++ % workers)].push_back(c);
+    std::vector<std::uint64_t> tail;
+    tail.push_back(static_cast<std::uint64_t>(workers));
+    for (const auto& wq : sigma) {
+        tail.push_back(wq.size());
+        for (const CallId& c : wq) {
+            tail.push_back(static_cast<std::uint64_t>(c.op));
+            tail.push_back(static_cast<std::uint64_t>(static_cast<std::int64_t>(c.query)));
+        }
+    }
+    std::vector<std::uint8_t> out(data, data + p.sigma_offset);
+    const std::size_t head = out.size();
+    out.resize(head + tail.size() * 8);
+    std::memcpy(out.data() + head, tail.data(), tail.size() * 8);
+    return out;
 }
 
 // ---------------------------------------------------------------- evaluator

@@ -339,3 +339,23 @@ def plan_call_groups(plan: bytes) -> Dict[tuple, tuple]:
     t = (C.c_uint64 * max(n, 1))()
     lib.hk_plan_call_groups(buf, len(plan), op, q, g, t, n)
     return {(op[i], q[i]): (g[i], t[i]) for i in range(n)}
+
+
+def partition_calls(plan: bytes, workers: int) -> bytes:
+    """Opt-in call-level partition (hk_plan_partition_calls): every operator's
+    calls dealt round-robin over `workers`. DIVERGES from the reference, which
+    places whole operators (scheduler.cpp:59-115)."""
+    lib = _lib.load()
+    buf = (C.c_uint8 * len(plan)).from_buffer_copy(plan)
+    n = lib.hk_plan_partition_calls(buf, len(plan), workers, None, 0)
+    if n < 0:
+        raise RuntimeError(_lib.last_error())
+    out = (C.c_uint8 * n)()
+    lib.hk_plan_partition_calls(buf, len(plan), workers, out, n)
+    return bytes(out)
+
+
+def replicate_workers(cfg: "SimConfig", workers: int) -> "SimConfig":
+    """SimConfig with the first worker's (capacity, block, budget) for every worker."""
+    from dataclasses import replace
+    return replace(cfg, workers=[cfg.workers[0]] * workers)
