@@ -118,8 +118,13 @@ double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_
         const size_t n_part = static_cast<size_t>(n_rows) * H * kMaxParts;
         HK_CUDA(cudaMalloc(&bufs[1], n_part * 128 * 4));
         HK_CUDA(cudaMalloc(&bufs[2], n_part * 8));
-        HK_CUDA(cudaMalloc(&bufs[3], (static_cast<size_t>(n_rows) * Hkv + 4) * 4));
-        HK_CUDA(cudaMemset(bufs[3], 0, (static_cast<size_t>(n_rows) * Hkv + 4) * 4));
+        // arrival counters [rows][Hkv], then queue state (head, exits, grid arrival) for the
+        // first call and for each of the 10 launches of the timing graph: a launch may
+        // claim queue items before griddepcontrol.wait, so back-to-back launches never
+        // share a queue head (as the engine's layers do not)
+        const size_t ctr_n = static_cast<size_t>(n_rows) * Hkv + 4 * 11;
+        HK_CUDA(cudaMalloc(&bufs[3], ctr_n * 4));
+        HK_CUDA(cudaMemset(bufs[3], 0, ctr_n * 4));
         int32_t* ctr = static_cast<int32_t*>(bufs[3]);
         const CUtensorMap tm = hkd::make_tmap_2d_bf16(kv, static_cast<uint64_t>(n_pages) * 2 * Hkv * 16, 128, 64, 16);
         hkd::DecodeAttnArgs a{static_cast<const hkd::bf16*>(qkv), nullptr, H, Hkv, (H + 2 * Hkv) * 128,
@@ -145,7 +150,13 @@ double hkx_decode_attention(const void* qkv, const void* kv, int n_pages, int n_
             HK_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
             cudaGraph_t g;
             HK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-            for (int i = 0; i < 10; ++i) hkd::decode_attention(a, tm, cs);
+            for (int i = 0; i < 10; ++i) {
+                hkd::DecodeAttnArgs ai = a;
+                ai.pv_next = ctr + static_cast<size_t>(n_rows) * Hkv + 4 * (i + 1);
+                ai.pv_done = ai.pv_next + 1;
+                ai.grid_arrive = ai.pv_next + 2;
+                hkd::decode_attention(ai, tm, cs);
+            }
             HK_CUDA(cudaStreamEndCapture(cs, &g));
             cudaGraphExec_t ge;
             HK_CUDA(cudaGraphInstantiate(&ge, g, 0));

@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+for k in 1 128; do echo "=== trace k=$k"; python tools/attn_trace.py $k 64 2>&1 | tail -16; echo "=== items k=$k"; python tools/attn_items.py $k 2>&1 | tail -8; done
