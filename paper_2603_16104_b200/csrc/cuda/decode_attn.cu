@@ -9,17 +9,19 @@
 //   shared items  decode rows that share a block-table prefix (the branches
 //                 of one pinned system prompt, e.g. configs[1]'s 2,048 tokens)
 //                 are (token, q-head) pairs of one kv head — 128/G tokens fill
-//                 a 128-row tcgen05 tile. A tile's prefix pages are split over
-//                 S CTAs (planner: ~64 shared CTAs for a <= 2K prefix). Warp 9
-//                 streams K/V straight from the paged pool with TMA (128B
-//                 swizzle, a 3-stage K ring and a 2-stage V ring, started
-//                 before griddepcontrol.wait: old pages do not depend on this
-//                 step); the two tiles of a kv head form the CTA pair and each
-//                 page is fetched once and multicast into both. Warp 8 issues
-//                 S = Q K^T into two TMEM buffers and O += P V with P read
-//                 from TMEM; 8 softmax warps (two threads per row) do the
-//                 online softmax with a lazy O rescale. Output: the row
-//                 normalised to bf16 + (m, l), one partial per item.
+//                 a 128-row tcgen05 tile. One CTA streams TWO tiles of a kv
+//                 head over a range of prefix pages (shared2_phase; planner:
+//                 ~64 CTAs for a <= 2K prefix, ~2/3 of the SMs for longer
+//                 ones). Warp 9 streams K/V straight from the paged pool with
+//                 TMA (128B swizzle, 2-stage K and V rings, started before
+//                 griddepcontrol.wait: old pages do not depend on this step);
+//                 warp 8 alternates the tiles' MMAs (PV_0, S_0', PV_1, S_1')
+//                 so one softmax warpgroup's exponentials (one thread per row,
+//                 the chunk in registers, P written over S in TMEM) overlap
+//                 the other tile's MMAs. Output: the row normalised to bf16 +
+//                 (m, l), one partial per item. (shared_phase — one tile per
+//                 CTA, CTA pairs multicasting the pages — serves the prefill
+//                 tiles, and decode under HK_ATTN_TWO_TILE=0.)
 //   private items every decode row's own pages (prompt suffix + generated
 //                 tokens) per kv head, as key ranges sized for one round on
 //                 the free warps; each warp pulls items from a global queue,
@@ -27,7 +29,8 @@
 //                 m16n8k16 with swapped operands (keys / head dims are the
 //                 16-row M side, the G q-heads the 8-wide N side).
 //   merge         after a grid-wide arrival (all CTAs co-resident: grid <=
-//                 SMs), every SM merges rows (merge16: w_p = l_p 2^(m_p - M));
+//                 SMs), every SM merges rows (merge16, up to 16 partials per
+//                 memory round trip: w_p = l_p 2^(m_p - M));
 //                 a row with a single item is written directly. A grid larger
 //                 than the SM count falls back to a separate merge launch.
 //   prefill tiles causal tiles (rows = prompt tokens x G heads, keys [0, pos])
@@ -475,6 +478,286 @@ __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const Dec
     }
 }
 
+// ------------------------------------------- shared, two tiles per CTA (decode)
+// The decode tiles of one (kv head, key range): up to 2 x 128 rows in one CTA,
+// each tile with its own softmax warpgroup (one thread per row, the whole
+// 128-key chunk in registers) and its own TMEM (S | O, P written over S). The
+// MMA warp alternates the tiles — PV_0(c), S_0(c+1), PV_1(c), S_1(c+1) — so one
+// warpgroup's exponentials overlap the other tile's MMAs: the 128 x 128 chunk
+// softmax is bound by the SFU (16 ex2/clk/SM, ~1,024 cycles), the MMAs of a
+// chunk by the tensor pipe (~1,024 cycles for S + PV), and the two overlap.
+// K/V are read once per CTA (no pairing), K and V rings of 2 stages.
+//   smem: sQ [2 tiles][2][128][64] | sK [2][2][128][64] | sV [2][2][128][64] | barriers | page ids
+//   TMEM: tile t at columns t * 256: S [0, 128) (P: bf16 pairs in [0, 64)), O [128, 256)
+constexpr int S2_Q = 2 * SQ_BYTES;                         // 64 KB
+constexpr int S2_BAR = S2_Q + 4 * SKV_BYTES;               // after 2 K + 2 V stages
+constexpr int S2_PG = S2_BAR + 256;                        // page ids of the item
+static_assert(1024 + S2_PG + SH_MAX_PAGES * 4 <= SH_SMEM - 1024, "shared2 smem overlaps the private barriers");
+
+template <int G>
+__device__ __forceinline__ void shared2_phase(const CUtensorMap& tm_kv, const DecodeAttnArgs& a, uint8_t* sm) {
+    uint8_t* sK0 = sm + S2_Q;
+    auto sQ = [&](int t) { return sm + t * SQ_BYTES; };
+    auto sK = [&](int c) { return sK0 + (c & 1) * SKV_BYTES; };
+    auto sV = [&](int c) { return sK0 + 2 * SKV_BYTES + (c & 1) * SKV_BYTES; };
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S2_BAR);
+    uint64_t* k_full = bars;        // [2] K chunk landed
+    uint64_t* k_empty = bars + 2;   // [2] K chunk read by both tiles' S
+    uint64_t* v_full = bars + 4;    // [2]
+    uint64_t* v_empty = bars + 6;   // [2] V chunk read by both tiles' PV
+    uint64_t* s_full = bars + 8;    // [tile] S written (implies the tile's previous PV completed)
+    uint64_t* p_full = bars + 10;   // [tile] P written (128 threads)
+    uint64_t* q_full = bars + 12;   // [tile] Q tile in smem (128 threads)
+    uint64_t* o_fin = bars + 14;    // [tile] last PV of the tile complete
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+    int* spg = reinterpret_cast<int*>(sm + S2_PG);
+
+    stamp(a, blockIdx.x, 0);
+    const ShItem it = a.sh[blockIdx.x];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int RB = ROWS / G;  // tokens per tile
+    const int ntile = it.ntok > RB ? 2 : 1;
+    const int nch = (it.npages + 7) / 8;
+    if (it.ntok <= 0 || nch == 0) return;  // padding item (keeps the cluster pairs aligned)
+
+    if (tid == 0) {
+        tma_prefetch_desc(&tm_kv);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&k_full[b], 1);
+            mbar_init(&k_empty[b], 1);
+            mbar_init(&v_full[b], 1);
+            mbar_init(&v_empty[b], 1);
+            mbar_init(&s_full[b], 1);
+            mbar_init(&p_full[b], 128);
+            mbar_init(&q_full[b], 128);
+            mbar_init(&o_fin[b], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 8) tmem_alloc(tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    stamp(a, blockIdx.x, 1);
+
+    if (warp == 9) {
+        // ---- TMA producer: decode tiles read shared pages written by earlier
+        // steps, so the loads start before griddepcontrol.wait
+        for (int i = lane; i < it.npages; i += 32) spg[i] = a.pages[it.ptab + it.page0 + i];
+        __syncwarp();
+        if (lane == 0) {
+            const int rows_per_head = a.Hkv * PG;  // pool-map rows between K and V of a page
+            auto load = [&](int c, int v) {
+                const int b = c & 1;
+                uint64_t* full = v ? &v_full[b] : &k_full[b];
+                if (c >= 2) mbar_wait(v ? &v_empty[b] : &k_empty[b], ((c >> 1) - 1) & 1);
+                const int np = min(8, it.npages - c * 8);
+                uint8_t* dst = v ? sV(c) : sK(c);
+                mbar_expect_tx(full, static_cast<uint32_t>(np) * 2 * 2048);
+                for (int i = 0; i < np; ++i) {
+                    const int rk = a.layer_row0 + (spg[c * 8 + i] * 2 * a.Hkv + it.kvh) * PG + v * rows_per_head;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) tma_load_2d(dst + h * SKV_BYTES / 2 + i * 2048, &tm_kv, full, h * 64, rk);
+                }
+            };
+            for (int c = 0; c <= nch; ++c) {
+                if (c < nch) load(c, 0);
+                if (c >= 1) load(c - 1, 1);
+            }
+        }
+        pdl_wait();
+        pdl_trigger();
+    } else if (warp == 8) {
+        // ---- MMA issuer
+        pdl_wait();
+        pdl_trigger();
+        if (lane == 0) {
+            auto issue_s = [&](int t, int c) {
+                const int nk = min(8, it.npages - c * 8) * PG;
+                const uint32_t idesc = umma_idesc_bf16(ROWS, nk);
+                const uint32_t q0 = smem_u32(sQ(t)), k0 = smem_u32(sK(c));
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * (SKV_BYTES / 2) + (kk & 3) * 32;
+                    umma_bf16(tmem + t * 256, umma_desc_sw128(q0 + (kk >> 2) * (SQ_BYTES / 2) + (kk & 3) * 32),
+                              umma_desc_sw128(k0 + off), idesc, kk > 0 ? 1u : 0u);
+                }
+                umma_commit(&s_full[t]);
+            };
+            auto issue_pv = [&](int t, int c) {
+                const int np = min(8, it.npages - c * 8);
+                const uint32_t v0 = smem_u32(sV(c));
+                const uint32_t idesc = umma_idesc_bf16(ROWS, HD) | (1u << 16);  // B = V, MN-major
+                for (int kk = 0; kk < np; ++kk)
+                    umma_bf16_ts(tmem + t * 256 + 128, tmem + t * 256 + kk * 8,
+                                 umma_desc_sw128_lbo(v0 + kk * 2048, SKV_BYTES / 2, 1024), idesc,
+                                 (c > 0 || kk > 0) ? 1u : 0u);
+            };
+            for (int t = 0; t < ntile; ++t) mbar_wait(&q_full[t], 0);
+            mbar_wait(&k_full[0], 0);
+            tc_fence_after();
+            for (int t = 0; t < ntile; ++t) issue_s(t, 0);
+            umma_commit(&k_empty[0]);
+            for (int c = 0; c < nch; ++c) {
+                mbar_wait(&v_full[c & 1], (c >> 1) & 1);
+                if (c + 1 < nch) mbar_wait(&k_full[(c + 1) & 1], ((c + 1) >> 1) & 1);
+                for (int t = 0; t < ntile; ++t) {
+                    // P_t(c) is written over S_t(c); S_t(c + 1) is issued after PV_t(c)
+                    // (tcgen05 MMAs of one thread execute in order)
+                    mbar_wait(&p_full[t], c & 1);
+                    tc_fence_after();
+                    cstamp(a, c, 4 + t);
+                    issue_pv(t, c);
+                    if (c + 1 == nch) umma_commit(&o_fin[t]);
+                    else issue_s(t, c + 1);
+                }
+                umma_commit(&v_empty[c & 1]);
+                if (c + 1 < nch) umma_commit(&k_empty[(c + 1) & 1]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---- softmax warpgroups: WG t = warps 4t .. 4t + 3, one thread per row of tile t
+        const int t = warp >> 2;
+        const int row = (warp & 3) * 32 + lane;
+        const uint32_t t_lane = tmem + t * 256 + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        const int tok0 = it.row0 + t * RB;                       // decode row of this tile's row 0
+        const int ntok_t = t < ntile ? min(RB, it.ntok - t * RB) : 0;
+        const int nrows = ntok_t * G;
+        pdl_wait();  // q comes from the qkv/RoPE kernel
+        pdl_trigger();
+        span_mark(a, 1);
+        if (t < ntile) {
+        {
+            // Q tile rows (token r / G, head kvh*G + r % G); rows >= nrows are zero
+            uint8_t* q = sQ(t);
+            const int wt = tid & 127;
+            uint4 qv[16];  // every load in flight at once (one round trip)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int idx = wt + i * 128, r = idx >> 4, ch = idx & 15;
+                qv[i] = make_uint4(0u, 0u, 0u, 0u);
+                if (r < nrows)
+                    qv[i] = __ldg(reinterpret_cast<const uint4*>(a.qkv + static_cast<size_t>(a.dec_tok0 + tok0 + r / G) * a.QKV +
+                                                                 (it.kvh * G + r % G) * HD + ch * 8));
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int idx = wt + i * 128, r = idx >> 4, ch = idx & 15;
+                *reinterpret_cast<uint4*>(q + (ch >> 3) * (SQ_BYTES / 2) + sw128(r, ch & 7)) = qv[i];
+            }
+            fence_proxy_async();
+            mbar_arrive(&q_full[t]);
+        }
+        stamp(a, blockIdx.x, 2);
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int c = 0; c < nch; ++c) {
+            const int nk = min(8, it.npages - c * 8) * PG;
+            mbar_wait(&s_full[t], c & 1);
+            tc_fence_after();
+            if (c == 0) stamp(a, blockIdx.x, 7);
+            if (tid == 0) cstamp(a, c, 0);
+            float s[128];
+            {
+                float* s0 = s;
+                float* s1 = s + 64;
+                tmem_ld64(t_lane, *reinterpret_cast<float(*)[64]>(s0));
+                tmem_ld64(t_lane + 64, *reinterpret_cast<float(*)[64]>(s1));
+            }
+            if (nk < 128) {
+#pragma unroll
+                for (int e = 0; e < 128; ++e)
+                    if (e >= nk) s[e] = -INFINITY;
+            }
+            float mx8[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mx8[j] = s[j];
+#pragma unroll
+            for (int j = 8; j < 128; ++j) mx8[j & 7] = fmaxf(mx8[j & 7], s[j]);
+            float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+            mx *= a.sl2;  // log2 domain
+            if (tid == 0) cstamp(a, c, 6);
+            // lazy rescale (exact: O and l always refer to m_run; p <= 2^8 between rescales)
+            const bool need = mx > m_run + 8.f;
+            const float al = need ? ex2(m_run - mx) : 1.f;
+            if (need) {
+                l_run *= al;
+                m_run = mx;
+            }
+            const float nm = -m_run;
+            uint32_t pk[64];
+            float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < 64; ++j) {
+                const float p0 = ex2(fmaf(s[2 * j], a.sl2, nm));
+                const float p1 = ex2(fmaf(s[2 * j + 1], a.sl2, nm));
+                ls[j & 3] += p0 + p1;
+                pk[j] = pack2(p0, p1);
+            }
+            l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+            if (tid == 0) cstamp(a, c, 1);
+            // s_full(c) implies PV(c - 1) completed: O may be rescaled now
+            if (c > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float v[32];
+                    const uint32_t ta = t_lane + 128 + j * 32;
+                    tmem_ld32(ta, v);
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] *= al;
+                    tmem_st32(ta, v);
+                }
+            }
+            // P (bf16 pairs, key-major) over S's first 64 columns: the PV MMA reads A there
+            tmem_st32u(t_lane, *reinterpret_cast<uint32_t(*)[32]>(pk));
+            tmem_st32u(t_lane + 32, *reinterpret_cast<uint32_t(*)[32]>(pk + 32));
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&p_full[t]);
+            if (c == 0) stamp(a, blockIdx.x, 8);
+            if (tid == 0) cstamp(a, c, 3);
+        }
+        mbar_wait(&o_fin[t], 0);
+        tc_fence_after();
+        stamp(a, blockIdx.x, 3);
+        // ---- output rows: normalised bf16 partials + (m, l), staged row-major in
+        // smem (the K/V stages are free) and written by bulk copies, 256 B per row
+        float v[128];
+        tmem_ld64(t_lane + 128, *reinterpret_cast<float(*)[64]>(v));
+        tmem_ld64(t_lane + 192, *reinterpret_cast<float(*)[64]>(v + 64));
+        const float inv = l_run > 0.f ? __frcp_rn(l_run) : 0.f;
+        constexpr int RS = HD * 2 + 16;  // padded staging row (bytes)
+        uint8_t* stage = sK0 + t * ROWS * RS;
+        {
+            uint4* dst = reinterpret_cast<uint4*>(stage + row * RS);
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                dst[e] = make_uint4(pack2(v[8 * e] * inv, v[8 * e + 1] * inv), pack2(v[8 * e + 2] * inv, v[8 * e + 3] * inv),
+                                    pack2(v[8 * e + 4] * inv, v[8 * e + 5] * inv), pack2(v[8 * e + 6] * inv, v[8 * e + 7] * inv));
+        }
+        const size_t pi = (static_cast<size_t>(tok0 + row / G) * a.H + it.kvh * G + row % G) * a.max_parts + it.rank;
+        if (row < nrows) a.part_ml[pi] = make_float2(m_run, l_run);
+        fence_proxy_async();
+        named_bar(3 + t, 128);
+        stamp(a, blockIdx.x, 11);
+        {
+            // each thread of the warpgroup copies one row
+            if (row < nrows) bulk_s2g(part_bf16(a) + pi * HD, stage + row * RS, HD * 2);
+            bulk_commit_wait_read();  // staging reusable; completion is awaited before the grid barrier
+        }
+        stamp(a, blockIdx.x, 5);
+        }  // t < ntile
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // ------------------------------------------------------ private (tensor cores)
 // One warp per item (a token's own pages for one kv head). MMA rows are the G
 // q-heads of the token (rows >= G are zero padding): per 16-key page,
@@ -710,8 +993,8 @@ __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const Dec
 
 // out[row][head] = merge of the row's n_parts partials. A 16-lane group per
 // (row, head), lane owns 8 dims; the part count, every (m, l) and every part's
-// 8 dims of a batch of 8 parts are loaded at once (one memory round trip);
-// unused slots are masked, never multiplied (they may hold stale bits).
+// 8 dims of a batch of up to 16 parts are loaded at once (one memory round
+// trip); unused slots are masked, never multiplied (they may hold stale bits).
 // All 32 lanes of the warp must call it (two pairs per warp).
 __device__ __forceinline__ void merge16(const DecodeAttnArgs& a, int pair, int n_pairs) {
     const unsigned full = 0xffffffffu;
@@ -726,21 +1009,21 @@ __device__ __forceinline__ void merge16(const DecodeAttnArgs& a, int pair, int n
     // the first batch's loads are issued together with the part count (they do
     // not depend on it; unused slots are masked): one L2 round trip per row
     // (a.any_merge = the step's max part count bounds the first batch: no loads of unused slots)
-    const int lim = a.any_merge > 1 ? min(8, a.any_merge) : 8;
+    const int lim = a.any_merge > 1 ? min(16, a.any_merge) : 16;
     float2 ml = sub < lim ? __ldcg(&a.part_ml[base + sub]) : make_float2(-INFINITY, 0.f);
-    uint4 v[8];  // 8 bf16 dims of each of the batch's parts
+    uint4 v[16];  // 8 bf16 dims of each of the batch's parts
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < 16; ++k)
         v[k] = k < lim ? __ldcg(reinterpret_cast<const uint4*>(part_bf16(a) + (base + k) * HD) + sub) : make_uint4(0u, 0u, 0u, 0u);
-    for (int k0 = 0; k0 < a.max_parts; k0 += 8) {
+    for (int k0 = 0; k0 < a.max_parts; k0 += 16) {
         if (!__any_sync(full, k0 < np)) break;
         if (k0 > 0) {
-            ml = sub < 8 ? __ldcg(&a.part_ml[base + k0 + sub]) : make_float2(-INFINITY, 0.f);
+            ml = __ldcg(&a.part_ml[base + k0 + sub]);
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
+            for (int k = 0; k < 16; ++k)
                 v[k] = __ldcg(reinterpret_cast<const uint4*>(part_bf16(a) + (base + k0 + k) * HD) + sub);
         }
-        const bool mine = sub < 8 && k0 + sub < np;
+        const bool mine = k0 + sub < np;
         float mx = mine ? ml.x : -INFINITY;
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(full, mx, o));
@@ -755,7 +1038,7 @@ __device__ __forceinline__ void merge16(const DecodeAttnArgs& a, int pair, int n
         for (int e = 0; e < 8; ++e) acc[e] *= sc;
         const int g0 = lane & 16;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 16; ++k) {
             const float wk = __shfl_sync(full, w, g0 + k);
             if (k0 + k < np) {
                 const uint32_t u[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
@@ -811,7 +1094,10 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_decode_kernel(const __grid
     PvNext nx;
     nx.idx = a.n_pv;
     if (blockIdx.x < a.n_sh) {
-        shared_phase<G>(tm_kv, a, sm);
+        if (a.sh[blockIdx.x].flags & 2)
+            shared2_phase<G>(tm_kv, a, sm);
+        else
+            shared_phase<G>(tm_kv, a, sm);
         __syncthreads();
         if (warp >= DA_PV_WARPS) return;
         // the planner sizes private items for one round on the queue-only CTAs;
@@ -972,11 +1258,14 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
     plan.pv.clear();
     plan.n_parts.assign(rows.size(), 0);
     plan.shared_bytes = plan.private_bytes = 0;
-    int tiles = 0;  // shared CTAs per split (row blocks padded to pairs) x kv heads
+    // decode tiles: two row blocks per CTA (shared2_phase), or CTA pairs of one row
+    // block each with multicast pages (shared_phase; HK_ATTN_TWO_TILE=0)
+    static const bool two_tile = !(std::getenv("HK_ATTN_TWO_TILE") && std::atoi(std::getenv("HK_ATTN_TWO_TILE")) == 0);
+    int tiles = 0;  // shared CTAs per split x kv heads
     for (const auto& g : groups)
         if (g.shared_pages > 0 && g.members > 1) {
             const int nrb = (g.members + rb - 1) / rb;
-            tiles += (nrb + (nrb & 1)) * Hkv;
+            tiles += (two_tile ? (nrb + 1) / 2 : nrb + (nrb & 1)) * Hkv;
         }
     plan.sh_cluster = 1;
     // private key split: about 8 private warps per SM over the whole step
@@ -1003,7 +1292,9 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
         // (r1c re-measure: ~64 shared CTAs at every k for a 2K prefix — the
         // private items then run as one round on the other ~84 SMs)
         (void)priv_pages_per_row;
-        const int target = max_nch > 16 ? num_sms : 64;
+        // two-tile CTAs: ~2/3 of the SMs for long prefixes (configs[4] at k = 1 / 128 / 256: 96 shared
+        // CTAs 47.9 / 50.0 / 52.8 us, 144 CTAs 44.4 / 56.5 / 71.2 us — the private rows need the rest)
+        const int target = max_nch > 16 ? (two_tile ? num_sms * 2 / 3 : num_sms) : 64;
         if (tiles > 0) best_s = std::max(1, std::min(8, static_cast<int>(std::lround(static_cast<double>(target) / tiles))));
         static const int env_splits = std::getenv("HK_ATTN_SPLITS") ? std::atoi(std::getenv("HK_ATTN_SPLITS")) : 0;
         if (env_splits > 0) best_s = env_splits;
@@ -1035,6 +1326,22 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
             // of 2) that fetch the pages once and multicast them; an odd count is
             // padded with an empty row block that only helps fetch
             const int nrb = (g.members + rb - 1) / rb;
+            if (two_tile) {
+                for (int h = 0; h < Hkv; ++h)
+                    for (int k = 0; k < splits; ++k)
+                        for (int j = 0; j < nrb; j += 2) {
+                            ShItem it{};
+                            it.row0 = g.row0 + j * rb;
+                            it.ntok = std::min(2 * rb, g.members - j * rb);
+                            it.kvh = h;
+                            it.ptab = rows[static_cast<size_t>(g.row0)].ptab;
+                            it.page0 = k * cpc * 8;
+                            it.npages = std::min(cpc * 8, shared_pages - it.page0);
+                            it.rank = k;
+                            it.flags = 2;
+                            plan.sh.push_back(it);
+                        }
+            } else
             for (int h = 0; h < Hkv; ++h)
                 for (int k = 0; k < splits; ++k)
                     for (int j = 0; j < nrb + (nrb & 1); ++j) {
@@ -1058,8 +1365,8 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
             const int k0 = shared_pages * PG, k1 = in.pos + 1;
             if (k1 <= k0) throw std::runtime_error("decode_attention: shared range covers the decode token");
             const int first = splits;  // the shared items contribute partials 0 .. splits - 1
-            // keep a row's partials within one 8-part merge batch when possible
-            const int part_cap = first < 8 ? 8 - first : max_parts - first;
+            // keep a row's partials within one 16-part merge batch when possible
+            const int part_cap = first < 16 ? 16 - first : max_parts - first;
             const int row_pages = (k1 - k0 + PG - 1) / PG;
             int npv0 = static_cast<int>(row_pages * q_warps / (Hkv * std::max(1.0, priv_pages)));
             npv0 = std::max(1, std::min(npv0, std::max(1, part_cap)));
@@ -1086,6 +1393,13 @@ void plan_decode_attention(const std::vector<DecodeRowIn>& rows, const std::vect
             plan.private_bytes += static_cast<double>(k1 - k0) * Hkv * kv_tok;
             plan.private_bytes += 2.0 * H * HD * 2;  // q in, o out
         }
+    }
+    // the launch pairs CTAs (clusters of 2, for the prefill tiles that follow):
+    // an empty two-tile item keeps every pair homogeneous
+    if (plan.sh.size() & 1) {
+        ShItem pad{};
+        pad.flags = 2;
+        plan.sh.push_back(pad);
     }
 }
 
