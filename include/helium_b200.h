@@ -34,6 +34,10 @@
  *       u64 n_parts, {u64 is_static, i64 span_or_source, i64 query}[n_parts],
  *       u64 n_preds, i64 preds[n_preds]
  *   u64 n_workers, per worker: u64 n, {i64 op, i64 query}[n]   Schedule sigma
+ *   optional, for the prompt cache (integration/plan_export.hpp writes it):
+ *   u64 magic2 = 0x3130304749534b48 ("HKSIG001"), u64 n,
+ *       per node: i64 id, u64 tainted, u64 sig[batch]    compute_signatures
+ *                                                         (signature.cpp:29-104)
  */
 #ifndef HELIUM_B200_H
 #define HELIUM_B200_H
@@ -153,6 +157,39 @@ int64_t hk_plan_partition_calls(const uint8_t* plan, size_t plan_len, int worker
  * (copies min(count, cap)) or -1. */
 int64_t hk_plan_call_groups(const uint8_t* plan, size_t plan_len, int64_t* op, int32_t* query, int32_t* group,
                             uint64_t* tokens, size_t cap);
+
+/* ------------------------------------------------------------ prompt cache */
+/* class PromptCache (prompt_cache.hpp:15-40): LRU from operator signature to
+ * the tokens that operator produced. hk_pcache_save / hk_pcache_load use the
+ * reference's JSON document byte for byte (prompt_cache.cpp:47-67), so the
+ * reference's optimizer (substitute_cached, optimizer.cpp:71-95) reads a cache
+ * harvested here and vice versa. Errors keep the reference wording
+ * ("prompt cache capacity must be positive", "prompt cache json: ..."). */
+typedef struct hk_pcache hk_pcache;
+hk_pcache* hk_pcache_create(size_t capacity);
+hk_pcache* hk_pcache_load(const char* json, size_t len);
+/* writes the JSON document (NUL-terminated, truncated to cap); returns bytes needed incl. NUL */
+size_t hk_pcache_save(const hk_pcache* c, char* buf, size_t cap);
+size_t hk_pcache_size(const hk_pcache* c);
+size_t hk_pcache_capacity(const hk_pcache* c);
+int hk_pcache_contains(const hk_pcache* c, uint64_t sig);
+/* hit: refreshes recency, copies min(len, cap) tokens, returns len; miss: -1 */
+int64_t hk_pcache_lookup(hk_pcache* c, uint64_t sig, uint64_t* out, size_t cap);
+int hk_pcache_insert(hk_pcache* c, uint64_t sig, const uint64_t* tokens, size_t n);
+/* keys least recently used first; returns the count, copies min(count, cap) */
+size_t hk_pcache_keys(const hk_pcache* c, uint64_t* out, size_t cap);
+/* harvest_into_cache (optimizer.cpp:113-125) from a finished run of `plan`
+ * (which must carry the HKSIG001 section): every untainted format / lambda /
+ * llm node, every query; llm values are the tokens this run's LLM body
+ * generated (the device transformer's, under an engine). Returns the number
+ * of entries inserted, or -1. */
+int64_t hk_pcache_harvest(hk_pcache* c, const uint8_t* plan, size_t plan_len, const hk_run* run);
+/* The same from call outputs in the hk_run_call_outputs layout (n_calls,
+ * {op, query, len, tokens[len]}...), for bindings that keep a run's outputs
+ * after freeing it. */
+int64_t hk_pcache_harvest_calls(hk_pcache* c, const uint8_t* plan, size_t plan_len, const uint64_t* calls,
+                                size_t n_words);
+void hk_pcache_destroy(hk_pcache* c);
 
 /* --------------------------------------------------------- LLM body (synth) */
 /* synth_llm_len / synth_llm_output (evaluator.hpp:29-32). */

@@ -26,6 +26,7 @@
 
 #include "helios/cost_model.hpp"
 #include "helios/evaluator.hpp"
+#include "helios/signature.hpp"
 #include "helios/trt.hpp"
 #include "helios/workflow.hpp"
 
@@ -66,10 +67,14 @@ class SpanPool {
 
 enum : std::uint64_t { kBound = 0, kOutput = 1, kLambda = 2, kFormat = 3, kLlm = 4 };
 
+// with_signatures appends the HKSIG001 section: compute_signatures
+// (signature.cpp:29-104) of every node, the keys of the prompt cache
+// (hk_pcache_harvest; optimizer.cpp:113-125 harvests with the same keys).
 inline std::vector<std::uint8_t> export_plan(const helios::CompiledGraph& c,
                                              const helios::ProfileStats& profile,
                                              const helios::TemplatedRadixTree& tree,
-                                             const helios::Schedule& sigma) {
+                                             const helios::Schedule& sigma,
+                                             bool with_signatures = true) {
     using namespace helios;
     SpanPool pool;
     struct NodeRec {
@@ -230,6 +235,16 @@ inline std::vector<std::uint8_t> export_plan(const helios::CompiledGraph& c,
         for (const CallId& cid : wq) {
             w.i(cid.op);
             w.i(cid.query);
+        }
+    }
+    if (with_signatures) {
+        const SignatureSet sigs = compute_signatures(c, profile);
+        w.u(0x3130304749534b48ull);  // "HKSIG001"
+        w.u(sigs.sig.size());
+        for (const auto& [id, v] : sigs.sig) {
+            w.i(id);
+            w.u(sigs.tainted.at(id) ? 1 : 0);
+            for (std::uint64_t x : v) w.u(x);
         }
     }
     std::vector<std::uint8_t> bytes(w.words.size() * 8);

@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "helios/prompt_cache.hpp"
 #include "helios/simulator.hpp"
 #include "helium_b200.h"
 #include "plan_export.hpp"
@@ -56,10 +57,16 @@ inline std::vector<std::vector<std::uint64_t>> csv_rows(const std::string& csv) 
 }
 }  // namespace detail
 
+// harvest_into (optional): the cross-run PromptCache of run_workflow
+// (run_pipeline.cpp:74-79). run_workflow fills it with the Evaluator's
+// synthesized values; under an engine the values the run GENERATED are the
+// transformer's, so this harvests them from the run itself
+// (hk_pcache_harvest, optimizer.cpp:113-125 with the same signatures) and the
+// next submission's substitute_cached fetches device tokens.
 inline helios::SimMetrics simulate_b200(const helios::CompiledGraph& g, const helios::ProfileStats& prof,
                                         const helios::TemplatedRadixTree& tree, const helios::Schedule& sigma,
                                         const helios::SimConfig& cfg, hk_engine* engine = nullptr,
-                                        std::uint32_t flags = 0) {
+                                        std::uint32_t flags = 0, helios::PromptCache* harvest_into = nullptr) {
     const std::vector<std::uint8_t> plan = export_plan(g, prof, tree, sigma);
     std::vector<std::uint64_t> cap, blk, bud;
     for (const auto& w : cfg.workers) {
@@ -113,6 +120,24 @@ inline helios::SimMetrics simulate_b200(const helios::CompiledGraph& g, const he
             vals.emplace_back(w.begin() + static_cast<std::ptrdiff_t>(i), w.begin() + static_cast<std::ptrdiff_t>(i + len));
             i += len;
         }
+    }
+    if (harvest_into) {
+        const std::string doc = harvest_into->serialize();
+        hk_pcache* pc = hk_pcache_load(doc.data(), doc.size());
+        if (!pc) {
+            hk_run_free(run);
+            throw std::runtime_error(hk_last_error());
+        }
+        const bool ok = hk_pcache_harvest(pc, plan.data(), plan.size(), run) >= 0;
+        std::string saved(ok ? hk_pcache_save(pc, nullptr, 0) : 0, '\0');
+        if (ok) hk_pcache_save(pc, saved.data(), saved.size());
+        hk_pcache_destroy(pc);
+        if (!ok) {
+            hk_run_free(run);
+            throw std::runtime_error(hk_last_error());
+        }
+        saved.pop_back();  // NUL
+        *harvest_into = helios::PromptCache::deserialize(saved);
     }
     hk_run_free(run);
     return out;

@@ -13,6 +13,7 @@
 //     (:132-199), synth_llm_len/output (evaluator.cpp:46-58) and the token
 //     hashes (tokens.cpp) for differential tests.
 #include <chrono>
+#include <memory>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -49,6 +50,8 @@ struct Pipeline {
     TemplatedRadixTree tree;
     Schedule sigma;
     SimConfig cfg;
+    std::unique_ptr<PromptCache> cache;  // spec "prompt_cache": cross-run cache document
+    OptimizeReport rewrite;
 };
 
 // bind -> optimize -> partition -> plan -> call tree -> schedule, exactly as
@@ -64,7 +67,9 @@ Pipeline build(const std::string& wf, const std::string& in, const std::string& 
     oo.prune = spec.value("prune", true);
     oo.merge_duplicates = spec.value("merge_duplicates", true);
     oo.cache_substitute = spec.value("cache_substitute", true);
-    optimize(p.compiled, p.profile, nullptr, oo);
+    if (spec.contains("prompt_cache"))
+        p.cache = std::make_unique<PromptCache>(PromptCache::deserialize(spec.at("prompt_cache").get<std::string>()));
+    p.rewrite = optimize(p.compiled, p.profile, p.cache.get(), oo);
 
     const int W = spec.value("workers", 1);
     std::vector<std::size_t> caps = spec.value("capacities", std::vector<std::size_t>{4096});
@@ -155,6 +160,16 @@ int ref_run(const char* wf, const char* in, const char* prof, const char* spec_j
             sj.push_back(s);
         }
         j["sigma"] = sj;
+        j["rewrite"] = {{"pruned", p.rewrite.pruned}, {"merged", p.rewrite.merged},
+                        {"substituted", p.rewrite.substituted}};
+        if (spec.value("harvest", false)) {
+            // run_workflow's harvest (run_pipeline.cpp:74-79): the evaluator's
+            // synthesized values into the (possibly fresh) cache
+            if (!p.cache) p.cache = std::make_unique<PromptCache>(spec.value("cache_capacity", std::size_t{4096}));
+            Evaluator ev(p.compiled, p.profile, EvalOptions{p.cfg.seed, p.cfg.stochastic, false});
+            j["harvested"] = harvest_into_cache(p.compiled, p.profile, ev, *p.cache);
+            j["prompt_cache_out"] = p.cache->serialize();
+        }
         *out_json = dup(j.dump());
         if (plan) {
             std::vector<std::uint8_t> b = helium_b200::export_plan(p.compiled, p.profile, p.tree, p.sigma);
@@ -291,6 +306,33 @@ std::size_t ref_synth_llm_output(const std::uint64_t* p, std::size_t n, double l
     for (std::size_t k = 0; k < o.size() && k < cap; ++k) out[k] = o[k];
     return o.size();
 }
+// reference PromptCache (prompt_cache.cpp) for differential tests
+void* ref_pcache_new(std::size_t capacity) {
+    try {
+        return new PromptCache(capacity);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+void* ref_pcache_load(const char* json) {
+    try {
+        return new PromptCache(PromptCache::deserialize(json));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+void ref_pcache_free(void* h) { delete static_cast<PromptCache*>(h); }
+void ref_pcache_insert(void* h, std::uint64_t sig, const std::uint64_t* t, std::size_t n) {
+    static_cast<PromptCache*>(h)->insert(sig, TokenSeq(t, t + n));
+}
+long long ref_pcache_lookup(void* h, std::uint64_t sig) {
+    const TokenSeq* v = static_cast<PromptCache*>(h)->lookup(sig);
+    return v ? static_cast<long long>(v->size()) : -1;
+}
+char* ref_pcache_save(void* h) { return dup(static_cast<PromptCache*>(h)->serialize()); }
+
 std::uint64_t ref_fnv1a64(const void* d, std::size_t n, std::uint64_t seed) { return fnv1a64(d, n, seed); }
 std::uint64_t ref_hash_combine(std::uint64_t h, std::uint64_t v) { return hash_combine(h, v); }
 std::size_t ref_tokenize(const char* text, std::uint64_t* out, std::size_t cap) {

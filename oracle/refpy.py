@@ -69,6 +69,16 @@ def load():
     lib.ref_tokenize.argtypes = [C.c_char_p, u64p, C.c_size_t]
     lib.ref_role_marker.restype = C.c_uint64
     lib.ref_role_marker.argtypes = [C.c_int]
+    lib.ref_pcache_new.restype = C.c_void_p
+    lib.ref_pcache_new.argtypes = [C.c_size_t]
+    lib.ref_pcache_load.restype = C.c_void_p
+    lib.ref_pcache_load.argtypes = [C.c_char_p]
+    lib.ref_pcache_free.argtypes = [C.c_void_p]
+    lib.ref_pcache_insert.argtypes = [C.c_void_p, C.c_uint64, u64p, C.c_size_t]
+    lib.ref_pcache_lookup.restype = C.c_longlong
+    lib.ref_pcache_lookup.argtypes = [C.c_void_p, C.c_uint64]
+    lib.ref_pcache_save.restype = C.c_void_p
+    lib.ref_pcache_save.argtypes = [C.c_void_p]
     _lib = lib
     return lib
 
@@ -103,6 +113,37 @@ def run(workflow, inputs, profile, spec, want_plan: bool = True) -> Tuple[dict, 
         blob = C.string_at(plan, n.value)
         lib.ref_free(plan)
     return res, blob
+
+
+class PromptCache:
+    """The reference's PromptCache (prompt_cache.cpp), for differential tests."""
+
+    def __init__(self, capacity: int = 4096, _h=None):
+        self.h = _h if _h is not None else load().ref_pcache_new(capacity)
+        if not self.h:
+            raise RuntimeError(_err())
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            load().ref_pcache_free(self.h)
+            self.h = None
+
+    @staticmethod
+    def deserialize(text: str) -> "PromptCache":
+        h = load().ref_pcache_load(text.encode())
+        if not h:
+            raise RuntimeError(_err())
+        return PromptCache(_h=h)
+
+    def insert(self, sig: int, value: Sequence[int]) -> None:
+        a = np.ascontiguousarray(np.asarray(list(value) or [0], dtype=np.uint64))
+        load().ref_pcache_insert(self.h, sig, a.ctypes.data_as(u64p), len(value))
+
+    def lookup_len(self, sig: int) -> int:
+        return int(load().ref_pcache_lookup(self.h, sig))
+
+    def serialize(self) -> str:
+        return _take_str(C.c_void_p(load().ref_pcache_save(self.h)))
 
 
 def time_run_workflow(workflow, inputs, profile, spec, reps: int = 3) -> Tuple[float, str]:

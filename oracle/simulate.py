@@ -132,6 +132,9 @@ def parse_plan(blob: bytes) -> Plan:
     sigma = []
     for _ in range(u()):
         sigma.append([(s64(), s64()) for _ in range(u())])
+    if i < len(w):  # optional HKSIG001 signature section (prompt cache keys): not used by simulate()
+        assert w[i] == 0x3130304749534b48, "plan: trailing bytes"
+        i = len(w)
     assert i == len(w)
     return Plan(batch, pool, spans, nodes, outputs, tree, sigma)
 

@@ -88,6 +88,18 @@ _SIGS = {
     "hk_plan_call_groups": (C.c_int64, [u8p, C.c_size_t, C.POINTER(C.c_int64), i32p, i32p, u64p, C.c_size_t]),
     "hk_static_pin_prefixes": (C.c_int64, [u8p, C.c_size_t, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t,
                                            u64p, C.c_size_t, u64p, C.c_size_t]),
+    "hk_pcache_create": (C.c_void_p, [C.c_size_t]),
+    "hk_pcache_load": (C.c_void_p, [C.c_char_p, C.c_size_t]),
+    "hk_pcache_save": (C.c_size_t, [C.c_void_p, C.c_char_p, C.c_size_t]),
+    "hk_pcache_size": (C.c_size_t, [C.c_void_p]),
+    "hk_pcache_capacity": (C.c_size_t, [C.c_void_p]),
+    "hk_pcache_contains": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "hk_pcache_lookup": (C.c_int64, [C.c_void_p, C.c_uint64, u64p, C.c_size_t]),
+    "hk_pcache_insert": (C.c_int, [C.c_void_p, C.c_uint64, u64p, C.c_size_t]),
+    "hk_pcache_keys": (C.c_size_t, [C.c_void_p, u64p, C.c_size_t]),
+    "hk_pcache_harvest": (C.c_int64, [C.c_void_p, u8p, C.c_size_t, C.c_void_p]),
+    "hk_pcache_harvest_calls": (C.c_int64, [C.c_void_p, u8p, C.c_size_t, u64p, C.c_size_t]),
+    "hk_pcache_destroy": (None, [C.c_void_p]),
     "hk_synth_llm_len": (C.c_size_t, [u64p, C.c_size_t, C.c_double, C.c_int, C.c_uint64, C.c_int]),
     "hk_synth_llm_output": (C.c_size_t, [u64p, C.c_size_t, C.c_double, C.c_int, C.c_uint64, C.c_int, u64p,
                                          C.c_size_t]),

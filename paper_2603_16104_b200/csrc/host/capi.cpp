@@ -1,6 +1,7 @@
 // extern "C" entry points of include/helium_b200.h for the host side
 // (executor, KvCache, pins, synth, hashes). Device entry points live in
 // csrc/cuda/engine.cu.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -18,6 +19,11 @@ std::unique_ptr<LlmBody> make_device_body(hk_engine* e, const Plan& plan, const 
 struct hk_run {
     hk::SimMetrics m;
     std::string reports[3];
+};
+
+struct hk_pcache {
+    hk::PromptCache c;
+    explicit hk_pcache(hk::PromptCache x) : c(std::move(x)) {}
 };
 
 struct hk_kvcache {
@@ -250,6 +256,94 @@ int64_t hk_plan_call_groups(const uint8_t* plan, size_t plan_len, int64_t* op, i
         },
         int64_t{-1});
 }
+
+hk_pcache* hk_pcache_create(size_t capacity) {
+    return guard([&]() { return new hk_pcache(hk::PromptCache(capacity)); }, static_cast<hk_pcache*>(nullptr));
+}
+hk_pcache* hk_pcache_load(const char* json, size_t len) {
+    return guard(
+        [&]() {
+            if (!json) throw std::runtime_error("prompt cache json: null document");
+            return new hk_pcache(hk::PromptCache::deserialize(std::string(json, len)));
+        },
+        static_cast<hk_pcache*>(nullptr));
+}
+size_t hk_pcache_save(const hk_pcache* c, char* buf, size_t cap) {
+    return guard(
+        [&]() -> size_t {
+            const std::string s = c->c.serialize();
+            if (buf && cap) {
+                const size_t n = std::min(cap - 1, s.size());
+                std::memcpy(buf, s.data(), n);
+                buf[n] = 0;
+            }
+            return s.size() + 1;
+        },
+        size_t{0});
+}
+size_t hk_pcache_size(const hk_pcache* c) { return c ? c->c.size() : 0; }
+size_t hk_pcache_capacity(const hk_pcache* c) { return c ? c->c.capacity() : 0; }
+int hk_pcache_contains(const hk_pcache* c, uint64_t sig) { return c && c->c.contains(sig) ? 1 : 0; }
+int64_t hk_pcache_lookup(hk_pcache* c, uint64_t sig, uint64_t* out, size_t cap) {
+    return guard(
+        [&]() -> int64_t {
+            const hk::TokenSeq* v = c->c.lookup(sig);
+            if (!v) return -1;
+            for (size_t i = 0; i < v->size() && i < cap; ++i) out[i] = (*v)[i];
+            return static_cast<int64_t>(v->size());
+        },
+        int64_t{-2});
+}
+int hk_pcache_insert(hk_pcache* c, uint64_t sig, const uint64_t* tokens, size_t n) {
+    return guard(
+        [&]() {
+            c->c.insert(sig, hk::TokenSeq(tokens, tokens + n));
+            return 0;
+        },
+        -1);
+}
+size_t hk_pcache_keys(const hk_pcache* c, uint64_t* out, size_t cap) {
+    if (!c) return 0;
+    const std::vector<uint64_t> k = c->c.keys_lru_first();
+    for (size_t i = 0; i < k.size() && i < cap; ++i) out[i] = k[i];
+    return k.size();
+}
+int64_t hk_pcache_harvest(hk_pcache* c, const uint8_t* plan, size_t plan_len, const hk_run* run) {
+    return guard(
+        [&]() -> int64_t {
+            if (!c || !run) throw std::runtime_error("harvest_into_cache: null cache or run");
+            const hk::Plan p = hk::parse_plan(plan, plan_len);
+            return static_cast<int64_t>(hk::harvest_into_cache(p, run->m, c->c));
+        },
+        int64_t{-1});
+}
+int64_t hk_pcache_harvest_calls(hk_pcache* c, const uint8_t* plan, size_t plan_len, const uint64_t* calls,
+                                size_t n_words) {
+    return guard(
+        [&]() -> int64_t {
+            if (!c || !calls) throw std::runtime_error("harvest_into_cache: null cache or call outputs");
+            const hk::Plan p = hk::parse_plan(plan, plan_len);
+            hk::SimMetrics m;
+            size_t i = 0;
+            auto word = [&]() {
+                if (i >= n_words) throw std::runtime_error("harvest_into_cache: truncated call outputs");
+                return calls[i++];
+            };
+            const uint64_t n = word();
+            for (uint64_t k = 0; k < n; ++k) {
+                hk::CallId cid;
+                cid.op = static_cast<hk::NodeId>(word());
+                cid.query = static_cast<int>(word());
+                const uint64_t len = word();
+                hk::TokenSeq t(len);
+                for (auto& x : t) x = word();
+                m.call_outputs[cid] = std::move(t);
+            }
+            return static_cast<int64_t>(hk::harvest_into_cache(p, m, c->c));
+        },
+        int64_t{-1});
+}
+void hk_pcache_destroy(hk_pcache* c) { delete c; }
 
 size_t hk_synth_llm_len(const uint64_t* p, size_t n, double len_out, int det, uint64_t seed, int stochastic) {
     return guard([&]() { return hk::synth_llm_len(hk::TokenSeq(p, p + n), len_out, det != 0, seed, stochastic != 0); },

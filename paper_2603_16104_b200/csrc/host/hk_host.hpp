@@ -10,6 +10,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <list>
 #include <map>
 #include <memory>
 #include <set>
@@ -100,6 +101,13 @@ struct Plan {
     std::vector<int> static_group;
     std::vector<std::size_t> static_group_tokens;
     std::size_t sigma_offset = 0;  // byte offset of the schedule section in the blob
+    std::size_t sig_offset = 0;    // byte offset after the schedule (optional signature section)
+    // Optional HKSIG001 section: the reference's per-(node, query) content
+    // signatures and taint flags (compute_signatures, signature.cpp:29-104),
+    // the prompt-cache keys.
+    bool has_sigs = false;
+    std::map<NodeId, std::vector<std::uint64_t>> sig;
+    std::map<NodeId, bool> tainted;
 
     const Token* span_ptr(std::int64_t s) const { return pool.data() + spans.at(static_cast<std::size_t>(s)).first; }
     std::size_t span_len(std::int64_t s) const { return spans.at(static_cast<std::size_t>(s)).second; }
@@ -132,6 +140,41 @@ class Evaluator {
     bool stochastic_, strict_;
     std::map<std::pair<NodeId, std::size_t>, TokenSeq> memo_;
 };
+
+// ---------------------------------------------------------- prompt cache
+// class PromptCache (prompt_cache.hpp:15-40, prompt_cache.cpp:9-71): LRU map
+// from operator signature to the token sequence that operator produced,
+// serialised in the reference's JSON wire format byte for byte, so the
+// reference's optimizer (substitute_cached, optimizer.cpp:71-95) can read a
+// cache this executor harvested from device-generated outputs and the other
+// way round.
+class PromptCache {
+  public:
+    explicit PromptCache(std::size_t capacity = 4096);
+    bool contains(std::uint64_t s) const { return index_.count(s) != 0; }
+    const TokenSeq* lookup(std::uint64_t s);  // nullptr on miss; a hit refreshes recency
+    void insert(std::uint64_t s, TokenSeq value);
+    std::size_t size() const { return entries_.size(); }
+    std::size_t capacity() const { return capacity_; }
+    std::vector<std::uint64_t> keys_lru_first() const;
+    std::string serialize() const;
+    static PromptCache deserialize(const std::string& json_text);
+
+  private:
+    using Entry = std::pair<std::uint64_t, TokenSeq>;
+    std::size_t capacity_;
+    std::list<Entry> entries_;  // front = least recent
+    std::unordered_map<std::uint64_t, std::list<Entry>::iterator> index_;
+};
+std::string sig_hex(std::uint64_t s);
+
+struct SimMetrics;
+// harvest_into_cache (optimizer.cpp:113-125) with the values of THIS run: every
+// untainted format / lambda / llm node of the plan, every query, keyed by the
+// plan's signatures, llm values = the tokens the LLM body generated (device
+// transformer or synth), format / lambda values evaluated over them. Returns
+// the number of entries inserted.
+std::size_t harvest_into_cache(const Plan& plan, const SimMetrics& run, PromptCache& cache);
 
 // ---------------------------------------------------------- page pool
 // Physical KV pages of one worker. Frees are deferred to the next iteration so

@@ -120,7 +120,21 @@ Plan parse_plan(const std::uint8_t* data, std::size_t n) {
             wq.push_back(c);
         }
     }
-    if (!r.done()) fail("plan: trailing bytes");
+    p.sig_offset = r.pos();
+    if (!r.done()) {
+        // optional: per-node content signatures (signature.cpp:29-104) for the prompt cache
+        if (r.u() != 0x3130304749534b48ull) fail("plan: trailing bytes");
+        std::size_t nsig = r.count();
+        for (std::size_t k = 0; k < nsig; ++k) {
+            const NodeId id = r.i();
+            p.tainted[id] = r.u() != 0;
+            std::vector<std::uint64_t>& v = p.sig[id];
+            v.resize(p.batch);
+            for (auto& x : v) x = r.u();
+        }
+        p.has_sigs = true;
+        if (!r.done()) fail("plan: trailing bytes");
+    }
     // TRT static groups (see Plan::static_group)
     p.static_group.assign(p.tree.size(), -1);
     p.static_group_tokens.assign(p.tree.size(), 0);
@@ -180,6 +194,7 @@ std::vector<std::uint8_t> partition_calls(const std::uint8_t* data, std::size_t 
     const std::size_t head = out.size();
     out.resize(head + tail.size() * 8);
     std::memcpy(out.data() + head, tail.data(), tail.size() * 8);
+    out.insert(out.end(), data + p.sig_offset, data + n);  // signature section, if any
     return out;
 }
 

@@ -239,6 +239,93 @@ def simulate(plan: bytes, cfg: SimConfig, engine=None, verify_lookup: bool = Fal
         lib.hk_run_free(h)
 
 
+class PromptCache:
+    """class PromptCache (prompt_cache.hpp:15-40) over the C ABI: an LRU map
+    from operator signature to the tokens that operator produced, saved and
+    loaded in the reference's JSON document byte for byte (prompt_cache.cpp),
+    so the reference's optimizer (substitute_cached, optimizer.cpp:71-95) can
+    serve a warm resubmission from values this executor generated."""
+
+    def __init__(self, capacity: int = 4096, _handle=None):
+        self._lib = _lib.load()
+        self.handle = _handle if _handle is not None else self._lib.hk_pcache_create(capacity)
+        if not self.handle:
+            raise RuntimeError(_lib.last_error())
+
+    def __del__(self):
+        h, self.handle = getattr(self, "handle", None), None
+        if h:
+            self._lib.hk_pcache_destroy(h)
+
+    def contains(self, sig: int) -> bool:
+        return bool(self._lib.hk_pcache_contains(self.handle, sig))
+
+    def lookup(self, sig: int) -> Optional[List[int]]:
+        """None on miss; a hit refreshes recency."""
+        n = self._lib.hk_pcache_lookup(self.handle, sig, None, 0)
+        if n < 0:
+            return None
+        out = (C.c_uint64 * max(1, n))()
+        self._lib.hk_pcache_lookup(self.handle, sig, out, n)
+        return list(out[:n])
+
+    def insert(self, sig: int, value: Sequence[int]) -> None:
+        arr, ptr = _lib.u64_array(list(value) or [0])
+        _lib.check_status(self._lib.hk_pcache_insert(self.handle, sig, ptr, len(value)), "PromptCache.insert")
+
+    def size(self) -> int:
+        return int(self._lib.hk_pcache_size(self.handle))
+
+    def capacity(self) -> int:
+        return int(self._lib.hk_pcache_capacity(self.handle))
+
+    def keys_lru_first(self) -> List[int]:
+        n = self._lib.hk_pcache_keys(self.handle, None, 0)
+        out = (C.c_uint64 * max(1, n))()
+        self._lib.hk_pcache_keys(self.handle, out, n)
+        return list(out[:n])
+
+    def serialize(self) -> str:
+        n = self._lib.hk_pcache_save(self.handle, None, 0)
+        buf = C.create_string_buffer(n)
+        self._lib.hk_pcache_save(self.handle, buf, n)
+        return buf.value.decode()
+
+    @staticmethod
+    def deserialize(json_text: str) -> "PromptCache":
+        b = json_text.encode()
+        h = _lib.load().hk_pcache_load(b, len(b))
+        if not h:
+            raise RuntimeError(_lib.last_error())
+        return PromptCache(_handle=h)
+
+    def save(self, path: str) -> None:
+        with open(path, "w") as f:
+            f.write(self.serialize())
+
+    @staticmethod
+    def load(path: str) -> "PromptCache":
+        with open(path) as f:
+            return PromptCache.deserialize(f.read())
+
+
+def harvest_into_cache(plan: bytes, m: SimMetrics, cache: PromptCache) -> int:
+    """harvest_into_cache (optimizer.cpp:113-125) with THIS run's values: every
+    untainted format / lambda / llm node of `plan` (exported with its
+    signature section), every query; llm values are the tokens the run's LLM
+    body generated (the device transformer's under an Engine). Returns the
+    number of entries inserted."""
+    words = [len(m.call_outputs)]
+    for (op, q), toks in sorted(m.call_outputs.items()):
+        words += [op & (2**64 - 1), q, len(toks), *toks]
+    arr, ptr = _lib.u64_array(words)
+    buf = (C.c_uint8 * len(plan)).from_buffer_copy(plan)
+    n = _lib.load().hk_pcache_harvest_calls(cache.handle, buf, len(plan), ptr, len(words))
+    if n < 0:
+        raise RuntimeError(_lib.last_error())
+    return int(n)
+
+
 def sim_metrics_json(m: SimMetrics) -> str:
     return m.metrics_json
 

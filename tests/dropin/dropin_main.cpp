@@ -10,8 +10,9 @@
 // with run_sim = false and simulate_b200(r.compiled, profile,
 // build_call_tree(r.compiled, profile, r.partition.worker_of), r.schedule,
 // sim_config(spec)) — the exact arguments of :72 — and compares every
-// SimMetrics field. Prints one JSON line {"equal": {...}, ...}; exit 0 when the
-// compared fields agree (outputs are compared only without an engine: with the
+// SimMetrics field and the cross-run prompt cache both runs harvested. Prints
+// one JSON line {"equal": {...}, ...}; exit 0 when the compared fields agree
+// (outputs and cached values are compared only without an engine: with the
 // transformer body they are the model's tokens, not synth_llm_output's).
 #include <cstdio>
 #include <fstream>
@@ -79,8 +80,10 @@ int main(int argc, char** argv) {
         for (int i = 5; i + 1 < argc; ++i)
             if (std::string(argv[i]) == "--engine") engine_kind = argv[i + 1];
 
-        // 1. the reference: run_workflow with its own simulate()
-        const RunResult ref = run_workflow(g, inputs, profile, spec, nullptr);
+        // 1. the reference: run_workflow with its own simulate() (and its
+        //    prompt-cache harvest, run_pipeline.cpp:74-79)
+        PromptCache ref_cache(js.value("cache_capacity", std::size_t{4096}));
+        const RunResult ref = run_workflow(g, inputs, profile, spec, &ref_cache);
 
         // 2. the same pipeline, simulate() at run_pipeline.cpp:72 replaced by simulate_b200
         RunSpec nosim = spec;
@@ -99,8 +102,9 @@ int main(int argc, char** argv) {
             eng = hk_engine_create(&mc, &ec);
             if (!eng) throw std::runtime_error(std::string("hk_engine_create: ") + hk_last_error());
         }
+        PromptCache b_cache(js.value("cache_capacity", std::size_t{4096}));
         const SimMetrics b2 = helium_b200::simulate_b200(r.compiled, profile, call_tree, r.schedule,
-                                                         sim_config(spec), eng);
+                                                         sim_config(spec), eng, 0, &b_cache);
         if (eng) hk_engine_destroy(eng);
 
         const SimMetrics& a = ref.sim;
@@ -115,8 +119,12 @@ int main(int argc, char** argv) {
         eq["calls_csv"] = sim_calls_csv(a) == sim_calls_csv(b2);
         eq["trace_csv"] = sim_trace_csv(a) == sim_trace_csv(b2);
         eq["outputs"] = a.outputs == b2.outputs;
-        bool ok = eq["counters"] && eq["pinned_evicted"] && eq["metrics_json"] && eq["calls_csv"] && eq["trace_csv"];
-        if (!eng) ok = ok && eq["outputs"];
+        // the harvested cross-run cache: same keys and, in mode S, the same values
+        eq["prompt_cache"] = ref_cache.serialize() == b_cache.serialize();
+        eq["prompt_cache_keys"] = ref_cache.keys_lru_first() == b_cache.keys_lru_first();
+        bool ok = eq["counters"] && eq["pinned_evicted"] && eq["metrics_json"] && eq["calls_csv"] && eq["trace_csv"] &&
+                  eq["prompt_cache_keys"];
+        if (!eng) ok = ok && eq["outputs"] && eq["prompt_cache"];
         json out{{"equal", eq},
                  {"ok", ok},
                  {"engine", engine_kind.empty() ? "none (mode S)" : engine_kind},
