@@ -548,6 +548,7 @@ __device__ __forceinline__ void shared2_phase(const CUtensorMap& tm_kv, const De
         __syncwarp();
         if (lane == 0) {
             const int rows_per_head = a.Hkv * PG;  // pool-map rows between K and V of a page
+            const uint64_t pol = policy_evict_first();
             auto load = [&](int c, int v) {
                 const int b = c & 1;
                 uint64_t* full = v ? &v_full[b] : &k_full[b];
@@ -558,7 +559,12 @@ __device__ __forceinline__ void shared2_phase(const CUtensorMap& tm_kv, const De
                 for (int i = 0; i < np; ++i) {
                     const int rk = a.layer_row0 + (spg[c * 8 + i] * 2 * a.Hkv + it.kvh) * PG + v * rows_per_head;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) tma_load_2d(dst + h * SKV_BYTES / 2 + i * 2048, &tm_kv, full, h * 64, rk);
+                    for (int h = 0; h < 2; ++h) {
+                        if (a.kv_evict_first)
+                            tma_load_2d_hint(dst + h * SKV_BYTES / 2 + i * 2048, &tm_kv, full, h * 64, rk, pol);
+                        else
+                            tma_load_2d(dst + h * SKV_BYTES / 2 + i * 2048, &tm_kv, full, h * 64, rk);
+                    }
                 }
             };
             for (int c = 0; c <= nch; ++c) {
@@ -827,6 +833,14 @@ __device__ __forceinline__ void pv_issue(const CUtensorMap& tm_kv, const DecodeA
     const int rk = a.layer_row0 + (page * 2 * a.Hkv + it.kvh) * PG;
     const int rows_per_head = a.Hkv * PG;
     mbar_expect_tx(bar, 8192);
+    if (a.kv_evict_first) {
+        const uint64_t pol = policy_evict_first();
+        tma_load_2d_hint(dst, &tm_kv, bar, 0, rk, pol);
+        tma_load_2d_hint(dst + 2048, &tm_kv, bar, 64, rk, pol);
+        tma_load_2d_hint(dst + 4096, &tm_kv, bar, 0, rk + rows_per_head, pol);
+        tma_load_2d_hint(dst + 6144, &tm_kv, bar, 64, rk + rows_per_head, pol);
+        return;
+    }
     tma_load_2d(dst, &tm_kv, bar, 0, rk);
     tma_load_2d(dst + 2048, &tm_kv, bar, 64, rk);
     tma_load_2d(dst + 4096, &tm_kv, bar, 0, rk + rows_per_head);

@@ -765,6 +765,7 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
     static const std::string skip_env = std::getenv("HK_DEBUG_SKIP") ? std::getenv("HK_DEBUG_SKIP") : "";
     auto skip = [&](const char* fam) { return !skip_env.empty() && skip_env.find(fam) != std::string::npos && !dec.empty(); };
     hkd::g_trace_prefill_rows = T_pre;
+    unsigned long long* attn_trace_pending = nullptr;  // HK_ATTN_TRACE (debug)
     auto enqueue = [&]() {
     int ck = clock.begin(5, st);
     hkd::embed(embed, f32, d, d_ids, d_slots, wk.slot_last, T, x, st);
@@ -830,6 +831,23 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
                                        static_cast<bf16*>(attn), scale * 1.4426950408889634f, nullptr,
                                        l2_prefetch_o ? lw.wo : nullptr,
                                        static_cast<size_t>(d) * H * hd * esz};
+                static const bool kv_ef = !(std::getenv("HK_ATTN_KV_EVICT_FIRST") &&
+                                            std::atoi(std::getenv("HK_ATTN_KV_EVICT_FIRST")) == 0);
+                da.kv_evict_first = kv_ef ? 1 : 0;
+                // debug (HK_ATTN_TRACE="step,layer,path"): the phase stamps of ONE launch inside the
+                // real pipeline (run with HK_NO_GRAPHS=1), dumped to path after the step
+                static const char* atr = std::getenv("HK_ATTN_TRACE");
+                static unsigned long long* atr_buf = nullptr;
+                if (atr) {
+                    long st_k = -1, ly = -1;
+                    std::sscanf(atr, "%ld,%ld", &st_k, &ly);
+                    if (static_cast<long>(stats.steps) == st_k && l == ly) {
+                        if (!atr_buf) HK_CUDA(cudaMalloc(&atr_buf, 65536 * 8));
+                        HK_CUDA(cudaMemsetAsync(atr_buf, 0, 65536 * 8, st));
+                        da.trace = atr_buf;
+                        attn_trace_pending = atr_buf;
+                    }
+                }
                 da.span = hkd::gemm_trace_slot(
                     -1, static_cast<int>((dplan.shared_bytes + dplan.private_bytes + prefill_bytes) / 1024),
                     static_cast<int>(dec.size()), static_cast<int>(dplan.sh.size()), 0);
@@ -912,6 +930,17 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         }
     } else {
         enqueue();
+    }
+    if (attn_trace_pending) {
+        const char* atr = std::getenv("HK_ATTN_TRACE");
+        const char* path = std::strrchr(atr, ',');
+        std::vector<unsigned long long> h(65536);
+        HK_CUDA(cudaStreamSynchronize(st));
+        HK_CUDA(cudaMemcpy(h.data(), attn_trace_pending, h.size() * 8, cudaMemcpyDeviceToHost));
+        if (FILE* f = path ? std::fopen(path + 1, "wb") : nullptr) {
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
     }
     if (S > 0) {
         if (logits_out_host)

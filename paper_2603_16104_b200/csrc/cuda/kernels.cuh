@@ -191,6 +191,8 @@ struct DecodeAttnArgs {
     const void* l2_prefetch;    // optional: bytes the next kernel streams (O-projection weights), pulled
     size_t l2_prefetch_bytes;   // into L2 by otherwise idle warps while HBM is under-used
     unsigned long long* span = nullptr;  // debug (HK_GEMM_TRACE): launch span slot, see gemm_trace_slot
+    int kv_evict_first = 0;  // decode K/V page loads carry an L2 evict_first hint (each page is read once
+                             // per step: keeps L2 for what is reused — instructions, metadata, partials)
 };
 // Host planning of one step's decode rows. Rows of a group are consecutive
 // and share `shared_pages` leading pages of their block tables.
