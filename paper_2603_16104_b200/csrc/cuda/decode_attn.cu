@@ -967,41 +967,47 @@ __device__ __forceinline__ void private_item(const CUtensorMap& tm_kv, const Dec
         l1 += __shfl_xor_sync(0xffffffffu, l1, off);
     }
     const int h0 = 2 * tig, h1 = h0 + 1;
-    if (it.part < 0) {
-        const float i0 = l0 > 0.f ? __frcp_rn(l0) : 0.f, i1 = l1 > 0.f ? __frcp_rn(l1) : 0.f;
-        bf16* op = a.out + (static_cast<size_t>(a.dec_tok0 + it.row) * a.H + it.kvh * G) * HD + gid;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (h0 < G) {
-                op[h0 * HD + j * 16] = __float2bfloat16_rn(o[j][0] * i0);
-                op[h0 * HD + j * 16 + 8] = __float2bfloat16_rn(o[j][2] * i0);
-            }
-            if (h1 < G) {
-                op[h1 * HD + j * 16] = __float2bfloat16_rn(o[j][1] * i1);
-                op[h1 * HD + j * 16 + 8] = __float2bfloat16_rn(o[j][3] * i1);
-            }
-        }
-        return;
-    }
-    const size_t pi0 = (static_cast<size_t>(it.row) * a.H + it.kvh * G + h0) * a.max_parts + it.part;
-    const size_t pi1 = pi0 + a.max_parts;
-    bf16* po0 = part_bf16(a) + pi0 * HD + gid;
-    bf16* po1 = part_bf16(a) + pi1 * HD + gid;
+    // The G normalised rows go through the warp's (now free) ring as bf16
+    // [G][128], then out as 16-byte stores: whole 32-byte sectors, instead of
+    // 2-byte stores of the accumulator layout that leave every sector of the
+    // rows partially written until the last lane's store lands.
     const float i0 = l0 > 0.f ? __frcp_rn(l0) : 0.f, i1 = l1 > 0.f ? __frcp_rn(l1) : 0.f;
+    bf16* st = reinterpret_cast<bf16*>(ring);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         if (h0 < G) {
-            po0[j * 16] = __float2bfloat16_rn(o[j][0] * i0);
-            po0[j * 16 + 8] = __float2bfloat16_rn(o[j][2] * i0);
+            st[h0 * HD + j * 16 + gid] = __float2bfloat16_rn(o[j][0] * i0);
+            st[h0 * HD + j * 16 + gid + 8] = __float2bfloat16_rn(o[j][2] * i0);
         }
         if (h1 < G) {
-            po1[j * 16] = __float2bfloat16_rn(o[j][1] * i1);
-            po1[j * 16 + 8] = __float2bfloat16_rn(o[j][3] * i1);
+            st[h1 * HD + j * 16 + gid] = __float2bfloat16_rn(o[j][1] * i1);
+            st[h1 * HD + j * 16 + gid + 8] = __float2bfloat16_rn(o[j][3] * i1);
         }
     }
-    if (gid == 0) {
+    __syncwarp();
+    const bool direct = it.part < 0;
+    for (int c = lane; c < G * 16; c += 32) {
+        const int head = c >> 4, d8 = (c & 15) * 8;
+        const uint4 v = *reinterpret_cast<const uint4*>(st + head * HD + d8);
+        bf16* dst = direct ? a.out + (static_cast<size_t>(a.dec_tok0 + it.row) * a.H + it.kvh * G + head) * HD + d8
+                           : part_bf16(a) +
+                                 ((static_cast<size_t>(it.row) * a.H + it.kvh * G + head) * a.max_parts + it.part) * HD + d8;
+        *reinterpret_cast<uint4*>(dst) = v;
+    }
+    __syncwarp();
+    fence_proxy_async();  // the ring's next TMA writes follow these generic accesses
+    if (!direct && gid == 0) {
+        const size_t pi0 = (static_cast<size_t>(it.row) * a.H + it.kvh * G + h0) * a.max_parts + it.part;
         if (h0 < G) a.part_ml[pi0] = make_float2(m0, l0);
-        if (h1 < G) a.part_ml[pi1] = make_float2(m1, l1);
+        if (h1 < G) a.part_ml[pi0 + a.max_parts] = make_float2(m1, l1);
+        // the row's last partial also fills the rest of its 32-byte sector of (m, l)
+        // slots (masked by the merge): a partly written sector is completed from
+        // DRAM when the merge reads it — a full memory round trip on its critical path
+        if (it.part + 1 == a.n_parts[it.row])
+            for (int q = it.part + 1; q < ((it.part | 3) + 1) && q < a.max_parts; ++q) {
+                if (h0 < G) a.part_ml[pi0 - it.part + q] = make_float2(-INFINITY, 0.f);
+                if (h1 < G) a.part_ml[pi0 + a.max_parts - it.part + q] = make_float2(-INFINITY, 0.f);
+            }
     }
 }
 
@@ -1218,7 +1224,8 @@ void launch_g(const DecodeAttnArgs& a, const CUtensorMap& tm, cudaStream_t st) {
     grid += grid & 1;  // CTA pairs (clusters of 2)
     if (a.n_sh & 1) throw std::runtime_error("decode_attention: shared items must come in pairs");
     DecodeAttnArgs k = a;
-    k.merge_in_kernel = a.any_merge && grid <= g_num_sms ? 1 : 0;
+    static const bool merge_separate = std::getenv("HK_ATTN_MERGE_SEPARATE") && std::atoi(std::getenv("HK_ATTN_MERGE_SEPARATE")) != 0;
+    k.merge_in_kernel = a.any_merge && grid <= g_num_sms && !merge_separate ? 1 : 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(SH_THREADS);

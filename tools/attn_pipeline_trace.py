@@ -53,6 +53,15 @@ if not args.child:
     if len(m0):
         print(f"  queue end {q_end.max():.2f}, grid barrier entered ..{bar.max():.2f}, merge start {m0.min():.2f}.."
               f"{m0.max():.2f}, merge end ..{m1.max():.2f} us")
+        has = (cta[:, 13] > 0) & (cta[:, 17] > 0)
+        dm = (cta[has, 17] - cta[has, 13]) / 1e3
+        print("  merge per CTA (us) min/p50/p90/max: " + " ".join(f"{x:.2f}" for x in np.percentile(dm, [0, 50, 90, 100])))
+        w = cta[:, 18] > 0
+        if w.any():
+            c1 = cta[w, 19] - cta[w, 18]
+            c2 = cta[w, 20] - cta[w, 19]
+            print("  merge16 thread 0 cycles: loads+math p50 %.0f max %.0f; store p50 %.0f max %.0f" % (
+                np.median(c1), c1.max(), np.median(c2[c2 > 0]) if (c2 > 0).any() else 0, c2.max()))
     sys.exit(0)
 
 import torch  # noqa: E402
