@@ -306,6 +306,59 @@ std::size_t ref_synth_llm_output(const std::uint64_t* p, std::size_t n, double l
     for (std::size_t k = 0; k < o.size() && k < cap; ++k) out[k] = o[k];
     return o.size();
 }
+// `helios run` (tools/helios_main.cpp:83-115) with the reference simulate(),
+// for the command-line drop-in test: spec keys are the CLI flags
+// (workers, capacity list, scheduler, seed, stochastic, no_prune, no_cse,
+// no_prompt_cache, no_proactive_kv, block, prefill_budget, pin_threshold,
+// alpha, trace, no_sim, cache: prompt-cache document or absent).
+// Returns {"report","calls_csv","trace_csv","outputs_json","schedule_json","cache_out"}.
+int ref_cli_run(const char* wf, const char* in, const char* prof, const char* spec_json, char** out_json) {
+    try {
+        json a = json::parse(spec_json);
+        WorkflowGraph g = parse_workflow(wf);
+        InputBatch inputs = parse_inputs(in);
+        ProfileStats profile = parse_profile(prof);
+        RunSpec spec;
+        spec.workers = a.value("workers", 1);
+        if (a.contains("capacity")) spec.capacities = a.at("capacity").get<std::vector<std::size_t>>();
+        spec.scheduler = scheduler_kind_from_name(a.value("scheduler", std::string("cache_aware")));
+        spec.seed = a.value("seed", std::uint64_t{0});
+        spec.stochastic = a.value("stochastic", false);
+        spec.prune = !a.value("no_prune", false);
+        spec.merge_duplicates = !a.value("no_cse", false);
+        spec.cache_substitute = !a.value("no_prompt_cache", false);
+        spec.proactive_pin = !a.value("no_proactive_kv", false);
+        spec.block = a.value("block", std::size_t{16});
+        spec.prefill_budget = a.value("prefill_budget", std::size_t{0});
+        spec.pin_threshold = a.value("pin_threshold", std::size_t{200});
+        spec.alpha = a.value("alpha", 0.0);
+        spec.collect_trace = a.value("trace", false);
+        spec.run_sim = !a.value("no_sim", false);
+        PromptCache cache(65536);
+        PromptCache* cp = nullptr;
+        if (a.contains("cache") && spec.cache_substitute) {
+            if (!a.at("cache").is_null()) cache = PromptCache::deserialize(a.at("cache").get<std::string>());
+            cp = &cache;
+        }
+        RunResult r = run_workflow(g, inputs, profile, spec, cp);
+        json oj = json::object();
+        for (const auto& [node, per_query] : r.sim.outputs) {
+            json arr = json::array();
+            for (const TokenSeq& v : per_query) arr.push_back(v);
+            oj[std::to_string(node)] = std::move(arr);
+        }
+        json j{{"report", run_report_json(r, spec) + "\n"}, {"calls_csv", sim_calls_csv(r.sim)},
+               {"trace_csv", sim_trace_csv(r.sim)}, {"outputs_json", oj.dump(2) + "\n"},
+               {"schedule_json", soft_schedule_json(r.soft) + "\n"},
+               {"cache_out", cp ? json(cache.serialize()) : json(nullptr)}};
+        *out_json = dup(j.dump());
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 // reference PromptCache (prompt_cache.cpp) for differential tests
 void* ref_pcache_new(std::size_t capacity) {
     try {

@@ -69,6 +69,7 @@ def load():
     lib.ref_tokenize.argtypes = [C.c_char_p, u64p, C.c_size_t]
     lib.ref_role_marker.restype = C.c_uint64
     lib.ref_role_marker.argtypes = [C.c_int]
+    lib.ref_cli_run.argtypes = [C.c_char_p] * 4 + [C.POINTER(C.c_void_p)]
     lib.ref_pcache_new.restype = C.c_void_p
     lib.ref_pcache_new.argtypes = [C.c_size_t]
     lib.ref_pcache_load.restype = C.c_void_p
@@ -113,6 +114,15 @@ def run(workflow, inputs, profile, spec, want_plan: bool = True) -> Tuple[dict, 
         blob = C.string_at(plan, n.value)
         lib.ref_free(plan)
     return res, blob
+
+
+def cli_run(workflow, inputs, profile, flags: dict) -> dict:
+    """`helios run` (tools/helios_main.cpp:83-115) with the reference simulate():
+    report / csv / outputs / schedule documents and the saved prompt cache."""
+    out = C.c_void_p()
+    if load().ref_cli_run(_j(workflow), _j(inputs), _j(profile), _j(flags), C.byref(out)) != 0:
+        raise RuntimeError(_err())
+    return json.loads(_take_str(out))
 
 
 class PromptCache:

@@ -1,0 +1,108 @@
+"""Command-line drop-in: `helios_b200 run` (integration/
+helios_b200_main.cpp, built by oracle/Makefile against the reference library
+like tools/helios_main.cpp) takes the reference CLI's flags and files and
+writes its byte-stable reports; simulate() runs in libhelium_b200.so. With the
+synthetic LLM body (--engine none) every document must equal the reference's
+`helios run` output (tools/helios_main.cpp:83-115, restated with the reference
+simulate() in oracle/ref_capi.cpp ref_cli_run), including the workflow /
+inputs / profile JSON parsing, every scheduler, the rewrite flags and the
+--cache-file prompt cache across two submissions."""
+import json
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_2603_16104_b200 import workloads as wl
+
+ROOT = Path(__file__).resolve().parents[1]
+BIN = ROOT / "oracle" / "_ref" / "helios_b200"
+needs_bin = pytest.mark.skipif(not BIN.exists(), reason="oracle/_ref/helios_b200 not built (needs /root/reference)")
+
+
+def _cli(tmp, wf, inputs, prof, flags: dict, cache_path=None, extra=()):
+    for name, doc in (("wf", wf), ("in", inputs), ("prof", prof)):
+        (tmp / f"{name}.json").write_text(json.dumps(doc))
+    argv = [str(BIN), "run", "--workflow", str(tmp / "wf.json"), "--inputs", str(tmp / "in.json"),
+            "--profile", str(tmp / "prof.json"), "--out", str(tmp / "report.json"),
+            "--calls-out", str(tmp / "calls.csv"), "--trace-out", str(tmp / "trace.csv"),
+            "--outputs-out", str(tmp / "outputs.json"), "--schedule-out", str(tmp / "schedule.json")]
+    for k, v in flags.items():
+        opt = "--" + {"no_cse": "no-cse", "no_prune": "no-prune", "no_prompt_cache": "no-prompt-cache",
+                      "no_proactive_kv": "no-proactive-kv", "prefill_budget": "prefill-budget",
+                      "pin_threshold": "pin-threshold", "no_sim": "no-sim"}.get(k, k)
+        if v is True:
+            argv.append(opt)
+        elif k == "capacity":
+            argv += [opt, ",".join(map(str, v))]
+        elif k != "trace":
+            argv += [opt, str(v)]
+    if cache_path is not None:
+        argv += ["--cache-file", str(cache_path)]
+    argv += list(extra)
+    p = subprocess.run(argv, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr
+    return {k: (tmp / f).read_text() for k, f in (("report", "report.json"), ("calls_csv", "calls.csv"),
+                                                   ("trace_csv", "trace.csv"), ("outputs_json", "outputs.json"),
+                                                   ("schedule_json", "schedule.json"))}
+
+
+def _ref(wf, inputs, prof, flags, cache=False, cache_doc=None):
+    from oracle import refpy
+    f = dict(flags, trace=True)  # --trace-out turns trace collection on (helios_main.cpp:95)
+    if cache:
+        f["cache"] = cache_doc
+    return refpy.cli_run(wf, inputs, prof, f)
+
+
+CASES = {
+    "c1": lambda: (*wl.c1_tiny_mapred()[:3], {"capacity": [8192], "prefill_budget": 256}),
+    "c1_w2_lspf": lambda: (*wl.c1_tiny_mapred()[:3], {"workers": 2, "capacity": [8192, 4096], "scheduler": "lspf"}),
+    "t_press_random": lambda: (*wl.c2_branches(n_branches=8, prefix_words=254, decode=16, capacity=1024,
+                                               budget=128)[:3],
+                               {"capacity": [1024], "scheduler": "random", "seed": 3, "pin_threshold": 64}),
+    "c1_flags": lambda: (*wl.c1_tiny_mapred()[:3], {"no_cse": True, "no_prune": True, "no_proactive_kv": True,
+                                                    "block": 8, "alpha": 0.5, "scheduler": "op_wise"}),
+    "c1_stochastic": lambda: (*wl.c1_tiny_mapred()[:3], {"stochastic": True, "seed": 11, "scheduler": "query_wise"}),
+}
+
+
+@needs_bin
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_cli_reports_equal_reference(tmp_path, name):
+    wf, inputs, prof, flags = CASES[name]()
+    mine = _cli(tmp_path, wf, inputs, prof, flags)
+    ref = _ref(wf, inputs, prof, flags)
+    for k in mine:
+        assert mine[k] == ref[k], k
+
+
+@needs_bin
+def test_cli_prompt_cache_file_two_submissions(tmp_path):
+    """--cache-file: the first submission writes the cache, the second reads
+    it (every operator substituted) — reports and saved cache equal the
+    reference CLI's at both submissions."""
+    wf, inputs, prof, flags = CASES["c1"]()
+    cache = tmp_path / "cache.json"
+    ref_doc = None
+    for sub in range(2):
+        mine = _cli(tmp_path, wf, inputs, prof, flags, cache_path=cache)
+        ref = _ref(wf, inputs, prof, flags, cache=True, cache_doc=ref_doc)
+        ref_doc = ref["cache_out"]
+        assert mine["report"] == ref["report"], sub
+        assert cache.read_text() == ref_doc, sub
+    assert json.loads(mine["report"])["rewrite"]["substituted"] >= 5
+
+
+@needs_bin
+def test_cli_usage_errors(tmp_path):
+    p = subprocess.run([str(BIN), "run", "--workflow", "x"], capture_output=True, text=True)
+    assert p.returncode == 2 and "required" in p.stderr
+    p = subprocess.run([str(BIN), "run", "--bogus", "1"], capture_output=True, text=True)
+    assert p.returncode == 2 and "not expected" in p.stderr
+    p = subprocess.run([str(BIN), "run", "--workflow", "a", "--inputs", "b", "--profile", "c", "--format", "xml"],
+                       capture_output=True, text=True)
+    assert p.returncode == 2
+    p = subprocess.run([str(BIN), "run", "--workflow", str(tmp_path / "missing.json"), "--inputs", "b",
+                        "--profile", "c"], capture_output=True, text=True)
+    assert p.returncode == 1 and "error" in p.stderr
