@@ -1,8 +1,11 @@
 """TEST INFRASTRUCTURE ONLY — CPU fp32 restatement of the random-init decoder.
 
-PARITY UNPINNED BY THE REFERENCE: the reference (/root/reference/proj) has no
-model — its LLM operator is a hash (evaluator.cpp:37-58). This numpy decoder is
-the oracle for the transformer math of the B200 engine (csrc/cuda/engine.cu):
+The reference (/root/reference/proj) has no model — its LLM operator is a
+hash (evaluator.cpp:37-58) — so the math of this decoder is pinned to an
+independent implementation instead: HuggingFace transformers' LlamaForCausalLM
+/ Qwen2ForCausalLM in fp32 with the same weights (tests/test_oracle_hf_cpu.py).
+This numpy decoder is the oracle for the transformer math of the B200 engine
+(csrc/cuda/engine.cu):
 standard Llama-3 / Qwen2.5 decoder layers (RMSNorm, RoPE rotate-half, GQA
 causal attention, SwiGLU MLP, untied LM head, optional QKV bias) with the
 engine's counter-based weight init reproduced bit-for-bit (init_uniform_kernel,
