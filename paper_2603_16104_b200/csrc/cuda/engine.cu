@@ -173,6 +173,8 @@ struct hk_engine {
     std::map<std::vector<int64_t>, int> graph_seen;
     bool use_graphs = true;
     bool l2_prefetch_o = false;  // decode attention pulls the O-projection weights into L2 (opt-in)
+    void* pin_xbuf = nullptr;    // K6 pin-exchange buffer (grown on demand, reused across runs)
+    uint64_t pin_xbuf_bytes = 0;
     // K6 pinned-prefix replication (hk_engine_set_pin_exchange)
     int pin_role = 0;
     hk_pin_exchange_fn pin_fn = nullptr;
@@ -400,6 +402,7 @@ hk_engine::~hk_engine() {
         if (mt.done) cudaEventDestroy(mt.done);
     }
     cudaFree(meta_dev);
+    cudaFree(pin_xbuf);
     for (int32_t* b : host_bufs) cudaFreeHost(b);
     cudaStreamDestroy(st);
 }
@@ -1131,11 +1134,17 @@ class DeviceBody : public LlmBody {
             for (std::size_t j = first_new[i]; j < pin_pages[i].size(); ++j) pages.push_back(pin_pages[i][j]);
         if (pages.empty()) return;
         const uint64_t bytes = static_cast<uint64_t>(pages.size()) * hk_engine_page_bytes(e_);
-        void* buf = nullptr;
-        HK_CUDA(cudaMalloc(&buf, bytes));
+        // one exchange buffer per engine, kept across runs (no cudaMalloc/cudaFree in a timed run)
+        if (e_->pin_xbuf_bytes < bytes) {
+            e_->sync();
+            cudaFree(e_->pin_xbuf);
+            e_->pin_xbuf = nullptr;
+            HK_CUDA(cudaMalloc(&e_->pin_xbuf, bytes));
+            e_->pin_xbuf_bytes = bytes;
+        }
+        void* buf = e_->pin_xbuf;
         auto done = [&](int rc, const char* what) {
             if (rc != 0) {
-                cudaFree(buf);
                 throw std::runtime_error(std::string("simulate: pin exchange ") + what + " failed for worker " +
                                          std::to_string(w) + (rc < 0 ? ": " + std::string(hk_last_error()) : ""));
             }
@@ -1148,7 +1157,6 @@ class DeviceBody : public LlmBody {
             done(hk_pool_scatter(e_, pw(w), buf, pages.data(), pages.size()), "scatter");
         }
         e_->sync();
-        cudaFree(buf);
     }
     void sync_trie(int w, KvTree& tree) override {
         e_->trie_sync(pw(w), tree.journal(), [&tree](int node) { return tree.node_key(node); });
