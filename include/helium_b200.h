@@ -150,6 +150,17 @@ int64_t hk_static_pin_prefixes(const uint8_t* plan, size_t plan_len, int worker,
  * run on several GPUs. Writes the new HKPLAN01 blob; returns its byte size
  * (copies min(size, cap) bytes; out may be NULL) or -1. */
 int64_t hk_plan_partition_calls(const uint8_t* plan, size_t plan_len, int workers, uint8_t* out, size_t cap);
+/* Native cache-aware planner: re-plans the value graph of
+ * `plan` for `workers` workers exactly as the reference's run_workflow does
+ * (run_pipeline.cpp:47-69 with the cache-aware scheduler): partition_workflow
+ * (scheduler.cpp:59-115), build_call_tree (trt.cpp:527-530) and
+ * plan_operators + expand_soft_schedule (scheduler.cpp:474-571), with the
+ * CostParams of capacities (one, or one per worker) and alpha (0 = 1/capacity).
+ * Writes the new HKPLAN01 blob (call tree + schedule replaced, value graph and
+ * signatures kept); returns its byte size (copies min(size, cap); out may be
+ * NULL) or -1. */
+int64_t hk_plan_schedule(const uint8_t* plan, size_t plan_len, int workers, const uint64_t* capacities, size_t n_caps,
+                         double alpha, uint8_t* out, size_t cap);
 /* The plan's TRT shared-prefix groups (trt.cpp:489-530), one per llm call in
  * (op, query) order: the deepest call-tree ancestor whose whole root path is
  * static text (-1: none) and that static path's token length. The decode

@@ -85,6 +85,7 @@ _SIGS = {
     "hk_kv_counters": (None, [C.c_void_p, u64p]),
     "hk_kv_destroy": (None, [C.c_void_p]),
     "hk_plan_partition_calls": (C.c_int64, [u8p, C.c_size_t, C.c_int, u8p, C.c_size_t]),
+    "hk_plan_schedule": (C.c_int64, [u8p, C.c_size_t, C.c_int, u64p, C.c_size_t, C.c_double, u8p, C.c_size_t]),
     "hk_plan_call_groups": (C.c_int64, [u8p, C.c_size_t, C.POINTER(C.c_int64), i32p, i32p, u64p, C.c_size_t]),
     "hk_static_pin_prefixes": (C.c_int64, [u8p, C.c_size_t, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t,
                                            u64p, C.c_size_t, u64p, C.c_size_t]),

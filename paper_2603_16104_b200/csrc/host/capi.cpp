@@ -237,6 +237,18 @@ int64_t hk_plan_partition_calls(const uint8_t* plan, size_t plan_len, int worker
         int64_t{-1});
 }
 
+int64_t hk_plan_schedule(const uint8_t* plan, size_t plan_len, int workers, const uint64_t* capacities, size_t n_caps,
+                         double alpha, uint8_t* out, size_t cap) {
+    return guard(
+        [&]() -> int64_t {
+            const std::vector<uint8_t> b =
+                hk::replan(plan, plan_len, workers, std::vector<uint64_t>(capacities, capacities + n_caps), alpha);
+            if (out) std::memcpy(out, b.data(), std::min(cap, b.size()));
+            return static_cast<int64_t>(b.size());
+        },
+        int64_t{-1});
+}
+
 int64_t hk_plan_call_groups(const uint8_t* plan, size_t plan_len, int64_t* op, int32_t* query, int32_t* group,
                             uint64_t* tokens, size_t cap) {
     return guard(

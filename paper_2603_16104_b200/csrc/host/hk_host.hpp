@@ -121,6 +121,10 @@ struct Plan {
 Plan parse_plan(const std::uint8_t* data, std::size_t n);
 // opt-in call-level partition of a plan over `workers` (diverges from the reference)
 std::vector<std::uint8_t> partition_calls(const std::uint8_t* data, std::size_t n, int workers);
+// native cache-aware planner (planner.cpp): partition_workflow + build_call_tree +
+// plan_operators of the reference, over the plan's value graph, for `workers`
+std::vector<std::uint8_t> replan(const std::uint8_t* data, std::size_t n, int workers,
+                                 const std::vector<std::uint64_t>& capacities, double alpha);
 
 // -------------------------------------------------------------- evaluator
 class Evaluator {

@@ -428,6 +428,21 @@ def plan_call_groups(plan: bytes) -> Dict[tuple, tuple]:
     return {(op[i], q[i]): (g[i], t[i]) for i in range(n)}
 
 
+def plan_schedule(plan: bytes, workers: int, capacities: Sequence[int], alpha: float = 0.0) -> bytes:
+    """Native cache-aware planner (partition_workflow + build_call_tree +
+    plan_operators, scheduler.cpp / trt.cpp): the plan's value graph re-planned
+    for `workers` workers; returns the new HKPLAN01 blob."""
+    lib = _lib.load()
+    buf = (C.c_uint8 * len(plan)).from_buffer_copy(plan)
+    caps, cptr = _lib.u64_array(list(capacities))
+    n = lib.hk_plan_schedule(buf, len(plan), workers, cptr, len(capacities), alpha, None, 0)
+    if n < 0:
+        raise RuntimeError(_lib.last_error())
+    out = (C.c_uint8 * n)()
+    lib.hk_plan_schedule(buf, len(plan), workers, cptr, len(capacities), alpha, out, n)
+    return bytes(out)
+
+
 def partition_calls(plan: bytes, workers: int) -> bytes:
     """Opt-in call-level partition (hk_plan_partition_calls): every operator's
     calls dealt round-robin over `workers`. DIVERGES from the reference, which
