@@ -321,6 +321,108 @@ __global__ void qkv_rope_kv_kernel(QkvArgs a) {
     }
 }
 
+// bf16 path, vectorised: a thread owns 4 rotated pairs of a q / k head (dims
+// i..i+3 and i+64..i+67: one float4 of each half per split) or 8 values of a v
+// head, so the split-K partials come in as 16-byte loads and q / K / V go out
+// as 8- / 16-byte stores. Per element the arithmetic (split order, bias,
+// bf16 rounding before the rotation) is the scalar kernel's.
+__device__ __forceinline__ uint2 pack_bf16x4(float a, float b, float c, float d) {
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+    uint2 u;
+    u.x = *reinterpret_cast<const uint32_t*>(&lo);
+    u.y = *reinterpret_cast<const uint32_t*>(&hi);
+    return u;
+}
+__global__ void qkv_rope_kv4_kernel(QkvArgs a) {
+    pdl_trigger();
+    const RopeArgs& r = a.r;
+    const int t = blockIdx.y;
+    const int half = r.hd / 2;                 // 64
+    const int n_rot = (r.H + r.Hkv) * (half / 4);
+    const int n_v = r.Hkv * (r.hd / 8);
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n_rot + n_v) return;
+    const int QKV = (r.H + 2 * r.Hkv) * r.hd;
+    const size_t tstride = static_cast<size_t>(r.T) * QKV;
+    const float* src = a.part + static_cast<size_t>(t) * QKV;
+    const int pos = r.pos[t];
+    const bool write = r.kvw[t] != 0;
+    bf16* row = static_cast<bf16*>(r.qkv) + static_cast<size_t>(t) * QKV;
+    bf16* kv = static_cast<bf16*>(r.kv_layer);
+    const size_t head_stride = static_cast<size_t>(r.block) * r.hd;
+    const int page = write ? r.pages[r.ptab[t] + pos / r.block] : 0;
+    const bf16* bias = static_cast<const bf16*>(a.bias);
+    const bool rot = u < n_rot;
+    const int hh = rot ? u / (half / 4) : 0;
+    const int i = rot ? (u % (half / 4)) * 4 : 0;
+    const int c0 = rot ? hh * r.hd + i : (r.H + r.Hkv) * r.hd + (u - n_rot) * 8;
+    const int c1 = rot ? c0 + half : c0 + 4;
+    float b[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (bias)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            b[e] = bf2f(bias[c0 + e]);
+            b[4 + e] = bf2f(bias[c1 + e]);
+        }
+    float2 cs[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cs[e] = rot ? r.rope[static_cast<size_t>(pos) * half + i + e] : make_float2(1.f, 0.f);
+    pdl_wait();
+    float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int s0 = 0; s0 < a.splits; s0 += 4) {
+        float4 p0[4], p1[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const bool ok = s0 + s < a.splits;
+            const float* base = src + static_cast<size_t>(s0 + s) * tstride;
+            p0[s] = ok ? __ldcg(reinterpret_cast<const float4*>(base + c0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            p1[s] = ok ? __ldcg(reinterpret_cast<const float4*>(base + c1)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {  // fixed split order: deterministic
+            x[0] += p0[s].x;
+            x[1] += p0[s].y;
+            x[2] += p0[s].z;
+            x[3] += p0[s].w;
+            x[4] += p1[s].x;
+            x[5] += p1[s].y;
+            x[6] += p1[s].z;
+            x[7] += p1[s].w;
+        }
+    }
+    if (bias)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] += b[e];
+    float o[8];
+    if (rot) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            // round to bf16 first: the oracle rotates the stored qkv
+            const float x0 = bf2f(f2bf(x[e])), x1 = bf2f(f2bf(x[4 + e]));
+            o[e] = x0 * cs[e].x - x1 * cs[e].y;
+            o[4 + e] = x1 * cs[e].x + x0 * cs[e].y;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = x[e];
+    }
+    const uint2 lo = pack_bf16x4(o[0], o[1], o[2], o[3]), hi = pack_bf16x4(o[4], o[5], o[6], o[7]);
+    *reinterpret_cast<uint2*>(row + c0) = lo;
+    *reinterpret_cast<uint2*>(row + c1) = hi;
+    if (!write) return;
+    if (rot && hh >= r.H) {
+        bf16* kd = kv + ((static_cast<size_t>(page) * 2 + 0) * r.Hkv + (hh - r.H)) * head_stride +
+                   static_cast<size_t>(pos % r.block) * r.hd;
+        *reinterpret_cast<uint2*>(kd + i) = lo;
+        *reinterpret_cast<uint2*>(kd + i + half) = hi;
+    } else if (!rot) {
+        const int vc = c0 - (r.H + r.Hkv) * r.hd;
+        bf16* vd = kv + ((static_cast<size_t>(page) * 2 + 1) * r.Hkv + vc / r.hd) * head_stride +
+                   static_cast<size_t>(pos % r.block) * r.hd + vc % r.hd;
+        *reinterpret_cast<uint4*>(vd) = make_uint4(lo.x, lo.y, hi.x, hi.y);
+    }
+}
+
 // Row kernel spread over a thread-block cluster: the RS CTAs of cluster
 // (token t) each own d / RS consecutive features (one float4 per thread),
 // load the residual and every split-K partial with all loads in flight, and
@@ -491,9 +593,13 @@ void qkv_rope_kv(const QkvArgs& a, cudaStream_t st) {
     const int half = a.r.hd / 2;
     const int n = (a.r.H + a.r.Hkv) * half + a.r.Hkv * half;
     dim3 grid((n + 255) / 256, a.r.T);
+    static const bool scalar = std::getenv("HK_ROPE_SCALAR") != nullptr;  // A/B: the one-pair-per-thread kernel
     if (a.r.f32)
         launch_pdl(qkv_rope_kv_kernel<float>, grid, dim3(256), 0, st, a);
-    else
+    else if (!scalar && a.r.hd == 128) {
+        const int n4 = (a.r.H + a.r.Hkv) * (half / 4) + a.r.Hkv * (a.r.hd / 8);
+        launch_pdl(qkv_rope_kv4_kernel, dim3((n4 + 255) / 256, a.r.T), dim3(256), 0, st, a);
+    } else
         launch_pdl(qkv_rope_kv_kernel<bf16>, grid, dim3(256), 0, st, a);
     HK_LAUNCHED(1);
 }
