@@ -169,6 +169,49 @@ int64_t hk_plan_schedule(const uint8_t* plan, size_t plan_len, int workers, cons
 int64_t hk_plan_call_groups(const uint8_t* plan, size_t plan_len, int64_t* op, int32_t* query, int32_t* group,
                             uint64_t* tokens, size_t cap);
 
+/* ------------------------------------------------------ run_workflow (native) */
+/* RunSpec (run_pipeline.hpp:16-38). scheduler: "cache_aware" (the baselines
+ * random / lspf / op_wise / query_wise stay in the reference library). */
+typedef struct hk_workflow_spec {
+    int32_t workers;
+    const uint64_t* capacities; /* one, or one per worker (kv tokens) */
+    size_t n_capacities;
+    const char* scheduler;
+    uint64_t seed;
+    int32_t stochastic;
+    int32_t prune;
+    int32_t merge_duplicates;
+    int32_t cache_substitute;
+    int32_t proactive_pin;
+    uint64_t pin_threshold;
+    double pin_capacity_frac;
+    uint64_t block;
+    uint64_t prefill_budget; /* 0 = capacity/8 */
+    double alpha;            /* 0 = 1/capacity */
+    int32_t run_sim;
+    int32_t collect_trace;
+    uint64_t max_iterations;
+} hk_workflow_spec;
+typedef struct hk_pcache hk_pcache;
+/* run_workflow (run_pipeline.cpp:47-81) entirely in this library: the
+ * reference's workflow / inputs / profile JSON (workflow_io.cpp), validate +
+ * bind (workflow.cpp), rewrite (optimizer.cpp: prune, fold duplicates,
+ * prompt-cache substitution when `cache` is set), the native planner
+ * (hk_plan_schedule), simulate() with the synthetic body (engine NULL) or the
+ * device transformer, and the prompt-cache harvest of this run's values.
+ * Errors keep the reference's messages ("workflow json: ...", "format node
+ * 3: bad slot ...", "simulate: ..."). The run's documents:
+ * hk_run_report(0|1|2) = sim metrics json / calls csv / trace csv, and
+ * hk_run_document(0|1|2) = run_report_json (run_pipeline.cpp:85-112) / the
+ * CLI's outputs json (helios_main.cpp:26-34) / soft_schedule_json
+ * (scheduler.cpp:573-581), each exactly the bytes `helios run` writes for
+ * --out / --outputs-out / --schedule-out (helios_main.cpp:100-112). */
+hk_run* hk_run_workflow(const char* workflow_json, const char* inputs_json, const char* profile_json,
+                        const hk_workflow_spec* spec, hk_pcache* cache, hk_engine* engine);
+size_t hk_run_document(const hk_run* run, int which, char* buf, size_t cap);
+/* the planned HKPLAN01 of hk_run_workflow (copies min(size, cap); returns size) */
+size_t hk_run_plan(const hk_run* run, uint8_t* out, size_t cap);
+
 /* ------------------------------------------------------------ prompt cache */
 /* class PromptCache (prompt_cache.hpp:15-40): LRU from operator signature to
  * the tokens that operator produced. hk_pcache_save / hk_pcache_load use the
@@ -176,7 +219,6 @@ int64_t hk_plan_call_groups(const uint8_t* plan, size_t plan_len, int64_t* op, i
  * reference's optimizer (substitute_cached, optimizer.cpp:71-95) reads a cache
  * harvested here and vice versa. Errors keep the reference wording
  * ("prompt cache capacity must be positive", "prompt cache json: ..."). */
-typedef struct hk_pcache hk_pcache;
 hk_pcache* hk_pcache_create(size_t capacity);
 hk_pcache* hk_pcache_load(const char* json, size_t len);
 /* writes the JSON document (NUL-terminated, truncated to cap); returns bytes needed incl. NUL */

@@ -52,6 +52,15 @@ class TrieOpC(C.Structure):
                 ("phash", C.c_uint64), ("key", u64p)]
 
 
+class WorkflowSpecC(C.Structure):
+    _fields_ = [("workers", C.c_int32), ("capacities", u64p), ("n_capacities", C.c_size_t), ("scheduler", C.c_char_p),
+                ("seed", C.c_uint64), ("stochastic", C.c_int32), ("prune", C.c_int32), ("merge_duplicates", C.c_int32),
+                ("cache_substitute", C.c_int32), ("proactive_pin", C.c_int32), ("pin_threshold", C.c_uint64),
+                ("pin_capacity_frac", C.c_double), ("block", C.c_uint64), ("prefill_budget", C.c_uint64),
+                ("alpha", C.c_double), ("run_sim", C.c_int32), ("collect_trace", C.c_int32),
+                ("max_iterations", C.c_uint64)]
+
+
 class EngineStatsC(C.Structure):
     _fields_ = [("pin_ms", C.c_double), ("iter_ms", C.c_double), ("h2d_bytes", C.c_uint64),
                 ("d2h_bytes", C.c_uint64), ("launches", C.c_uint64), ("steps", C.c_uint64),
@@ -89,6 +98,10 @@ _SIGS = {
     "hk_plan_call_groups": (C.c_int64, [u8p, C.c_size_t, C.POINTER(C.c_int64), i32p, i32p, u64p, C.c_size_t]),
     "hk_static_pin_prefixes": (C.c_int64, [u8p, C.c_size_t, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t,
                                            u64p, C.c_size_t, u64p, C.c_size_t]),
+    "hk_run_workflow": (C.c_void_p, [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(WorkflowSpecC), C.c_void_p,
+                                     C.c_void_p]),
+    "hk_run_document": (C.c_size_t, [C.c_void_p, C.c_int, C.c_char_p, C.c_size_t]),
+    "hk_run_plan": (C.c_size_t, [C.c_void_p, u8p, C.c_size_t]),
     "hk_pcache_create": (C.c_void_p, [C.c_size_t]),
     "hk_pcache_load": (C.c_void_p, [C.c_char_p, C.c_size_t]),
     "hk_pcache_save": (C.c_size_t, [C.c_void_p, C.c_char_p, C.c_size_t]),

@@ -22,6 +22,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "libhelium_b200.so"
+CLI = PKG / "helios_b200"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -87,15 +88,24 @@ def build(verbose: bool = False) -> Path:
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
         os.replace(tmp, LIB)
+    # the self-contained command line (csrc/cli): `helios run` over the C ABI
+    cli_src = CSRC / "cli" / "helios_b200.cpp"
+    if not CLI.exists() or CLI.stat().st_mtime < max(LIB.stat().st_mtime, cli_src.stat().st_mtime, hdr_mtime):
+        cmd = [CXX, "-std=c++20", "-O2", "-Wall", f"-I{ROOT / 'include'}", str(cli_src), "-o", str(CLI),
+               f"-L{PKG}", "-lhelium_b200", "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"cli build failed:\n{r.stdout}\n{r.stderr}")
     if verbose:
-        print(f"built {LIB}")
+        print(f"built {LIB} and {CLI}")
     return LIB
 
 
 def clean():
     shutil.rmtree(OBJ, ignore_errors=True)
-    if LIB.exists():
-        LIB.unlink()
+    for f in (LIB, CLI):
+        if f.exists():
+            f.unlink()
 
 
 if __name__ == "__main__":

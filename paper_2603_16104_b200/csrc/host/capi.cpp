@@ -19,6 +19,8 @@ std::unique_ptr<LlmBody> make_device_body(hk_engine* e, const Plan& plan, const 
 struct hk_run {
     hk::SimMetrics m;
     std::string reports[3];
+    std::string docs[3];            // hk_run_workflow: report json, outputs json, soft schedule json
+    std::vector<uint8_t> plan;      // hk_run_workflow: the planned HKPLAN01
 };
 
 struct hk_pcache {
@@ -100,6 +102,66 @@ hk_run* hk_simulate_ex(const uint8_t* plan, size_t plan_len, const hk_sim_config
             return run.release();
         },
         nullptr);
+}
+
+hk_run* hk_run_workflow(const char* workflow_json, const char* inputs_json, const char* profile_json,
+                        const hk_workflow_spec* spec, hk_pcache* cache, hk_engine* engine) {
+    return guard(
+        [&]() -> hk_run* {
+            if (!workflow_json || !inputs_json || !profile_json || !spec)
+                throw std::runtime_error("hk_run_workflow: null argument");
+            hk::WorkflowSpec ws;
+            ws.workers = spec->workers;
+            ws.capacities.assign(spec->capacities, spec->capacities + spec->n_capacities);
+            ws.scheduler = spec->scheduler ? spec->scheduler : "cache_aware";
+            ws.seed = spec->seed;
+            ws.stochastic = spec->stochastic != 0;
+            ws.prune = spec->prune != 0;
+            ws.merge_duplicates = spec->merge_duplicates != 0;
+            ws.cache_substitute = spec->cache_substitute != 0;
+            ws.proactive_pin = spec->proactive_pin != 0;
+            ws.pin_threshold = spec->pin_threshold;
+            ws.pin_capacity_frac = spec->pin_capacity_frac;
+            ws.block = spec->block;
+            ws.prefill_budget = spec->prefill_budget;
+            ws.alpha = spec->alpha;
+            ws.run_sim = spec->run_sim != 0;
+            ws.collect_trace = spec->collect_trace != 0;
+            ws.max_iterations = spec->max_iterations;
+            hk::BodyFactory mk = [engine](const hk::Plan& p, const hk::SimConfig& sc) -> std::unique_ptr<hk::LlmBody> {
+                if (engine) return hk::make_device_body(engine, p, sc, -1);
+                return std::make_unique<hk::SyntheticBody>(sc.seed, sc.stochastic);
+            };
+            hk::WorkflowRun wr = hk::run_workflow(workflow_json, inputs_json, profile_json, ws, cache ? &cache->c : nullptr, mk);
+            auto run = std::make_unique<hk_run>();
+            run->m = std::move(wr.metrics);
+            run->reports[0] = hk::sim_metrics_json(run->m);
+            run->reports[1] = wr.calls_csv;
+            run->reports[2] = wr.trace_csv;
+            run->docs[0] = wr.report_json;
+            run->docs[1] = wr.outputs_json;
+            run->docs[2] = wr.schedule_json;
+            run->plan = std::move(wr.plan);
+            return run.release();
+        },
+        static_cast<hk_run*>(nullptr));
+}
+
+size_t hk_run_document(const hk_run* r, int which, char* buf, size_t cap) {
+    if (!r || which < 0 || which > 2) return 0;
+    const std::string& s = r->docs[which];
+    if (buf && cap) {
+        const size_t n = std::min(cap - 1, s.size());
+        std::memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    }
+    return s.size() + 1;
+}
+
+size_t hk_run_plan(const hk_run* r, uint8_t* out, size_t cap) {
+    if (!r) return 0;
+    if (out) std::memcpy(out, r->plan.data(), std::min(cap, r->plan.size()));
+    return r->plan.size();
 }
 
 int hk_run_metrics(const hk_run* r, hk_metrics* o) {

@@ -125,6 +125,15 @@ std::vector<std::uint8_t> partition_calls(const std::uint8_t* data, std::size_t 
 // plan_operators of the reference, over the plan's value graph, for `workers`
 std::vector<std::uint8_t> replan(const std::uint8_t* data, std::size_t n, int workers,
                                  const std::vector<std::uint64_t>& capacities, double alpha);
+struct PlanOutcome {
+    std::vector<std::uint8_t> blob;                    // HKPLAN01 with the new call tree + schedule
+    std::vector<std::vector<std::vector<NodeId>>> soft;  // SoftSchedule (inner sequences per worker)
+    std::vector<std::vector<CallId>> sigma;
+    std::uint64_t passes = 0, forced_emits = 0, emitted = 0;  // SchedulerStats
+    double makespan = 0;                               // evaluate_schedule (cost_model.cpp:32-120)
+};
+PlanOutcome replan_full(const std::uint8_t* data, std::size_t n, int workers,
+                        const std::vector<std::uint64_t>& capacities, double alpha);
 
 // -------------------------------------------------------------- evaluator
 class Evaluator {
@@ -448,5 +457,36 @@ struct ExecOptions {
 };
 
 SimMetrics simulate(const Plan& plan, const SimConfig& cfg, LlmBody& body, const ExecOptions& opts = {});
+
+// ------------------------------------------------------- run_workflow (native)
+// RunSpec (run_pipeline.hpp:16-38) and the documents of `helios run`
+// (pipeline.cpp): parse -> bind -> rewrite -> plan -> simulate -> reports.
+struct WorkflowSpec {
+    int workers = 1;
+    std::vector<std::uint64_t> capacities = {4096};
+    std::string scheduler = "cache_aware";
+    std::uint64_t seed = 0;
+    bool stochastic = false;
+    bool prune = true, merge_duplicates = true, cache_substitute = true;
+    bool proactive_pin = true;
+    std::size_t pin_threshold = 200;
+    double pin_capacity_frac = 0.5;
+    std::size_t block = 16, prefill_budget = 0;
+    double alpha = 0;
+    bool run_sim = true, collect_trace = false;
+    std::uint64_t max_iterations = 0;
+};
+struct WorkflowRun {
+    std::vector<std::uint8_t> plan;  // the planned HKPLAN01
+    SimMetrics metrics;
+    std::string report_json, calls_csv, trace_csv, outputs_json, schedule_json;
+};
+using BodyFactory = std::function<std::unique_ptr<LlmBody>(const Plan&, const SimConfig&)>;
+WorkflowRun run_workflow(const std::string& workflow_json, const std::string& inputs_json,
+                         const std::string& profile_json, const WorkflowSpec& spec, PromptCache* cache,
+                         const BodyFactory& make_body);
+// harvest_into_cache with the Evaluator's synthesized llm values (run_pipeline.cpp:74-79 as
+// the reference does it): for runs whose LLM body did not run (run_sim = false)
+std::size_t harvest_into_cache_synth(const Plan& plan, std::uint64_t seed, bool stochastic, PromptCache& cache);
 
 }  // namespace hk

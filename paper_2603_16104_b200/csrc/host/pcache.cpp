@@ -256,10 +256,25 @@ PromptCache PromptCache::deserialize(const std::string& json_text) {
     return c;
 }
 
+namespace {
+std::size_t harvest(const Plan& plan, Evaluator& ev, PromptCache& cache);
+}  // namespace
+
 std::size_t harvest_into_cache(const Plan& plan, const SimMetrics& run, PromptCache& cache) {
     if (!plan.has_sigs) fail("harvest_into_cache: the plan carries no signatures (export it with them)");
     Evaluator ev(plan, 0, false, /*strict_llm=*/true);
     for (const auto& [cid, toks] : run.call_outputs) ev.put_llm_output(cid.op, static_cast<std::size_t>(cid.query), toks);
+    return harvest(plan, ev, cache);
+}
+
+std::size_t harvest_into_cache_synth(const Plan& plan, std::uint64_t seed, bool stochastic, PromptCache& cache) {
+    if (!plan.has_sigs) fail("harvest_into_cache: the plan carries no signatures (export it with them)");
+    Evaluator ev(plan, seed, stochastic, /*strict_llm=*/false);
+    return harvest(plan, ev, cache);
+}
+
+namespace {
+std::size_t harvest(const Plan& plan, Evaluator& ev, PromptCache& cache) {
     std::size_t inserted = 0;
     for (const auto& [id, n] : plan.nodes) {  // ascending ids: the reference's map order
         if (n.kind != Kind::kFormat && n.kind != Kind::kLambda && n.kind != Kind::kLlm) continue;
@@ -275,5 +290,6 @@ std::size_t harvest_into_cache(const Plan& plan, const SimMetrics& run, PromptCa
     }
     return inserted;
 }
+}  // namespace
 
 }  // namespace hk

@@ -586,6 +586,7 @@ struct Planner {
     std::vector<std::vector<InnerSeq>> out;
     bool force_active = false;
     std::size_t emitted_count = 0;
+    std::uint64_t passes = 0, forced_emits = 0;  // SchedulerStats (scheduler.hpp:33-40)
 
     Planner(const Trt& t, const std::vector<WorkerParams>& p, std::size_t b) : tree(t), params(p), batch(b) {}
 
@@ -626,7 +627,10 @@ struct Planner {
         prev_leaf[w] = leaf;
         for (int n : paths.at(leaf)) unemitted_under[static_cast<std::size_t>(n)]--;
         ++emitted_count;
-        force_active = false;
+        if (force_active) {
+            force_active = false;
+            ++forced_emits;
+        }
         const GroupKey gk = group_of.at(leaf);
         GroupState& g = groups.at(gk);
         g.emitted.push_back(leaf);
@@ -837,9 +841,15 @@ struct Planner {
     }
 };
 
+struct Scheduled {
+    std::vector<std::vector<InnerSeq>> soft;
+    std::vector<std::vector<CallId>> sigma;
+    std::uint64_t passes = 0, forced_emits = 0, emitted = 0;
+};
+
 // scheduler.cpp:474-561 + expand_soft_schedule (:563-571)
-std::vector<std::vector<CallId>> plan_operators(const GraphView& g, const std::vector<WorkerParams>& params,
-                                               const std::map<NodeId, int>& worker_of) {
+Scheduled plan_operators(const GraphView& g, const std::vector<WorkerParams>& params,
+                         const std::map<NodeId, int>& worker_of) {
     const Trt tree = build_tree(g, worker_of, false);
     for (const auto& [op, w] : worker_of)
         if (w < 0 || w >= static_cast<int>(params.size()))
@@ -895,18 +905,80 @@ std::vector<std::vector<CallId>> plan_operators(const GraphView& g, const std::v
     }
     const std::size_t total = tree.leaves().size();
     while (pl.emitted_count < total) {
+        ++pl.passes;
         pl.force_active = false;
         if (pl.recurse(tree.root())) continue;
         pl.force_active = true;
+        ++pl.passes;
         if (!pl.recurse(tree.root())) fail("scheduling stalled: dependency cycle among llm operators");
     }
     pl.flush_remaining();
-    std::vector<std::vector<CallId>> sigma(pl.out.size());
+    Scheduled r;
+    r.sigma.resize(pl.out.size());
     for (std::size_t w = 0; w < pl.out.size(); ++w)
         for (const InnerSeq& seq : pl.out[w])
             for (NodeId op : seq)
-                for (std::size_t b = 0; b < g.p.batch; ++b) sigma[w].push_back(CallId{op, static_cast<int>(b)});
-    return sigma;
+                for (std::size_t b = 0; b < g.p.batch; ++b) r.sigma[w].push_back(CallId{op, static_cast<int>(b)});
+    r.soft = std::move(pl.out);
+    r.passes = pl.passes;
+    r.forced_emits = pl.forced_emits;
+    r.emitted = pl.emitted_count;
+    return r;
+}
+
+// evaluate_schedule (cost_model.cpp:32-120): replay sigma against the analytic
+// model over the call tree; returns the makespan
+double evaluate_schedule(const Trt& tree, const std::vector<std::vector<CallId>>& sigma,
+                         const std::vector<WorkerParams>& params) {
+    std::size_t total = 0;
+    for (const auto& wq : sigma) total += wq.size();
+    if (total != tree.leaves().size())
+        fail("schedule covers " + std::to_string(total) + " of " + std::to_string(tree.leaves().size()) + " calls");
+    std::map<int, double> complete_at, delay_of;
+    std::vector<std::size_t> next(sigma.size(), 0);
+    std::vector<double> frontier(sigma.size(), 0.0);
+    std::vector<int> prev_leaf(sigma.size(), -1);
+    double makespan = 0;
+    std::size_t placed = 0;
+    bool progress = true;
+    while (placed < total && progress) {
+        progress = false;
+        for (std::size_t w = 0; w < sigma.size(); ++w) {
+            while (next[w] < sigma[w].size()) {
+                const CallId& c = sigma[w][next[w]];
+                const int lf = tree.leaf_index(c.op, c.query);
+                if (lf < 0) fail("schedule names unknown call");
+                const TNode& leaf = tree.node(lf);
+                double ready = 0.0;
+                bool blocked = false;
+                for (int p : leaf.preds) {
+                    auto it = complete_at.find(p);
+                    if (it == complete_at.end()) {
+                        blocked = true;
+                        break;
+                    }
+                    ready = std::max(ready, it->second + delay_of.at(p));
+                }
+                if (blocked) break;
+                const WorkerParams& wp = params[w];
+                const double alpha = wp.resolved_alpha();
+                const double u_p = tree.prefill_weight(prev_leaf[w], lf);
+                const double usage = total_usage(alpha, leaf.leaf.len_out, u_p);
+                const double begin = std::max(frontier[w], ready);
+                const double complete = begin + usage;
+                complete_at[lf] = complete;
+                delay_of[lf] = precedence_delay(alpha, wp.capacity, leaf.leaf.len_out);
+                frontier[w] = complete;
+                prev_leaf[w] = lf;
+                makespan = std::max(makespan, complete);
+                ++next[w];
+                ++placed;
+                progress = true;
+            }
+        }
+    }
+    if (placed < total) fail("schedule deadlock");
+    return makespan;
 }
 
 // ---------------------------------------------------------------- writer
@@ -928,8 +1000,8 @@ class Writer {
 // graph, outputs and signatures are kept; the call tree is rebuilt for the new
 // partition (build_call_tree, trt.cpp:527-530) and the schedule comes from
 // plan_operators over the capacities (run_pipeline.cpp:47-69, cache-aware).
-std::vector<std::uint8_t> replan(const std::uint8_t* data, std::size_t n, int workers,
-                                 const std::vector<std::uint64_t>& capacities, double alpha) {
+PlanOutcome replan_full(const std::uint8_t* data, std::size_t n, int workers,
+                        const std::vector<std::uint64_t>& capacities, double alpha) {
     const Plan p = parse_plan(data, n);
     if (workers < 1) fail("workers must be positive");
     if (capacities.empty()) fail("no worker capacities given");
@@ -942,8 +1014,16 @@ std::vector<std::uint8_t> replan(const std::uint8_t* data, std::size_t n, int wo
                                       alpha});
     const GraphView g(p);
     const std::map<NodeId, int> worker_of = partition_workflow(g, workers);
-    const std::vector<std::vector<CallId>> sigma = plan_operators(g, params, worker_of);
+    Scheduled sch = plan_operators(g, params, worker_of);
+    const std::vector<std::vector<CallId>>& sigma = sch.sigma;
     const Trt tree = build_tree(g, worker_of, true);
+    PlanOutcome res;
+    res.makespan = evaluate_schedule(tree, sigma, params);
+    res.passes = sch.passes;
+    res.forced_emits = sch.forced_emits;
+    res.emitted = sch.emitted;
+    res.soft = sch.soft;
+    res.sigma = sigma;
 
     // re-serialise: token pool + spans (the plan's, then the tree's new static runs)
     Writer wr;
@@ -1010,10 +1090,16 @@ std::vector<std::uint8_t> replan(const std::uint8_t* data, std::size_t n, int wo
             wr.i(c.query);
         }
     }
-    std::vector<std::uint8_t> out(wr.w.size() * 8);
+    std::vector<std::uint8_t>& out = res.blob;
+    out.resize(wr.w.size() * 8);
     std::memcpy(out.data(), wr.w.data(), out.size());
     out.insert(out.end(), data + p.sig_offset, data + n);  // signature section, if any
-    return out;
+    return res;
+}
+
+std::vector<std::uint8_t> replan(const std::uint8_t* data, std::size_t n, int workers,
+                                 const std::vector<std::uint64_t>& capacities, double alpha) {
+    return replan_full(data, n, workers, capacities, alpha).blob;
 }
 
 }  // namespace hk

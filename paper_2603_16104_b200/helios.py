@@ -326,6 +326,42 @@ def harvest_into_cache(plan: bytes, m: SimMetrics, cache: PromptCache) -> int:
     return int(n)
 
 
+def run_workflow(workflow: str, inputs: str, profile: str, workers: int = 1, capacities=(4096,),
+                 cache: Optional["PromptCache"] = None, engine=None, **spec) -> dict:
+    """run_workflow (run_pipeline.cpp:47-81) natively: the reference's JSON
+    documents in, `helios run`'s documents out ({"report", "calls_csv",
+    "trace_csv", "outputs_json", "schedule_json", "plan"}). spec keys mirror
+    RunSpec: seed, stochastic, prune, merge_duplicates, cache_substitute,
+    proactive_pin, pin_threshold, pin_capacity_frac, block, prefill_budget,
+    alpha, run_sim, collect_trace, max_iterations."""
+    lib = _lib.load()
+    caps, cptr = _lib.u64_array(list(capacities))
+    c = _lib.WorkflowSpecC(workers, cptr, len(capacities), spec.get("scheduler", "cache_aware").encode(),
+                           spec.get("seed", 0), int(spec.get("stochastic", False)), int(spec.get("prune", True)),
+                           int(spec.get("merge_duplicates", True)), int(spec.get("cache_substitute", True)),
+                           int(spec.get("proactive_pin", True)), spec.get("pin_threshold", 200),
+                           spec.get("pin_capacity_frac", 0.5), spec.get("block", 16), spec.get("prefill_budget", 0),
+                           spec.get("alpha", 0.0), int(spec.get("run_sim", True)), int(spec.get("collect_trace", False)),
+                           spec.get("max_iterations", 0))
+    h = lib.hk_run_workflow(workflow.encode(), inputs.encode(), profile.encode(), C.byref(c),
+                            cache.handle if cache is not None else None, engine.handle if engine is not None else None)
+    if not h:
+        raise RuntimeError(_lib.last_error())
+    try:
+        def doc(which):
+            n = lib.hk_run_document(h, which, None, 0)
+            buf = C.create_string_buffer(n)
+            lib.hk_run_document(h, which, buf, n)
+            return buf.value.decode()
+        n = lib.hk_run_plan(h, None, 0)
+        plan = (C.c_uint8 * n)()
+        lib.hk_run_plan(h, plan, n)
+        return {"report": doc(0), "outputs_json": doc(1), "schedule_json": doc(2), "calls_csv": _report(h, 1),
+                "trace_csv": _report(h, 2), "plan": bytes(plan)}
+    finally:
+        lib.hk_run_free(h)
+
+
 def sim_metrics_json(m: SimMetrics) -> str:
     return m.metrics_json
 

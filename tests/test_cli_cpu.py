@@ -16,14 +16,17 @@ import pytest
 from paper_2603_16104_b200 import workloads as wl
 
 ROOT = Path(__file__).resolve().parents[1]
-BIN = ROOT / "oracle" / "_ref" / "helios_b200"
+BIN = ROOT / "oracle" / "_ref" / "helios_b200"          # linked against the reference library
+NATIVE = ROOT / "paper_2603_16104_b200" / "helios_b200"  # self-contained (build.py)
 needs_bin = pytest.mark.skipif(not BIN.exists(), reason="oracle/_ref/helios_b200 not built (needs /root/reference)")
+needs_ref = pytest.mark.skipif(not (ROOT / "oracle" / "_ref" / "libhelios_ref.so").exists(),
+                               reason="reference library not built")
 
 
-def _cli(tmp, wf, inputs, prof, flags: dict, cache_path=None, extra=()):
+def _cli(tmp, wf, inputs, prof, flags: dict, cache_path=None, extra=(), binary=None):
     for name, doc in (("wf", wf), ("in", inputs), ("prof", prof)):
-        (tmp / f"{name}.json").write_text(json.dumps(doc))
-    argv = [str(BIN), "run", "--workflow", str(tmp / "wf.json"), "--inputs", str(tmp / "in.json"),
+        (tmp / f"{name}.json").write_text(doc if isinstance(doc, str) else json.dumps(doc))
+    argv = [str(binary or BIN), "run", "--workflow", str(tmp / "wf.json"), "--inputs", str(tmp / "in.json"),
             "--profile", str(tmp / "prof.json"), "--out", str(tmp / "report.json"),
             "--calls-out", str(tmp / "calls.csv"), "--trace-out", str(tmp / "trace.csv"),
             "--outputs-out", str(tmp / "outputs.json"), "--schedule-out", str(tmp / "schedule.json")]
@@ -31,6 +34,8 @@ def _cli(tmp, wf, inputs, prof, flags: dict, cache_path=None, extra=()):
         opt = "--" + {"no_cse": "no-cse", "no_prune": "no-prune", "no_prompt_cache": "no-prompt-cache",
                       "no_proactive_kv": "no-proactive-kv", "prefill_budget": "prefill-budget",
                       "pin_threshold": "pin-threshold", "no_sim": "no-sim"}.get(k, k)
+        if v is False:
+            continue
         if v is True:
             argv.append(opt)
         elif k == "capacity":
@@ -67,6 +72,19 @@ CASES = {
 }
 
 
+CASES.update({
+    "c1_w2_native": lambda: (*wl.c1_tiny_mapred()[:3], {"workers": 2, "capacity": [8192, 4096]}),
+    "c1_flags_native": lambda: (*wl.c1_tiny_mapred()[:3], {"no_cse": True, "no_prune": True, "no_proactive_kv": True,
+                                                           "block": 8, "alpha": 0.5}),
+    "c1_stochastic_native": lambda: (*wl.c1_tiny_mapred()[:3], {"stochastic": True, "seed": 11}),
+    "t_press_native": lambda: (*wl.c2_branches(n_branches=8, prefix_words=254, decode=16, capacity=1024,
+                                               budget=128)[:3], {"capacity": [1024], "pin_threshold": 64}),
+    "c4_w2_native": lambda: (*wl.c4_overlap(workers=2)[:3], {"workers": 2, "capacity": [262144],
+                                                             "prefill_budget": 8192}),
+    "c1_nosim_native": lambda: (*wl.c1_tiny_mapred()[:3], {"no_sim": True}),
+})
+
+
 @needs_bin
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_cli_reports_equal_reference(tmp_path, name):
@@ -77,8 +95,47 @@ def test_cli_reports_equal_reference(tmp_path, name):
         assert mine[k] == ref[k], k
 
 
+@needs_ref
+@pytest.mark.parametrize("name", sorted(k for k, c in CASES.items() if "scheduler" not in c()[3]))
+def test_native_cli_reports_equal_reference(tmp_path, name):
+    """The self-contained helios_b200 (JSON IO, bind, rewrites, planner,
+    simulate and reports all in libhelium_b200.so) against the reference CLI
+    path, byte for byte."""
+    wf, inputs, prof, flags = CASES[name]()
+    mine = _cli(tmp_path, wf, inputs, prof, flags, binary=NATIVE)
+    ref = _ref(wf, inputs, prof, flags)
+    for k in mine:
+        assert mine[k] == ref[k], k
+
+
+@needs_ref
+@pytest.mark.parametrize("seed", range(30))
+def test_native_cli_random_workflows(tmp_path, seed):
+    """Random DAGs of every operator kind (workload_gen.cpp:427-489), with
+    duplicate subgraphs (CSE), dead nodes (prune), nondeterministic llms,
+    1-3 workers, two --cache-file submissions."""
+    import random
+    from oracle import refpy
+    rng = random.Random(seed)
+    wf, inp, prof = refpy.generate_workload(
+        {"llm_ops": rng.randint(1, 6), "batch": rng.randint(1, 4), "allow_nondeterminism": True, "seed": seed},
+        random=True)
+    flags = {"workers": rng.choice([1, 2, 3]), "capacity": [rng.choice([64, 256, 4096])], "seed": seed,
+             "stochastic": rng.random() < 0.3}
+    cache = tmp_path / "cache.json"
+    ref_doc = None
+    for sub in range(2):
+        mine = _cli(tmp_path, wf, inp, prof, flags, cache_path=cache, binary=NATIVE)
+        ref = _ref(wf, inp, prof, flags, cache=True, cache_doc=ref_doc)
+        ref_doc = ref["cache_out"]
+        for k in mine:
+            assert mine[k] == ref[k], (sub, k)
+        assert cache.read_text() == ref_doc, sub
+
+
 @needs_bin
-def test_cli_prompt_cache_file_two_submissions(tmp_path):
+@pytest.mark.parametrize("native", [False, True])
+def test_cli_prompt_cache_file_two_submissions(tmp_path, native):
     """--cache-file: the first submission writes the cache, the second reads
     it (every operator substituted) — reports and saved cache equal the
     reference CLI's at both submissions."""
@@ -86,7 +143,7 @@ def test_cli_prompt_cache_file_two_submissions(tmp_path):
     cache = tmp_path / "cache.json"
     ref_doc = None
     for sub in range(2):
-        mine = _cli(tmp_path, wf, inputs, prof, flags, cache_path=cache)
+        mine = _cli(tmp_path, wf, inputs, prof, flags, cache_path=cache, binary=NATIVE if native else BIN)
         ref = _ref(wf, inputs, prof, flags, cache=True, cache_doc=ref_doc)
         ref_doc = ref["cache_out"]
         assert mine["report"] == ref["report"], sub
@@ -95,14 +152,16 @@ def test_cli_prompt_cache_file_two_submissions(tmp_path):
 
 
 @needs_bin
-def test_cli_usage_errors(tmp_path):
-    p = subprocess.run([str(BIN), "run", "--workflow", "x"], capture_output=True, text=True)
+@pytest.mark.parametrize("native", [False, True])
+def test_cli_usage_errors(tmp_path, native):
+    BIN_ = NATIVE if native else BIN
+    p = subprocess.run([str(BIN_), "run", "--workflow", "x"], capture_output=True, text=True)
     assert p.returncode == 2 and "required" in p.stderr
-    p = subprocess.run([str(BIN), "run", "--bogus", "1"], capture_output=True, text=True)
+    p = subprocess.run([str(BIN_), "run", "--bogus", "1"], capture_output=True, text=True)
     assert p.returncode == 2 and "not expected" in p.stderr
-    p = subprocess.run([str(BIN), "run", "--workflow", "a", "--inputs", "b", "--profile", "c", "--format", "xml"],
+    p = subprocess.run([str(BIN_), "run", "--workflow", "a", "--inputs", "b", "--profile", "c", "--format", "xml"],
                        capture_output=True, text=True)
     assert p.returncode == 2
-    p = subprocess.run([str(BIN), "run", "--workflow", str(tmp_path / "missing.json"), "--inputs", "b",
+    p = subprocess.run([str(BIN_), "run", "--workflow", str(tmp_path / "missing.json"), "--inputs", "b",
                         "--profile", "c"], capture_output=True, text=True)
     assert p.returncode == 1 and "error" in p.stderr

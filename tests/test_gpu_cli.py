@@ -8,15 +8,16 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-from test_cli_cpu import BIN, _cli, _ref, needs_bin  # noqa: E402
+from test_cli_cpu import BIN, NATIVE, _cli, _ref, needs_bin  # noqa: E402
 from paper_2603_16104_b200 import workloads as wl  # noqa: E402
 
 
 @needs_bin
-def test_cli_device_engine_single_operator(tmp_path):
+@pytest.mark.parametrize("native", [False, True])
+def test_cli_device_engine_single_operator(tmp_path, native):
     wf, inputs, prof, _ = wl.c2_branches(n_branches=8, prefix_words=254, decode=16, capacity=1024, budget=128)
     flags = {"capacity": [1024], "pin_threshold": 64}
-    mine = _cli(tmp_path, wf, inputs, prof, flags, extra=("--engine", "tiny"))
+    mine = _cli(tmp_path, wf, inputs, prof, flags, extra=("--engine", "tiny"), binary=NATIVE if native else BIN)
     ref = _ref(wf, inputs, prof, flags)
     assert mine["report"] == ref["report"]
     assert mine["calls_csv"] == ref["calls_csv"] and mine["trace_csv"] == ref["trace_csv"]
