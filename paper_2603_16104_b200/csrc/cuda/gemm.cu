@@ -42,6 +42,7 @@ struct GemmParams {
     float* partial;
     int cluster;  // 1: the grid.z split-K CTAs form a cluster and reduce through DSMEM
     int skip_epi; // timing experiments only (HK_GEMM_DEBUG_SKIP_EPI): no output stores
+    int tfirst = 0;  // grid.x = token tiles, grid.y = weight tiles
     unsigned long long* trace;  // debug (HK_GEMM_TRACE): [first CTA start, first wait done, ~last end,
                                 //  ~last main-loop end] (atomicMin)
 };
@@ -69,8 +70,12 @@ __global__ void __launch_bounds__(128, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM;
-    const int n0 = blockIdx.y * BN;
+    // token-tile-fastest grids (p.tfirst, several token tiles): the CTAs that read
+    // one weight tile are launched together, so L2 serves it to all but the first
+    const int mtile = p.tfirst ? static_cast<int>(blockIdx.y) : static_cast<int>(blockIdx.x);
+    const int ntile = p.tfirst ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.y);
+    const int m0 = mtile * BM;
+    const int n0 = ntile * BN;
     const int kb0 = blockIdx.z * p.kb_per_split;
     const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
     const int nkb = kb1 - kb0;
@@ -235,8 +240,8 @@ __global__ void __launch_bounds__(128, 1)
         const int nt = min(BN, p.T - n0);
         for (int idx = threadIdx.x; idx < 64 * nt; idx += blockDim.x) {
             const int r = idx & 63, c = idx >> 6;
-            const int f = blockIdx.x * 64 + r;  // output feature
-            if (blockIdx.x * BM + r < p.N) {
+            const int f = mtile * 64 + r;  // output feature
+            if (mtile * BM + r < p.N) {
                 const float g = xs[r * (BN + 1) + c], u = xs[(r + 64) * (BN + 1) + c];
                 static_cast<bf16*>(p.out)[static_cast<size_t>(n0 + c) * p.ldo + f] =
                     f2bf(__fdividef(g, 1.0f + __expf(-g)) * u);
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(128, 1)
                 if (o.x > b.x) b = o;  // earlier warps hold lower rows: keep them on ties
             }
             const int n = n0 + c;
-            if (n < p.T) reinterpret_cast<float2*>(p.out)[static_cast<size_t>(blockIdx.x) * p.T + n] = b;
+            if (n < p.T) reinterpret_cast<float2*>(p.out)[static_cast<size_t>(mtile) * p.T + n] = b;
         }
     }
     if (p.epi < kEpiSwiGLU && !p.cluster && !p.skip_epi) {
@@ -593,7 +598,9 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
     p.trace = gemm_trace_slot(N, K, T, splits, mt * nt * splits);
     const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
     const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
-    dim3 grid(mt, nt, splits);
+    static const bool wfirst = std::getenv("HK_GEMM_WEIGHT_TILE_FIRST") != nullptr;  // A/B: the old grid order
+    p.tfirst = nt > 1 && !wfirst && !cluster ? 1 : 0;
+    dim3 grid = p.tfirst ? dim3(nt, mt, splits) : dim3(mt, nt, splits);
     switch (BN) {
         case 16: launch_tc<16, 4>(tw, tx, p, grid, st); break;
         case 32: launch_tc<32, 4>(tw, tx, p, grid, st); break;
