@@ -443,6 +443,155 @@ CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t rows, uint64_t cols, ui
 
 namespace {
 
+// ---------------------------------------------------------------------------
+// Prefill gate/up with the SwiGLU epilogue, persistent: one CTA per SM walks
+// its tiles (token tiles fastest) with TWO TMEM accumulators, so the epilogue
+// of tile i (TMEM -> registers -> silu(gate) * up -> bf16 stores) runs while
+// the MMAs of tile i + 1 stream (the one-tile-per-CTA kernel left the tensor
+// pipe idle during every epilogue: 43-50 % tensor-pipe activity at T = 2048).
+//   warp 0 TMA, warp 1 MMA, warps 2-5 epilogue (warp w reads TMEM lanes
+//   32 (w % 4) .. +31: quarters 0-1 are gate rows, 2-3 the matching up rows).
+//   smem: STAGES x (A 128 x 64 | B 256 x 64) | up exchange [64][33] fp32 |
+//         output block [32 tokens][64 features] bf16 | barriers
+constexpr int PK_BN = 256, PK_STAGES = 3, PK_EC = 32;  // epilogue column chunk (tokens)
+constexpr size_t pk_smem_bytes() {
+    return 1024 + PK_STAGES * (BM * BK * 2 + PK_BN * BK * 2) + 64 * (PK_EC + 1) * 4 + PK_EC * 64 * 2 +
+           (2 * PK_STAGES + 4) * 8 + 16;
+}
+
+__global__ void __launch_bounds__(192, 1)
+    gemm_swiglu_pk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int A_BYTES = BM * BK * 2, B_BYTES = PK_BN * BK * 2;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + PK_STAGES * A_BYTES;
+    float* xup = reinterpret_cast<float*>(sB + PK_STAGES * B_BYTES);   // [64][PK_EC + 1]
+    bf16* ob = reinterpret_cast<bf16*>(xup + 64 * (PK_EC + 1));          // [PK_EC][64]
+    uint64_t* full = reinterpret_cast<uint64_t*>(ob + PK_EC * 64);
+    uint64_t* empty = full + PK_STAGES;
+    uint64_t* acc_full = empty + PK_STAGES;   // [2]
+    uint64_t* acc_empty = acc_full + 2;       // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mt = (p.N + BM - 1) / BM, nt = (p.T + PK_BN - 1) / PK_BN;
+    const int tiles = mt * nt, nkb = p.kb_total;
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&tmW);
+        tma_prefetch_desc(&tmX);
+        for (int st = 0; st < PK_STAGES; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_w = policy_evict_first();
+            const uint64_t pol_x = policy_evict_last();
+            pdl_wait();
+            int g = 0;  // k-blocks issued so far by this CTA (stage ring position)
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = (t / nt) * BM, n0 = (t % nt) * PK_BN;
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int st = g % PK_STAGES;
+                    if (g >= PK_STAGES) mbar_wait(&empty[st], ((g / PK_STAGES) - 1) & 1);
+                    mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
+                    tma_load_2d_hint(sA + st * A_BYTES, &tmW, &full[st], kb * BK, m0, pol_w);
+                    tma_load_2d_hint(sB + st * B_BYTES, &tmX, &full[st], kb * BK, n0, pol_x);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        pdl_wait();
+        constexpr uint32_t idesc = umma_idesc_bf16(BM, PK_BN);
+        int g = 0, i = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+            const int b = i & 1;
+            if (i >= 2) mbar_wait(&acc_empty[b], ((i >> 1) - 1) & 1);
+            tc_fence_after();
+            for (int kb = 0; kb < nkb; ++kb, ++g) {
+                const int st = g % PK_STAGES;
+                mbar_wait(&full[st], (g / PK_STAGES) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t a_base = smem_u32(sA + st * A_BYTES);
+                    const uint32_t b_base = smem_u32(sB + st * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        umma_bf16(tmem + b * PK_BN, umma_desc_sw128(a_base + k * 32), umma_desc_sw128(b_base + k * 32), idesc,
+                                  (kb | k) != 0 ? 1u : 0u);
+                    umma_commit(&empty[st]);
+                    if (kb == nkb - 1) umma_commit(&acc_full[b]);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ---- epilogue warps: 128 threads, thread = TMEM lane (weight row of the tile)
+        pdl_wait();
+        const int q = warp & 3;  // lane quarter this warp may read
+        const int row = q * 32 + lane;
+        const int et = threadIdx.x - 64;  // 0..127
+        int i = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+            const int b = i & 1;
+            const int mtile = t / nt, n0 = (t % nt) * PK_BN;
+            mbar_wait(&acc_full[b], (i >> 1) & 1);
+            tc_fence_after();
+            for (int c0 = 0; c0 < PK_BN; c0 += PK_EC) {
+                float v[PK_EC];
+                tmem_ld32(tmem + b * PK_BN + c0 + (static_cast<uint32_t>(q * 32) << 16), v);
+                if (c0 + PK_EC == PK_BN) {  // the whole accumulator is in registers: free it
+                    tc_fence_before();
+                    mbar_arrive(&acc_empty[b]);
+                }
+                if (row >= 64) {
+#pragma unroll
+                    for (int j = 0; j < PK_EC; ++j) xup[(row - 64) * (PK_EC + 1) + j] = v[j];
+                }
+                named_bar(1, 128);
+                if (row < 64) {
+#pragma unroll
+                    for (int j = 0; j < PK_EC; ++j) {
+                        const float g = v[j], u = xup[row * (PK_EC + 1) + j];
+                        ob[j * 64 + row] = f2bf(__fdividef(g, 1.0f + __expf(-g)) * u);
+                    }
+                }
+                named_bar(1, 128);
+                // [PK_EC tokens][64 features]: 128-byte rows, 16 bytes per thread x 2
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int idx = et + k * 128, j = idx >> 3, c8 = (idx & 7) * 8;
+                    const int n = n0 + c0 + j, f = mtile * 64 + c8;
+                    if (n < p.T && f < p.N / 2)
+                        *reinterpret_cast<uint4*>(static_cast<bf16*>(p.out) + static_cast<size_t>(n) * p.ldo + f) =
+                            *reinterpret_cast<const uint4*>(ob + j * 64 + c8);
+                }
+                named_bar(1, 128);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 template <int BN, int STAGES>
 constexpr size_t smem_bytes() {
     return 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 1) * 8 + 16;
@@ -598,6 +747,21 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
     p.trace = gemm_trace_slot(N, K, T, splits, mt * nt * splits);
     const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
     const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
+    static const bool pk_off = std::getenv("HK_GEMM_SWIGLU_PERSIST") && std::atoi(std::getenv("HK_GEMM_SWIGLU_PERSIST")) == 0;
+    if (epi == kEpiSwiGLU && BN == 256 && !pk_off && N % BM == 0 && !p.skip_epi) {
+        // prefill gate/up: persistent tiles, epilogue under the next tile's MMAs
+        static bool configured = false;
+        constexpr size_t sm = pk_smem_bytes();
+        if (!configured) {
+            HK_CUDA(cudaFuncSetAttribute(gemm_swiglu_pk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sm)));
+            configured = true;
+        }
+        const CUtensorMap txp = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), PK_BN);
+        launch_pdl(gemm_swiglu_pk_kernel, dim3(std::min(mt * nt, g_num_sms)), dim3(192), sm, st, tw, txp, p);
+        HK_LAUNCHED(1);
+        return 1;
+    }
     static const bool wfirst = std::getenv("HK_GEMM_WEIGHT_TILE_FIRST") != nullptr;  // A/B: the old grid order
     p.tfirst = nt > 1 && !wfirst && !cluster ? 1 : 0;
     dim3 grid = p.tfirst ? dim3(nt, mt, splits) : dim3(mt, nt, splits);

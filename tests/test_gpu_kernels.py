@@ -65,10 +65,12 @@ def test_gemm_splitk_bias_and_residual(splits):
     assert (resid - (ref + 1)).abs().max().item() / scale < 1e-4
 
 
-@pytest.mark.parametrize("T", [1, 64, 300])
-def test_gemm_swiglu_epilogue(T):
+@pytest.mark.parametrize("T,F,K", [(1, 512, 256), (64, 512, 256), (300, 512, 256), (2085, 2048, 1024)])
+def test_gemm_swiglu_epilogue(T, F, K):
+    """Decode (T <= 128) and prefill tiles; (2085, 2048, 1024): 32 weight tiles x 9
+    token tiles (the last ragged) = 288 tiles over the persistent prefill kernel's
+    148 CTAs — two TMEM accumulators in turn, the stage ring wrapping across tiles."""
     lib = _lib.load()
-    F, K = 512, 256
     g = torch.Generator(device="cuda").manual_seed(T)
     Wg = (torch.rand(F, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) * 0.1
     Wu = (torch.rand(F, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) * 0.1
