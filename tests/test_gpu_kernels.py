@@ -24,6 +24,7 @@ def _ptr(t):
 GEMM_SHAPES = [
     (128, 64, 1), (256, 128, 16), (512, 256, 33), (384, 192, 64), (256, 512, 100), (1024, 512, 300),
     (6144, 4096, 64), (4096, 4096, 64), (4096, 14336, 64), (28672, 4096, 64), (6144, 4096, 1024),
+    (4096, 1024, 2085),
 ]
 
 
@@ -44,6 +45,13 @@ def test_gemm_tcgen05_matches_torch(N, K, T):
     torch.cuda.synchronize()
     errb = (outb.float() - ref).abs().max().item() / ref.abs().max().item()
     assert errb < 1e-2, errb
+    # the engine's split-K "partials" epilogue (prefill: one split, persistent tiles)
+    part = torch.zeros(T, N, device="cuda", dtype=torch.float32)
+    sp = lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(part), N, K, T, 3, None, 1, None)
+    assert sp == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    errp = (part - ref).abs().max().item() / ref.abs().max().item()
+    assert errp < 1e-4, errp
 
 
 @pytest.mark.parametrize("splits", [1, 2, 3, 7])
