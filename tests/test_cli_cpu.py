@@ -165,3 +165,33 @@ def test_cli_usage_errors(tmp_path, native):
     p = subprocess.run([str(BIN_), "run", "--workflow", str(tmp_path / "missing.json"), "--inputs", "b",
                         "--profile", "c"], capture_output=True, text=True)
     assert p.returncode == 1 and "error" in p.stderr
+
+
+BAD = {
+    "bad_slot": (lambda wf: wf["nodes"].append({"id": 99, "kind": "format", "args": {"template": "x {a}"}})),
+    "dup_id": (lambda wf: wf["nodes"].append(dict(wf["nodes"][0]))),
+    "missing_edge_src": (lambda wf: wf.setdefault("edges", []).append({"from": 1234, "to": 0, "slot": 0})),
+    "bad_kind": (lambda wf: wf["nodes"].append({"id": 98, "kind": "tensor", "args": {}})),
+    "bad_role": (lambda wf: wf["nodes"].append({"id": 97, "kind": "llm", "args": {
+        "messages": [{"role": "robot", "parts": [{"text": "hi"}]}]}})),
+    "output_not_output": (lambda wf: wf["outputs"].append(0)),
+}
+
+
+@needs_ref
+@pytest.mark.parametrize("name", sorted(BAD))
+def test_native_cli_rejects_bad_workflows_like_reference(tmp_path, name):
+    """Malformed workflows: the native reader fails with the reference's message."""
+    from oracle import refpy
+    wf, inputs, prof, flags = CASES["c1"]()
+    wf = json.loads(json.dumps(wf))
+    BAD[name](wf)
+    with pytest.raises(RuntimeError) as ref_err:
+        refpy.cli_run(wf, inputs, prof, dict(flags, trace=True))
+    for f, doc in (("wf", wf), ("in", inputs), ("prof", prof)):
+        (tmp_path / f"{f}.json").write_text(json.dumps(doc))
+    p = subprocess.run([str(NATIVE), "run", "--workflow", str(tmp_path / "wf.json"), "--inputs",
+                        str(tmp_path / "in.json"), "--profile", str(tmp_path / "prof.json")],
+                       capture_output=True, text=True)
+    assert p.returncode == 1
+    assert p.stderr.strip() == "error: " + str(ref_err.value), (p.stderr, str(ref_err.value))
