@@ -53,6 +53,113 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// ---- epilogues shared by the one-CTA and the CTA-pair kernels: this CTA's
+// 128 weight rows (TMEM lanes) x BN token columns, after the accumulator is final.
+
+// SwiGLU: W rows interleaved per 128-row tile as [64 gate | 64 up]; bf16 out [T][N/2]
+template <int BN>
+__device__ __forceinline__ void epi_swiglu(const GemmParams& p, uint32_t tmem, uint8_t* smem, int warp, int lane,
+                                           int mtile, int n0) {
+    const int row = warp * 32 + lane;
+    // TMEM lanes 0-63 hold gate rows, 64-127 the matching up rows (a warp
+    // may only read lanes 32w..32w+31): every warp parks its rows in smem,
+    // then all 128 threads produce silu(gate) * up with coalesced stores.
+    float* xs = reinterpret_cast<float*>(smem);  // [128][BN + 1], pipeline buffers are free now
+    if constexpr (BN >= 32) {
+        // 32-column TMEM loads: a quarter of the load/wait round trips of x8
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+            float v[32];
+            tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) xs[row * (BN + 1) + c + j] = v[j];
+        }
+    } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 8) {
+            float v[8];
+            tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) xs[row * (BN + 1) + c + j] = v[j];
+        }
+    }
+    __syncthreads();
+    const int nt = min(BN, p.T - n0);
+    for (int idx = threadIdx.x; idx < 64 * nt; idx += blockDim.x) {
+        const int r = idx & 63, c = idx >> 6;
+        const int f = mtile * 64 + r;  // output feature
+        if (mtile * BM + r < p.N) {
+            const float g = xs[r * (BN + 1) + c], u = xs[(r + 64) * (BN + 1) + c];
+            static_cast<bf16*>(p.out)[static_cast<size_t>(n0 + c) * p.ldo + f] =
+                f2bf(__fdividef(g, 1.0f + __expf(-g)) * u);
+        }
+    }
+}
+
+// fp32 rows (kEpiPartial / StoreF32 / StoreBf16 / AddF32)
+template <int BN>
+__device__ __forceinline__ void epi_rows(const GemmParams& p, uint32_t tmem, uint8_t* smem, int warp, int lane, int m0,
+                                         int n0, int zsplit) {
+    const int row = warp * 32 + lane;
+    const int m = m0 + row;
+    const bool m_ok = m < p.N;
+    // Stage the fp32 tile through shared memory as [token][feature] (the
+    // pipeline buffers are free now), then every warp writes whole rows of
+    // 128 consecutive features: 16-byte stores, 512 contiguous bytes per
+    // warp instruction, in the [token][ldo] / [split][token][N] layouts.
+    constexpr int SO = BM + 4;  // padded row: conflict-free column writes and float4 row reads
+    float* so = reinterpret_cast<float*>(smem);
+    const float bias = (p.bias && m_ok && p.epi != kEpiPartial) ? bf2f(p.bias[m]) : 0.f;
+#pragma unroll
+    for (int c = 0; c < BN; c += 32) {
+        if constexpr (BN >= 32) {
+            float v[32];
+            tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) so[(c + j) * SO + row] = v[j] + bias;
+        }
+    }
+    if constexpr (BN < 32) {
+#pragma unroll
+        for (int c = 0; c < BN; c += 8) {
+            float v[8];
+            tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) so[(c + j) * SO + row] = v[j] + bias;
+        }
+    }
+    __syncthreads();
+    const int rows = min(BN, p.T - n0);
+    const bool full_m = m0 + BM <= p.N;
+    for (int r = warp; r < rows; r += 4) {
+        const int n = n0 + r;
+        const float4 v = reinterpret_cast<const float4*>(so + r * SO)[lane];
+        const int mm = m0 + lane * 4;
+        if (p.epi == kEpiPartial) {
+            float* dst = p.partial + (static_cast<size_t>(zsplit) * p.T + n) * p.N + mm;
+            if (full_m) {
+                *reinterpret_cast<float4*>(dst) = v;
+            } else {
+                const float e[4] = {v.x, v.y, v.z, v.w};
+                for (int q = 0; q < 4; ++q)
+                    if (mm + q < p.N) dst[q] = e[q];
+            }
+        } else {
+            const float e[4] = {v.x, v.y, v.z, v.w};
+            for (int q = 0; q < 4; ++q) {
+                if (mm + q >= p.N) break;
+                const size_t o = static_cast<size_t>(n) * p.ldo + mm + q;
+                if (p.epi == kEpiStoreBf16)
+                    static_cast<bf16*>(p.out)[o] = f2bf(e[q]);
+                else if (p.epi == kEpiAddF32)
+                    static_cast<float*>(p.out)[o] += e[q];
+                else
+                    static_cast<float*>(p.out)[o] = e[q];
+            }
+        }
+    }
+}
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(128, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p) {
@@ -214,39 +321,7 @@ __global__ void __launch_bounds__(128, 1)
         }
         cluster_sync_all();  // peers keep their smem until every rank has read it
     } else if (p.epi == kEpiSwiGLU) {
-        // TMEM lanes 0-63 hold gate rows, 64-127 the matching up rows (a warp
-        // may only read lanes 32w..32w+31): every warp parks its rows in smem,
-        // then all 128 threads produce silu(gate) * up with coalesced stores.
-        float* xs = reinterpret_cast<float*>(smem);  // [128][BN + 1], pipeline buffers are free now
-        if constexpr (BN >= 32) {
-            // 32-column TMEM loads: a quarter of the load/wait round trips of x8
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                float v[32];
-                tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) xs[row * (BN + 1) + c + j] = v[j];
-            }
-        } else {
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 8) {
-                float v[8];
-                tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) xs[row * (BN + 1) + c + j] = v[j];
-            }
-        }
-        __syncthreads();
-        const int nt = min(BN, p.T - n0);
-        for (int idx = threadIdx.x; idx < 64 * nt; idx += blockDim.x) {
-            const int r = idx & 63, c = idx >> 6;
-            const int f = mtile * 64 + r;  // output feature
-            if (mtile * BM + r < p.N) {
-                const float g = xs[r * (BN + 1) + c], u = xs[(r + 64) * (BN + 1) + c];
-                static_cast<bf16*>(p.out)[static_cast<size_t>(n0 + c) * p.ldo + f] =
-                    f2bf(__fdividef(g, 1.0f + __expf(-g)) * u);
-            }
-        }
+        epi_swiglu<BN>(p, tmem, smem, warp, lane, mtile, n0);
     } else if (p.epi == kEpiArgmax) {
         float2* red = reinterpret_cast<float2*>(smem);  // [4][BN] (value, index)
 #pragma unroll 1
@@ -281,66 +356,133 @@ __global__ void __launch_bounds__(128, 1)
         }
     }
     if (p.epi < kEpiSwiGLU && !p.cluster && !p.skip_epi) {
-        // Stage the fp32 tile through shared memory as [token][feature] (the
-        // pipeline buffers are free now), then every warp writes whole rows of
-        // 128 consecutive features: 16-byte stores, 512 contiguous bytes per
-        // warp instruction, in the [token][ldo] / [split][token][N] layouts.
-        constexpr int SO = BM + 4;  // padded row: conflict-free column writes and float4 row reads
-        float* so = reinterpret_cast<float*>(smem);
-        const float bias = (p.bias && m_ok && p.epi != kEpiPartial) ? bf2f(p.bias[m]) : 0.f;
-#pragma unroll
-        for (int c = 0; c < BN; c += 32) {
-            if constexpr (BN >= 32) {
-                float v[32];
-                tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) so[(c + j) * SO + row] = v[j] + bias;
-            }
-        }
-        if constexpr (BN < 32) {
-#pragma unroll
-            for (int c = 0; c < BN; c += 8) {
-                float v[8];
-                tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) so[(c + j) * SO + row] = v[j] + bias;
-            }
-        }
-        __syncthreads();
-        const int rows = min(BN, p.T - n0);
-        const bool full_m = m0 + BM <= p.N;
-        for (int r = warp; r < rows; r += 4) {
-            const int n = n0 + r;
-            const float4 v = reinterpret_cast<const float4*>(so + r * SO)[lane];
-            const int mm = m0 + lane * 4;
-            if (p.epi == kEpiPartial) {
-                float* dst = p.partial + (static_cast<size_t>(blockIdx.z) * p.T + n) * p.N + mm;
-                if (full_m) {
-                    *reinterpret_cast<float4*>(dst) = v;
-                } else {
-                    const float e[4] = {v.x, v.y, v.z, v.w};
-                    for (int q = 0; q < 4; ++q)
-                        if (mm + q < p.N) dst[q] = e[q];
-                }
-            } else {
-                const float e[4] = {v.x, v.y, v.z, v.w};
-                for (int q = 0; q < 4; ++q) {
-                    if (mm + q >= p.N) break;
-                    const size_t o = static_cast<size_t>(n) * p.ldo + mm + q;
-                    if (p.epi == kEpiStoreBf16)
-                        static_cast<bf16*>(p.out)[o] = f2bf(e[q]);
-                    else if (p.epi == kEpiAddF32)
-                        static_cast<float*>(p.out)[o] += e[q];
-                    else
-                        static_cast<float*>(p.out)[o] = e[q];
-                }
-            }
-        }
+        epi_rows<BN>(p, tmem, smem, warp, lane, m0, n0, static_cast<int>(blockIdx.z));
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 2) tmem_dealloc(tmem, TMEM_COLS);
     if (p.trace && threadIdx.x == 0) atomicMin(&p.trace[3], ~gtimer());  // last CTA to finish its main loop + stores
+    if (p.trace && threadIdx.x == 0) atomicMin(&p.trace[2], ~gtimer());
+}
+
+// ---------------------------------------------------------------------------
+// Prefill GEMMs on CTA pairs (tcgen05 cta_group::2): a cluster of two CTAs on
+// one TPC computes a 256-weight-row x 256-token tile. Each CTA stages its own
+// 128 weight rows and HALF of the token rows (32 KB per k-block instead of
+// 48 KB), rank 0 issues M=256 MMAs that read both CTAs' shared memory, and
+// each CTA's TMEM holds its 128 rows x 256 tokens for the usual epilogue.
+// Halving the operand bytes per MMA keeps shared-memory bandwidth (TMA writes
+// + MMA reads) under the per-SM limit that caps the one-CTA M=128 x N=256 tile.
+constexpr int C2_BN = 256;  // tokens per pair tile
+template <int STAGES>
+constexpr size_t smem2_bytes() {
+    return 1024 + STAGES * (BM * BK * 2 + (C2_BN / 2) * BK * 2) + (2 * STAGES + 1) * 8 + 16;
+}
+
+template <int STAGES>
+__global__ void __launch_bounds__(128, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int A_BYTES = BM * BK * 2;           // this CTA's 128 weight rows
+    constexpr int B_BYTES = (C2_BN / 2) * BK * 2;  // this CTA's 128 of the tile's 256 tokens
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* done = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    // cluster (2, 1, 1): grid.x = 2 x token tiles (pair member fastest), grid.y = weight-tile
+    // pairs — consecutive clusters walk the token tiles of one weight pair (L2 reuse)
+    const uint32_t rank = cluster_ctarank();
+    const int ntile = static_cast<int>(blockIdx.x) >> 1;
+    const int mtile = static_cast<int>(blockIdx.y) * 2 + static_cast<int>(rank);
+    const int m0 = mtile * BM;
+    const int n0 = ntile * C2_BN;
+    const int kb0 = blockIdx.z * p.kb_per_split;
+    const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
+    const int nkb = kb1 - kb0;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmW);
+        tma_prefetch_desc(&tmX);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc_cg2(tmem_slot, C2_BN);
+    tc_fence_before();
+    cluster_sync_all();  // both CTAs' barriers initialised before any peer TMA completes on them
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    pdl_trigger();
+    if (p.trace && threadIdx.x == 0) atomicMin(&p.trace[0], gtimer());
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_w = policy_evict_first();
+            const uint64_t pol_x = policy_evict_last();
+            // both CTAs' loads complete on rank 0's full barriers; rank 0 expects the pair's bytes
+            const uint32_t full0 = mapa_shared(smem_u32(full), 0);
+            const int nb = n0 + static_cast<int>(rank) * (C2_BN / 2);
+            const int pre = min(STAGES, nkb);
+            for (int i = 0; i < pre; ++i) {
+                if (rank == 0) mbar_expect_tx(&full[i], 2 * (A_BYTES + B_BYTES));
+                tma_load_2d_cg2(sA + i * A_BYTES, &tmW, full0 + i * 8, (kb0 + i) * BK, m0, pol_w);
+            }
+            pdl_wait();
+            if (p.trace && rank == 0) atomicMin(&p.trace[1], gtimer());
+            for (int i = 0; i < pre; ++i)
+                tma_load_2d_cg2(sB + i * B_BYTES, &tmX, full0 + i * 8, (kb0 + i) * BK, nb, pol_x);
+            for (int i = pre; i < nkb; ++i) {
+                const int s = i % STAGES;
+                mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+                if (rank == 0) mbar_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
+                tma_load_2d_cg2(sA + s * A_BYTES, &tmW, full0 + s * 8, (kb0 + i) * BK, m0, pol_w);
+                tma_load_2d_cg2(sB + s * B_BYTES, &tmX, full0 + s * 8, (kb0 + i) * BK, nb, pol_x);
+            }
+        }
+    } else if (warp == 1 && rank == 0) {
+        constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, C2_BN);
+        for (int i = 0; i < nkb; ++i) {
+            const int s = i % STAGES;
+            mbar_wait(&full[s], (i / STAGES) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t a_base = smem_u32(sA + s * A_BYTES);
+                const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                    umma_bf16_cg2(tmem, umma_desc_sw128(a_base + k * 32), umma_desc_sw128(b_base + k * 32), idesc,
+                                  (i | k) != 0 ? 1u : 0u);
+                umma_commit_cg2_mc(&empty[s], 3);  // frees stage s in both CTAs
+                if (i == nkb - 1) umma_commit_cg2_mc(done, 3);
+            }
+            __syncwarp();
+        }
+    }
+
+    mbar_wait(done, 0);
+    __syncwarp();
+    tc_fence_after();
+    pdl_wait();
+    if (!p.skip_epi) {
+        if (p.epi == kEpiSwiGLU)
+            epi_swiglu<C2_BN>(p, tmem, smem, warp, lane, mtile, n0);
+        else
+            epi_rows<C2_BN>(p, tmem, smem, warp, lane, m0, n0, static_cast<int>(blockIdx.z));
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // the pair deallocates together
+    if (warp == 2) tmem_dealloc_cg2(tmem, C2_BN);
+    if (p.trace && threadIdx.x == 0) atomicMin(&p.trace[3], ~gtimer());
     if (p.trace && threadIdx.x == 0) atomicMin(&p.trace[2], ~gtimer());
 }
 
@@ -592,6 +734,156 @@ __global__ void __launch_bounds__(192, 1)
     }
 }
 
+// The persistent gate/up kernel on CTA pairs: a cluster of two CTAs walks
+// 256-weight-row x 256-token pair tiles (token tiles fastest); per k-block each
+// CTA stages its 128 weight rows and half the tokens, rank 0 issues the M=256
+// MMAs into the two accumulators, and both CTAs' epilogue warps free an
+// accumulator on rank 0's barrier. Same SwiGLU epilogue as above.
+constexpr int PK2_STAGES = 6;
+constexpr size_t pk2_smem_bytes() {
+    return 1024 + PK2_STAGES * (BM * BK * 2 + (PK_BN / 2) * BK * 2) + 64 * (PK_EC + 1) * 4 + PK_EC * 64 * 2 +
+           (2 * PK2_STAGES + 4) * 8 + 16;
+}
+
+__global__ void __launch_bounds__(192, 1)
+    gemm_swiglu_pk2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int A_BYTES = BM * BK * 2, B_BYTES = (PK_BN / 2) * BK * 2;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + PK2_STAGES * A_BYTES;
+    float* xup = reinterpret_cast<float*>(sB + PK2_STAGES * B_BYTES);  // [64][PK_EC + 1]
+    bf16* ob = reinterpret_cast<bf16*>(xup + 64 * (PK_EC + 1));         // [PK_EC][64]
+    uint64_t* full = reinterpret_cast<uint64_t*>(ob + PK_EC * 64);
+    uint64_t* empty = full + PK2_STAGES;
+    uint64_t* acc_full = empty + PK2_STAGES;  // [2]
+    uint64_t* acc_empty = acc_full + 2;       // [2] (rank 0's: 256 arrivals, both CTAs' epilogues)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int pair = static_cast<int>(blockIdx.x) >> 1, n_pairs = static_cast<int>(gridDim.x) >> 1;
+    const int mpt = (p.N + BM - 1) / BM / 2, nt = (p.T + PK_BN - 1) / PK_BN;  // weight-tile pairs, token tiles
+    const int tiles = mpt * nt, nkb = p.kb_total;
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&tmW);
+        tma_prefetch_desc(&tmX);
+        for (int st = 0; st < PK2_STAGES; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 256);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_cg2(tmem_slot, 512);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_w = policy_evict_first();
+            const uint64_t pol_x = policy_evict_last();
+            const uint32_t full0 = mapa_shared(smem_u32(full), 0);
+            pdl_wait();
+            int g = 0;
+            for (int t = pair; t < tiles; t += n_pairs) {
+                const int m0 = ((t / nt) * 2 + static_cast<int>(rank)) * BM;
+                const int nb = (t % nt) * PK_BN + static_cast<int>(rank) * (PK_BN / 2);
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int st = g % PK2_STAGES;
+                    if (g >= PK2_STAGES) mbar_wait(&empty[st], ((g / PK2_STAGES) - 1) & 1);
+                    if (rank == 0) mbar_expect_tx(&full[st], 2 * (A_BYTES + B_BYTES));
+                    tma_load_2d_cg2(sA + st * A_BYTES, &tmW, full0 + st * 8, kb * BK, m0, pol_w);
+                    tma_load_2d_cg2(sB + st * B_BYTES, &tmX, full0 + st * 8, kb * BK, nb, pol_x);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0) {
+            pdl_wait();
+            constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, PK_BN);
+            int g = 0, i = 0;
+            for (int t = pair; t < tiles; t += n_pairs, ++i) {
+                const int b = i & 1;
+                if (i >= 2) mbar_wait(&acc_empty[b], ((i >> 1) - 1) & 1);
+                tc_fence_after();
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int st = g % PK2_STAGES;
+                    mbar_wait(&full[st], (g / PK2_STAGES) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t a_base = smem_u32(sA + st * A_BYTES);
+                        const uint32_t b_base = smem_u32(sB + st * B_BYTES);
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k)
+                            umma_bf16_cg2(tmem + b * PK_BN, umma_desc_sw128(a_base + k * 32),
+                                          umma_desc_sw128(b_base + k * 32), idesc, (kb | k) != 0 ? 1u : 0u);
+                        umma_commit_cg2_mc(&empty[st], 3);
+                        if (kb == nkb - 1) umma_commit_cg2_mc(&acc_full[b], 3);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else {
+        pdl_wait();
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int et = threadIdx.x - 64;
+        const uint32_t acc_empty0 = mapa_shared(smem_u32(acc_empty), 0);
+        int i = 0;
+        for (int t = pair; t < tiles; t += n_pairs, ++i) {
+            const int b = i & 1;
+            const int mtile = (t / nt) * 2 + static_cast<int>(rank), n0 = (t % nt) * PK_BN;
+            mbar_wait(&acc_full[b], (i >> 1) & 1);
+            tc_fence_after();
+            for (int c0 = 0; c0 < PK_BN; c0 += PK_EC) {
+                float v[PK_EC];
+                tmem_ld32(tmem + b * PK_BN + c0 + (static_cast<uint32_t>(q * 32) << 16), v);
+                if (c0 + PK_EC == PK_BN) {
+                    tc_fence_before();
+                    mbar_arrive_cluster(acc_empty0 + b * 8);
+                }
+                if (row >= 64) {
+#pragma unroll
+                    for (int j = 0; j < PK_EC; ++j) xup[(row - 64) * (PK_EC + 1) + j] = v[j];
+                }
+                named_bar(1, 128);
+                if (row < 64) {
+#pragma unroll
+                    for (int j = 0; j < PK_EC; ++j) {
+                        const float g = v[j], u = xup[row * (PK_EC + 1) + j];
+                        ob[j * 64 + row] = f2bf(__fdividef(g, 1.0f + __expf(-g)) * u);
+                    }
+                }
+                named_bar(1, 128);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int idx = et + k * 128, j = idx >> 3, c8 = (idx & 7) * 8;
+                    const int n = n0 + c0 + j, f = mtile * 64 + c8;
+                    if (n < p.T && f < p.N / 2)
+                        *reinterpret_cast<uint4*>(static_cast<bf16*>(p.out) + static_cast<size_t>(n) * p.ldo + f) =
+                            *reinterpret_cast<const uint4*>(ob + j * 64 + c8);
+                }
+                named_bar(1, 128);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_cg2(tmem, 512);
+    }
+}
+
 template <int BN, int STAGES>
 constexpr size_t smem_bytes() {
     return 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 1) * 8 + 16;
@@ -624,6 +916,33 @@ void launch_tc(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p
         cfg.numAttrs = 2;
     }
     HK_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES>, tw, tx, p));
+    HK_LAUNCHED(1);
+}
+
+template <int STAGES>
+void launch_tc2(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p, dim3 grid, cudaStream_t st) {
+    static bool configured = false;
+    constexpr size_t sm = smem2_bytes<STAGES>();
+    if (!configured) {
+        HK_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sm)));
+        configured = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    HK_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<STAGES>, tw, tx, p));
     HK_LAUNCHED(1);
 }
 
@@ -747,8 +1066,45 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
     p.trace = gemm_trace_slot(N, K, T, splits, mt * nt * splits);
     const CUtensorMap tw = make_map_2d(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), BM);
     const CUtensorMap tx = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), static_cast<uint32_t>(BN));
+    // prefill tiles (256 tokens) on CTA pairs: two weight tiles per cluster
+    // (HK_GEMM_CG2=0: one CTA per tile; HK_GEMM_CG2_SWIGLU=1: gate/up too, instead of the persistent kernel)
+    static const bool cg2_off = std::getenv("HK_GEMM_CG2") && std::atoi(std::getenv("HK_GEMM_CG2")) == 0;
+    static const bool cg2_swiglu = std::getenv("HK_GEMM_CG2_SWIGLU") && std::atoi(std::getenv("HK_GEMM_CG2_SWIGLU")) != 0;
+    const bool use_cg2 = BN == 256 && !cg2_off && !cluster && mt % 2 == 0 && epi != kEpiArgmax && !p.skip_epi &&
+                         (epi != kEpiSwiGLU || cg2_swiglu);
     static const bool pk_off = std::getenv("HK_GEMM_SWIGLU_PERSIST") && std::atoi(std::getenv("HK_GEMM_SWIGLU_PERSIST")) == 0;
-    if (epi == kEpiSwiGLU && BN == 256 && !pk_off && N % BM == 0 && !p.skip_epi) {
+    static const bool pk2_off = std::getenv("HK_GEMM_SWIGLU_PAIRS") && std::atoi(std::getenv("HK_GEMM_SWIGLU_PAIRS")) == 0;
+    if (epi == kEpiSwiGLU && BN == 256 && !pk_off && !pk2_off && !cg2_off && !use_cg2 && N % (2 * BM) == 0 &&
+        !p.skip_epi && g_num_sms >= 2) {
+        // prefill gate/up: persistent CTA pairs
+        static bool configured = false;
+        constexpr size_t sm = pk2_smem_bytes();
+        if (!configured) {
+            HK_CUDA(cudaFuncSetAttribute(gemm_swiglu_pk2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sm)));
+            configured = true;
+        }
+        const CUtensorMap txh = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), PK_BN / 2);
+        const int pairs = std::min((mt / 2) * nt, g_num_sms / 2);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * pairs);
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = 2;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        HK_CUDA(cudaLaunchKernelEx(&cfg, gemm_swiglu_pk2_kernel, tw, txh, p));
+        HK_LAUNCHED(1);
+        return 1;
+    }
+    if (epi == kEpiSwiGLU && BN == 256 && !pk_off && !use_cg2 && N % BM == 0 && !p.skip_epi) {
         // prefill gate/up: persistent tiles, epilogue under the next tile's MMAs
         static bool configured = false;
         constexpr size_t sm = pk_smem_bytes();
@@ -761,6 +1117,17 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
         launch_pdl(gemm_swiglu_pk_kernel, dim3(std::min(mt * nt, g_num_sms)), dim3(192), sm, st, tw, txp, p);
         HK_LAUNCHED(1);
         return 1;
+    }
+    if (use_cg2) {
+        const CUtensorMap txh = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), C2_BN / 2);
+        launch_tc2<6>(tw, txh, p, dim3(2 * nt, mt / 2, splits), st);
+        if (via_ws) {
+            const size_t total = static_cast<size_t>(T) * N;
+            const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 4096));
+            splitk_reduce_kernel<<<blocks, 256, 0, st>>>(workspace, splits, T, N, epi, out, ldo, bias);
+            HK_LAUNCHED(1);
+        }
+        return splits;
     }
     static const bool wfirst = std::getenv("HK_GEMM_WEIGHT_TILE_FIRST") != nullptr;  // A/B: the old grid order
     p.tfirst = nt > 1 && !wfirst && !cluster ? 1 : 0;

@@ -24,7 +24,7 @@ def _ptr(t):
 GEMM_SHAPES = [
     (128, 64, 1), (256, 128, 16), (512, 256, 33), (384, 192, 64), (256, 512, 100), (1024, 512, 300),
     (6144, 4096, 64), (4096, 4096, 64), (4096, 14336, 64), (28672, 4096, 64), (6144, 4096, 1024),
-    (4096, 1024, 2085),
+    (4096, 1024, 2085), (384, 192, 300), (2048, 512, 257),
 ]
 
 
@@ -52,6 +52,26 @@ def test_gemm_tcgen05_matches_torch(N, K, T):
     torch.cuda.synchronize()
     errp = (part - ref).abs().max().item() / ref.abs().max().item()
     assert errp < 1e-4, errp
+
+
+@pytest.mark.parametrize("splits,T", [(1, 600), (3, 600), (2, 1024)])
+def test_gemm_pair_tiles_splitk_partials(splits, T):
+    """Prefill tiles on CTA pairs (tcgen05 cta_group::2, 256 weight rows x 256
+    tokens per cluster): split-K fp32 partials [splits][T][N] sum to the
+    product; T = 600 leaves a ragged last token tile whose second half is
+    entirely out of bounds (TMA zero fill)."""
+    lib = _lib.load()
+    N, K = 1024, 1024
+    g = torch.Generator(device="cuda").manual_seed(splits * 1000 + T)
+    W = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) * (3.0 / K) ** 0.5
+    X = (torch.rand(T, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    ref = X.float() @ W.float().t()
+    part = torch.full((splits, T, N), float("nan"), device="cuda", dtype=torch.float32)
+    sp = lib.hkx_gemm_bf16(_ptr(W), _ptr(X), _ptr(part), N, K, T, 3, None, splits, None)
+    assert sp == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    err = (part.sum(0) - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-4, err
 
 
 @pytest.mark.parametrize("splits", [1, 2, 3, 7])

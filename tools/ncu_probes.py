@@ -29,6 +29,29 @@ if what == "prefill_gemm":
                                      N, K, T, epi, None, 0, None) == 0, _lib.last_error()
         torch.cuda.synchronize()
         print(f"{name}: N={N} K={K} T={T}: {2 * N * K * T / 1e12:.3f} TFLOP per launch")
+elif what == "prefill_gemm_time":
+    # CUDA-event timing of the same launches (20 back to back, inputs resident; not under a profiler)
+    T = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
+    peak = 1392.0
+    for name, N, K, epi in [("qkv", 6144, 4096, 3), ("o", 4096, 4096, 3), ("gate_up", 28672, 4096, 4),
+                            ("down", 4096, 14336, 3)]:
+        W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+        X = torch.randn(T, K, device="cuda").to(torch.bfloat16)
+        out = torch.zeros(T, N // 2 if epi == 4 else N, device="cuda", dtype=torch.bfloat16 if epi == 4 else torch.float32)
+        call = lambda: lib.hkx_gemm_bf16(C.c_void_p(W.data_ptr()), C.c_void_p(X.data_ptr()), C.c_void_p(out.data_ptr()),
+                                         N, K, T, epi, None, 0, None)
+        for _ in range(3):
+            assert call() == 0, _lib.last_error()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            call()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / 20 * 1e3
+        tf = 2 * N * K * T / us / 1e6
+        print(f"{name:8s} T={T}: {us:8.1f} us  {tf:7.1f} TFLOP/s  frac {tf / peak:.3f}")
 elif what == "pool":
     from paper_2603_16104_b200.engine import LLAMA3_8B, Engine, EngineConfig
     eng = Engine(LLAMA3_8B, EngineConfig(pages_per_worker=1024, max_calls=8, max_step_tokens=256, max_ctx_tokens=2048))
