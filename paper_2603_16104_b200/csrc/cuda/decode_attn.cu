@@ -147,6 +147,11 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float fmax3(float x, float y, float z) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(x), "f"(y), "f"(z));
+    return r;
+}
 template <int G>
 __device__ __forceinline__ void shared_phase(const CUtensorMap& tm_kv, const DecodeAttnArgs& a, uint8_t* sm) {
     uint8_t* sQ = sm;
@@ -676,13 +681,17 @@ __device__ __forceinline__ void shared2_phase(const CUtensorMap& tm_kv, const De
                 for (int e = 0; e < 128; ++e)
                     if (e >= nk) s[e] = -INFINITY;
             }
-            float mx8[8];
+            // the chunk loop is issue-bound: three-input max (FMNMX3) and packed
+            // fp32x2 FMA / add (FFMA2 / FADD2) halve those instruction counts
+            float m4[4] = {s[0], s[1], s[2], s[3]};
 #pragma unroll
-            for (int j = 0; j < 8; ++j) mx8[j] = s[j];
+            for (int j = 4; j < 124; j += 8) {
 #pragma unroll
-            for (int j = 8; j < 128; ++j) mx8[j & 7] = fmaxf(mx8[j & 7], s[j]);
-            float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+                for (int q = 0; q < 4; ++q) m4[q] = fmax3(m4[q], s[j + q], s[j + 4 + q]);
+            }
+            m4[0] = fmax3(m4[0], s[124], s[125]);
+            m4[1] = fmax3(m4[1], s[126], s[127]);
+            float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
             mx *= a.sl2;  // log2 domain
             if (tid == 0) cstamp(a, c, 6);
             // lazy rescale (exact: O and l always refer to m_run; p <= 2^8 between rescales)
@@ -694,15 +703,16 @@ __device__ __forceinline__ void shared2_phase(const CUtensorMap& tm_kv, const De
             }
             const float nm = -m_run;
             uint32_t pk[64];
-            float ls[4] = {0.f, 0.f, 0.f, 0.f};
+            const float2 sl2v = make_float2(a.sl2, a.sl2), nmv = make_float2(nm, nm);
+            float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
             for (int j = 0; j < 64; ++j) {
-                const float p0 = ex2(fmaf(s[2 * j], a.sl2, nm));
-                const float p1 = ex2(fmaf(s[2 * j + 1], a.sl2, nm));
-                ls[j & 3] += p0 + p1;
+                const float2 x = __ffma2_rn(make_float2(s[2 * j], s[2 * j + 1]), sl2v, nmv);
+                const float p0 = ex2(x.x), p1 = ex2(x.y);
+                ls2[j & 1] = __fadd2_rn(ls2[j & 1], make_float2(p0, p1));
                 pk[j] = pack2(p0, p1);
             }
-            l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+            l_run += (ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y);
             if (tid == 0) cstamp(a, c, 1);
             // s_full(c) implies PV(c - 1) completed: O may be rescaled now
             if (c > 0 && __any_sync(0xffffffffu, need)) {
