@@ -334,6 +334,47 @@ int hk_trie_apply(hk_engine* e, int worker, const hk_trie_op* ops, size_t n);
 int hk_trie_match(hk_engine* e, int worker, const uint64_t* tokens, const uint64_t* offsets, size_t n,
                   int32_t* matched_blocks, int32_t* node_path, int32_t* page_table, size_t stride);
 
+/* ---- step-level entry points: for a host that runs its own
+ * iteration loop (the reference's simulate() body, simulator.cpp:331-374) and
+ * owns the block tables. Every call is synchronous on the engine stream. */
+/* A call slot holds the call's last sampled token on the device (the next
+ * decode step's input) and its generated tokens. -1 + hk_last_error on failure. */
+int hk_slot_alloc(hk_engine* e, int worker);
+int hk_slot_free(hk_engine* e, int worker, int slot);
+/* One segment of a ragged step: a prefill chunk of `count` tokens at positions
+ * [start, start + count) with their vocab ids, or a decode step (ids == NULL,
+ * count == 1) whose input is the slot's last sampled token at position `start`.
+ * `pages` is the call's block table covering positions [0, start + count)
+ * (page p holds positions [16p, 16p + 16) of the call); the K/V of the
+ * segment's positions are written into it when write_kv != 0, earlier
+ * positions are read from it (shared prefix pages may appear in several
+ * calls' tables). */
+typedef struct hk_step_seg {
+    int32_t slot;          /* call slot; -1 for a prefill chunk that samples nothing */
+    int32_t start;
+    int32_t count;
+    int32_t sample;        /* greedy-sample the token after the segment's last position */
+    const uint32_t* ids;   /* count vocab ids, or NULL (decode) */
+    const int32_t* pages;
+    int32_t n_pages;
+    int32_t write_kv;
+} hk_step_seg;
+/* One ragged forward (prefill chunks + decode rows, the engine's K3/K4/K5 path;
+ * the reference's chunked prefill simulator.cpp:331-343 and decode step
+ * :347-374 of one worker and iteration). sampled[i] = the token sampled for
+ * segment i (-1 when it does not sample); logits (optional, [n][vocab] fp32)
+ * receives the vocab logits of every sampling segment's last position. */
+int hk_step(hk_engine* e, int worker, const hk_step_seg* segs, size_t n, int32_t* sampled, float* logits);
+/* Prefill a pin (static prefix, simulator.cpp:257-263) into `pages` without
+ * sampling: K/V of positions [0, n) land in pages[0 .. ceil(n / 16)). */
+int hk_pin_prefill(hk_engine* e, int worker, const uint32_t* ids, size_t n, const int32_t* pages, size_t n_pages);
+/* K6 page broadcast outside hk_simulate: role 1 gathers `pages` into a device
+ * buffer (n x hk_engine_page_bytes, hk_pool_gather layout) and calls fn with
+ * it (the caller broadcasts, e.g. ncclBroadcast); role 2 calls fn to fill the
+ * buffer, then scatters it into `pages`. */
+int hk_kv_broadcast(hk_engine* e, int worker, int role, const int32_t* pages, size_t n, hk_pin_exchange_fn fn,
+                    void* user);
+
 /* Stand-alone greedy generation of one prompt (vocab ids) through the paged
  * engine — prefill then n_new decode steps — used by model parity tests.
  * logits (optional) receives the vocab logits of each sampled position. */

@@ -52,6 +52,11 @@ class TrieOpC(C.Structure):
                 ("phash", C.c_uint64), ("key", u64p)]
 
 
+class StepSegC(C.Structure):
+    _fields_ = [("slot", C.c_int32), ("start", C.c_int32), ("count", C.c_int32), ("sample", C.c_int32),
+                ("ids", u32p), ("pages", i32p), ("n_pages", C.c_int32), ("write_kv", C.c_int32)]
+
+
 class WorkflowSpecC(C.Structure):
     _fields_ = [("workers", C.c_int32), ("capacities", u64p), ("n_capacities", C.c_size_t), ("scheduler", C.c_char_p),
                 ("seed", C.c_uint64), ("stochastic", C.c_int32), ("prune", C.c_int32), ("merge_duplicates", C.c_int32),
@@ -133,6 +138,11 @@ _SIGS = {
     "hk_trie_apply": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(TrieOpC), C.c_size_t]),
     "hk_trie_match": (C.c_int, [C.c_void_p, C.c_int, u64p, u64p, C.c_size_t, i32p, i32p, i32p, C.c_size_t]),
     "hk_generate": (C.c_int, [C.c_void_p, u32p, C.c_size_t, C.c_size_t, u32p, f32p]),
+    "hk_slot_alloc": (C.c_int, [C.c_void_p, C.c_int]),
+    "hk_slot_free": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "hk_step": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(StepSegC), C.c_size_t, i32p, f32p]),
+    "hk_pin_prefill": (C.c_int, [C.c_void_p, C.c_int, u32p, C.c_size_t, i32p, C.c_size_t]),
+    "hk_kv_broadcast": (C.c_int, [C.c_void_p, C.c_int, C.c_int, i32p, C.c_size_t, PinExchangeFn, C.c_void_p]),
     "hk_engine_kernel_ms": (C.c_double, [C.c_void_p, C.c_char_p, u64p, C.POINTER(C.c_double)]),
     "hk_engine_profile": (C.c_int, [C.c_void_p, C.c_int]),
     # include/helium_b200_kernels.h

@@ -173,6 +173,7 @@ struct hk_engine {
     std::map<std::vector<int64_t>, int> graph_seen;
     bool use_graphs = true;
     bool l2_prefetch_o = false;  // decode attention pulls the O-projection weights into L2 (opt-in)
+    std::vector<int> last_sslots;  // call slot of each sampled row of the last step (logits row order)
     void* pin_xbuf = nullptr;    // K6 pin-exchange buffer (grown on demand, reused across runs)
     uint64_t pin_xbuf_bytes = 0;
     // K6 pinned-prefix replication (hk_engine_set_pin_exchange)
@@ -966,6 +967,7 @@ void hk_engine::step(int w, std::vector<SegIn>& segs, float* logits_out_host) {
         free_ev.pop_back();
         p.worker = w;
         p.slots = sslots;
+        last_sslots = sslots;
         // ids, then their logits (read back for the parity checks; 4 B per token)
         HK_CUDA(cudaMemcpyAsync(p.host, sample_ids, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, st));
         HK_CUDA(cudaMemcpyAsync(p.host + S, sample_ids + maxS, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, st));
@@ -1402,6 +1404,138 @@ int hk_generate(hk_engine* e, const uint32_t* ids, size_t n, size_t n_new, uint3
         auto& toks = e->workers[0].slot_tokens[static_cast<size_t>(slot)];
         for (size_t k = 0; k < n_new; ++k) out[k] = static_cast<uint32_t>(toks.at(k));
         e->free_slot(0, slot);
+    });
+}
+
+// ---------------------------------------------------------- step-level C ABI
+// one ragged forward of a worker (hk_step), pin prefill and the
+// K6 page broadcast as stand-alone calls, for hosts that drive their own loop.
+int hk_slot_alloc(hk_engine* e, int w) {
+    try {
+        if (w < 0 || w >= static_cast<int>(e->workers.size())) throw std::runtime_error("hk_slot_alloc: bad worker");
+        const int slot = e->alloc_slot(w);
+        e->harvest(true);
+        e->workers[static_cast<size_t>(w)].slot_tokens[static_cast<size_t>(slot)].clear();
+        e->workers[static_cast<size_t>(w)].slot_logits[static_cast<size_t>(slot)].clear();
+        return slot;
+    } catch (const std::exception& ex) {
+        hk::set_error(ex.what());
+        return -1;
+    }
+}
+
+int hk_slot_free(hk_engine* e, int w, int slot) {
+    return guarded([&] {
+        if (w < 0 || w >= static_cast<int>(e->workers.size())) throw std::runtime_error("hk_slot_free: bad worker");
+        if (slot < 0 || slot >= static_cast<int>(e->ec.max_calls)) throw std::runtime_error("hk_slot_free: bad slot");
+        e->sync();
+        e->free_slot(w, slot);
+    });
+}
+
+int hk_step(hk_engine* e, int w, const hk_step_seg* in, size_t n, int32_t* sampled, float* logits) {
+    return guarded([&] {
+        if (w < 0 || w >= static_cast<int>(e->workers.size())) throw std::runtime_error("hk_step: bad worker");
+        std::vector<std::vector<int>> tables(n);
+        std::vector<std::vector<uint32_t>> ids(n);
+        std::vector<hk_engine::SegIn> segs(n);
+        std::vector<int> seen;
+        for (size_t i = 0; i < n; ++i) {
+            const hk_step_seg& g = in[i];
+            if (g.count <= 0 || g.start < 0) throw std::runtime_error("hk_step: empty segment or negative start");
+            if (!g.pages || g.n_pages <= 0) throw std::runtime_error("hk_step: segment without a block table");
+            if (!g.ids && g.count != 1) throw std::runtime_error("hk_step: a decode segment (ids == NULL) has count 1");
+            if ((g.sample || !g.ids) && g.slot < 0) throw std::runtime_error("hk_step: sampling / decode needs a call slot");
+            if (g.sample) {
+                if (std::find(seen.begin(), seen.end(), g.slot) != seen.end())
+                    throw std::runtime_error("hk_step: a slot samples at most once per step");
+                seen.push_back(g.slot);
+            }
+            tables[i].assign(g.pages, g.pages + g.n_pages);
+            hk_engine::SegIn& s = segs[i];
+            s.slot = g.slot;
+            s.start = g.start;
+            s.count = g.count;
+            s.sample = g.sample != 0;
+            s.write_kv = g.write_kv != 0;
+            s.table = &tables[i];
+            if (g.ids) {
+                ids[i].assign(static_cast<size_t>(g.start) + g.count, 0u);
+                std::copy(g.ids, g.ids + g.count, ids[i].begin() + g.start);
+                s.ids = &ids[i];
+                s.from_prompt = true;
+            } else {
+                s.from_prompt = false;
+            }
+        }
+        const size_t V = static_cast<size_t>(e->V);
+        std::vector<float> lg(logits ? seen.size() * V : 0);
+        e->step(w, segs, logits && !seen.empty() ? lg.data() : nullptr);
+        e->sync();
+        auto& wk = e->workers[static_cast<size_t>(w)];
+        for (size_t i = 0; i < n; ++i) {
+            if (!in[i].sample) {
+                if (sampled) sampled[i] = -1;
+                continue;
+            }
+            const auto& toks = wk.slot_tokens[static_cast<size_t>(in[i].slot)];
+            if (sampled) sampled[i] = toks.empty() ? -1 : static_cast<int32_t>(toks.back());
+            if (logits) {
+                const auto it = std::find(e->last_sslots.begin(), e->last_sslots.end(), in[i].slot);
+                if (it == e->last_sslots.end()) throw std::runtime_error("hk_step: sampled row not found");
+                std::copy_n(lg.begin() + static_cast<std::ptrdiff_t>((it - e->last_sslots.begin()) * V), V,
+                            logits + i * V);
+            }
+        }
+    });
+}
+
+int hk_pin_prefill(hk_engine* e, int w, const uint32_t* ids, size_t n, const int32_t* pages, size_t n_pages) {
+    return guarded([&] {
+        if (w < 0 || w >= static_cast<int>(e->workers.size())) throw std::runtime_error("hk_pin_prefill: bad worker");
+        const size_t block = e->ec.block_tokens;
+        if (n_pages * block < n) throw std::runtime_error("hk_pin_prefill: pages do not cover the sequence");
+        std::vector<int> table(pages, pages + n_pages);
+        std::vector<uint32_t> seq(ids, ids + n);
+        for (size_t c0 = 0; c0 < n; c0 += static_cast<size_t>(e->maxT)) {
+            std::vector<hk_engine::SegIn> segs(1);
+            segs[0].slot = -1;
+            segs[0].start = static_cast<int>(c0);
+            segs[0].count = static_cast<int>(std::min(n - c0, static_cast<size_t>(e->maxT)));
+            segs[0].table = &table;
+            segs[0].ids = &seq;
+            e->step(w, segs);
+        }
+        e->sync();
+    });
+}
+
+int hk_kv_broadcast(hk_engine* e, int w, int role, const int32_t* pages, size_t n, hk_pin_exchange_fn fn, void* user) {
+    return guarded([&] {
+        if (role != 1 && role != 2) throw std::runtime_error("hk_kv_broadcast: role must be 1 (source) or 2 (receiver)");
+        if (!fn) throw std::runtime_error("hk_kv_broadcast: no exchange function");
+        if (n == 0) return;
+        const uint64_t bytes = static_cast<uint64_t>(n) * hk_engine_page_bytes(e);
+        if (e->pin_xbuf_bytes < bytes) {
+            e->sync();
+            cudaFree(e->pin_xbuf);
+            e->pin_xbuf = nullptr;
+            HK_CUDA(cudaMalloc(&e->pin_xbuf, bytes));
+            e->pin_xbuf_bytes = bytes;
+        }
+        void* buf = e->pin_xbuf;
+        auto check = [&](int rc, const char* what) {
+            if (rc != 0) throw std::runtime_error(std::string("hk_kv_broadcast: ") + what + " failed");
+        };
+        if (role == 1) {
+            check(hk_pool_gather(e, w, pages, n, buf), "gather");
+            check(fn(user, w, buf, bytes), "exchange callback");
+        } else {
+            e->sync();
+            check(fn(user, w, buf, bytes), "exchange callback");
+            check(hk_pool_scatter(e, w, buf, pages, n), "scatter");
+        }
+        e->sync();
     });
 }
 

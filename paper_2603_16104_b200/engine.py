@@ -190,6 +190,69 @@ class Engine:
         e, self._pin_exc = getattr(self, "_pin_exc", None), None
         return e
 
+    # step-level entry points (include/helium_b200.h: hk_slot_*, hk_step, hk_pin_prefill, hk_kv_broadcast)
+    def slot_alloc(self, worker: int = 0) -> int:
+        s = _lib.load().hk_slot_alloc(self.handle, worker)
+        if s < 0:
+            raise RuntimeError(f"hk_slot_alloc: {_lib.last_error()}")
+        return s
+
+    def slot_free(self, worker: int, slot: int):
+        _lib.check_status(_lib.load().hk_slot_free(self.handle, worker, slot), "hk_slot_free")
+
+    def step(self, worker: int, segs: List[dict], want_logits: bool = False):
+        """One ragged forward. Each seg: slot, start, count, sample, ids (list of
+        vocab ids, or None for a decode step of the slot's last sampled token),
+        pages (the call's block table), write_kv (default True). Returns the
+        sampled token per seg (-1 where it does not sample) [and the logits
+        [n][vocab] of the sampling segs' last positions]."""
+        arr = (_lib.StepSegC * max(len(segs), 1))()
+        keep = []
+        for i, g in enumerate(segs):
+            ids = None
+            if g.get("ids") is not None:
+                ids = np.ascontiguousarray(np.asarray(g["ids"], dtype=np.uint32))
+                keep.append(ids)
+            pages = np.ascontiguousarray(np.asarray(g["pages"], dtype=np.int32))
+            keep.append(pages)
+            count = len(ids) if ids is not None else int(g.get("count", 1))
+            arr[i] = _lib.StepSegC(int(g.get("slot", -1)), int(g["start"]), count, int(bool(g.get("sample", False))),
+                                   ids.ctypes.data_as(_lib.u32p) if ids is not None else None,
+                                   pages.ctypes.data_as(_lib.i32p), len(pages), int(bool(g.get("write_kv", True))))
+        sampled = np.full(max(len(segs), 1), -1, dtype=np.int32)
+        logits = np.zeros((len(segs), self.model.vocab), dtype=np.float32) if want_logits else None
+        rc = _lib.load().hk_step(self.handle, worker, arr, len(segs), sampled.ctypes.data_as(_lib.i32p),
+                                 logits.ctypes.data_as(_lib.f32p) if want_logits else None)
+        _lib.check_status(rc, "hk_step")
+        return (sampled[:len(segs)], logits) if want_logits else sampled[:len(segs)]
+
+    def pin_prefill(self, worker: int, ids: Sequence[int], pages: Sequence[int]):
+        a = np.ascontiguousarray(np.asarray(ids, dtype=np.uint32))
+        p = np.ascontiguousarray(np.asarray(pages, dtype=np.int32))
+        _lib.check_status(_lib.load().hk_pin_prefill(self.handle, worker, a.ctypes.data_as(_lib.u32p), len(a),
+                                                     p.ctypes.data_as(_lib.i32p), len(p)), "hk_pin_prefill")
+
+    def kv_broadcast(self, worker: int, role: int, pages: Sequence[int], fn):
+        """K6 page broadcast (hk_kv_broadcast): role 1 gathers `pages` and calls
+        fn(device_ptr, nbytes); role 2 calls fn to fill the buffer, then
+        scatters it into `pages`."""
+        p = np.ascontiguousarray(np.asarray(pages, dtype=np.int32))
+        err = []
+
+        def _cb(_user, _worker, buf, nbytes):
+            try:
+                fn(int(buf or 0), int(nbytes))
+                return 0
+            except Exception as e:  # re-raised below
+                err.append(e)
+                return 1
+
+        cb = _lib.PinExchangeFn(_cb)
+        rc = _lib.load().hk_kv_broadcast(self.handle, worker, role, p.ctypes.data_as(_lib.i32p), len(p), cb, None)
+        if err:
+            raise err[0]
+        _lib.check_status(rc, "hk_kv_broadcast")
+
     def pool_gather(self, worker: int, pages: Sequence[int], dst_ptr: int):
         p = np.ascontiguousarray(np.asarray(pages, dtype=np.int32))
         _lib.check_status(_lib.load().hk_pool_gather(self.handle, worker, p.ctypes.data_as(_lib.i32p), len(p),
