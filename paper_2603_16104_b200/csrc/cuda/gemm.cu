@@ -884,6 +884,182 @@ __global__ void __launch_bounds__(192, 1)
     }
 }
 
+// The fp32-row prefill GEMMs (QKV / O / down partial rows) on persistent CTA
+// pairs: the gate/up kernel's pipeline with the row epilogue — per 32-token
+// chunk, TMEM -> registers -> smem [32 tokens][128 features] -> 512-byte row
+// stores — drained while the next tile's MMAs run. Units are (split, weight
+// pair, token tile), token tiles fastest.
+constexpr size_t pr2_smem_bytes() {
+    return 1024 + PK2_STAGES * (BM * BK * 2 + (PK_BN / 2) * BK * 2) + PK_EC * (BM + 4) * 4 +
+           (2 * PK2_STAGES + 4) * 8 + 16;
+}
+
+__global__ void __launch_bounds__(192, 1)
+    gemm_rows_pk2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int A_BYTES = BM * BK * 2, B_BYTES = (PK_BN / 2) * BK * 2;
+    constexpr int SO = BM + 4;  // padded staging row
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + PK2_STAGES * A_BYTES;
+    float* so = reinterpret_cast<float*>(sB + PK2_STAGES * B_BYTES);  // [PK_EC tokens][SO]
+    uint64_t* full = reinterpret_cast<uint64_t*>(so + PK_EC * SO);
+    uint64_t* empty = full + PK2_STAGES;
+    uint64_t* acc_full = empty + PK2_STAGES;
+    uint64_t* acc_empty = acc_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int pair = static_cast<int>(blockIdx.x) >> 1, n_pairs = static_cast<int>(gridDim.x) >> 1;
+    const int mpt = (p.N + BM - 1) / BM / 2, nt = (p.T + PK_BN - 1) / PK_BN;
+    const int per_split = mpt * nt;
+    const int splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+    const int units = per_split * splits;
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&tmW);
+        tma_prefetch_desc(&tmX);
+        for (int st = 0; st < PK2_STAGES; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 256);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_cg2(tmem_slot, 512);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+
+    auto unit_of = [&](int u, int& m0, int& n0, int& z, int& kb0, int& nkb) {
+        z = u / per_split;
+        const int r = u % per_split;
+        m0 = ((r / nt) * 2 + static_cast<int>(rank)) * BM;
+        n0 = (r % nt) * PK_BN;
+        kb0 = z * p.kb_per_split;
+        nkb = min(p.kb_per_split, p.kb_total - kb0);
+    };
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_w = policy_evict_first();
+            const uint64_t pol_x = policy_evict_last();
+            const uint32_t full0 = mapa_shared(smem_u32(full), 0);
+            pdl_wait();
+            int g = 0;
+            for (int u = pair; u < units; u += n_pairs) {
+                int m0, n0, z, kb0, nkb;
+                unit_of(u, m0, n0, z, kb0, nkb);
+                const int nb = n0 + static_cast<int>(rank) * (PK_BN / 2);
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int st = g % PK2_STAGES;
+                    if (g >= PK2_STAGES) mbar_wait(&empty[st], ((g / PK2_STAGES) - 1) & 1);
+                    if (rank == 0) mbar_expect_tx(&full[st], 2 * (A_BYTES + B_BYTES));
+                    tma_load_2d_cg2(sA + st * A_BYTES, &tmW, full0 + st * 8, (kb0 + kb) * BK, m0, pol_w);
+                    tma_load_2d_cg2(sB + st * B_BYTES, &tmX, full0 + st * 8, (kb0 + kb) * BK, nb, pol_x);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0) {
+            pdl_wait();
+            constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, PK_BN);
+            int g = 0, i = 0;
+            for (int u = pair; u < units; u += n_pairs, ++i) {
+                int m0, n0, z, kb0, nkb;
+                unit_of(u, m0, n0, z, kb0, nkb);
+                const int b = i & 1;
+                if (i >= 2) mbar_wait(&acc_empty[b], ((i >> 1) - 1) & 1);
+                tc_fence_after();
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int st = g % PK2_STAGES;
+                    mbar_wait(&full[st], (g / PK2_STAGES) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t a_base = smem_u32(sA + st * A_BYTES);
+                        const uint32_t b_base = smem_u32(sB + st * B_BYTES);
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k)
+                            umma_bf16_cg2(tmem + b * PK_BN, umma_desc_sw128(a_base + k * 32),
+                                          umma_desc_sw128(b_base + k * 32), idesc, (kb | k) != 0 ? 1u : 0u);
+                        umma_commit_cg2_mc(&empty[st], 3);
+                        if (kb == nkb - 1) umma_commit_cg2_mc(&acc_full[b], 3);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else {
+        pdl_wait();
+        const int q = warp & 3;  // TMEM lane quarter of this warp
+        const int row = q * 32 + lane;
+        const int ew = warp - 2;  // 0..3: store warp index
+        const uint32_t acc_empty0 = mapa_shared(smem_u32(acc_empty), 0);
+        int i = 0;
+        for (int u = pair; u < units; u += n_pairs, ++i) {
+            int m0, n0, z, kb0, nkb;
+            unit_of(u, m0, n0, z, kb0, nkb);
+            const int b = i & 1;
+            const bool m_ok = m0 + row < p.N;
+            const float bias = (p.bias && m_ok && p.epi != kEpiPartial) ? bf2f(p.bias[m0 + row]) : 0.f;
+            const bool full_m = m0 + BM <= p.N;
+            mbar_wait(&acc_full[b], (i >> 1) & 1);
+            tc_fence_after();
+            for (int c0 = 0; c0 < PK_BN; c0 += PK_EC) {
+                float v[PK_EC];
+                tmem_ld32(tmem + b * PK_BN + c0 + (static_cast<uint32_t>(q * 32) << 16), v);
+                if (c0 + PK_EC == PK_BN) {
+                    tc_fence_before();
+                    mbar_arrive_cluster(acc_empty0 + b * 8);
+                }
+#pragma unroll
+                for (int j = 0; j < PK_EC; ++j) so[j * SO + row] = v[j] + bias;
+                named_bar(1, 128);
+                const int rows = min(PK_EC, p.T - n0 - c0);
+                for (int r = ew; r < rows; r += 4) {
+                    const int n = n0 + c0 + r;
+                    const float4 w = reinterpret_cast<const float4*>(so + r * SO)[lane];
+                    const int mm = m0 + lane * 4;
+                    if (p.epi == kEpiPartial) {
+                        float* dst = p.partial + (static_cast<size_t>(z) * p.T + n) * p.N + mm;
+                        if (full_m) {
+                            *reinterpret_cast<float4*>(dst) = w;
+                        } else {
+                            const float e[4] = {w.x, w.y, w.z, w.w};
+                            for (int qq = 0; qq < 4; ++qq)
+                                if (mm + qq < p.N) dst[qq] = e[qq];
+                        }
+                    } else {
+                        const float e[4] = {w.x, w.y, w.z, w.w};
+                        for (int qq = 0; qq < 4; ++qq) {
+                            if (mm + qq >= p.N) break;
+                            const size_t o = static_cast<size_t>(n) * p.ldo + mm + qq;
+                            if (p.epi == kEpiStoreBf16)
+                                static_cast<bf16*>(p.out)[o] = f2bf(e[qq]);
+                            else if (p.epi == kEpiAddF32)
+                                static_cast<float*>(p.out)[o] += e[qq];
+                            else
+                                static_cast<float*>(p.out)[o] = e[qq];
+                        }
+                    }
+                }
+                named_bar(1, 128);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_cg2(tmem, 512);
+    }
+}
+
 template <int BN, int STAGES>
 constexpr size_t smem_bytes() {
     return 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 1) * 8 + 16;
@@ -1117,6 +1293,42 @@ int gemm_bf16(const bf16* W, const bf16* X, int N, int K, int T, int epi, void* 
         launch_pdl(gemm_swiglu_pk_kernel, dim3(std::min(mt * nt, g_num_sms)), dim3(192), sm, st, tw, txp, p);
         HK_LAUNCHED(1);
         return 1;
+    }
+    static const bool pr2_off = std::getenv("HK_GEMM_ROWS_PERSIST") && std::atoi(std::getenv("HK_GEMM_ROWS_PERSIST")) == 0;
+    if (use_cg2 && epi != kEpiSwiGLU && !pr2_off && (mt / 2) * nt * splits > g_num_sms / 2) {  // > one wave of pairs
+        // prefill fp32-row GEMMs: persistent CTA pairs, epilogue under the next tile's MMAs
+        static bool configured = false;
+        constexpr size_t sm = pr2_smem_bytes();
+        if (!configured) {
+            HK_CUDA(cudaFuncSetAttribute(gemm_rows_pk2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sm)));
+            configured = true;
+        }
+        const CUtensorMap txh = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), PK_BN / 2);
+        const int pairs = std::min((mt / 2) * nt * splits, g_num_sms / 2);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * pairs);
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = 2;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        HK_CUDA(cudaLaunchKernelEx(&cfg, gemm_rows_pk2_kernel, tw, txh, p));
+        HK_LAUNCHED(1);
+        if (via_ws) {
+            const size_t total = static_cast<size_t>(T) * N;
+            const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 4096));
+            splitk_reduce_kernel<<<blocks, 256, 0, st>>>(workspace, splits, T, N, epi, out, ldo, bias);
+            HK_LAUNCHED(1);
+        }
+        return splits;
     }
     if (use_cg2) {
         const CUtensorMap txh = make_map_2d(X, static_cast<uint64_t>(T), static_cast<uint64_t>(K), C2_BN / 2);
