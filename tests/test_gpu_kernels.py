@@ -54,14 +54,17 @@ def test_gemm_tcgen05_matches_torch(N, K, T):
     assert errp < 1e-4, errp
 
 
-@pytest.mark.parametrize("splits,T", [(1, 600), (3, 600), (2, 1024)])
-def test_gemm_pair_tiles_splitk_partials(splits, T):
+@pytest.mark.parametrize("splits,T,N", [(1, 600, 1024), (3, 600, 1024), (2, 1024, 1024), (2, 1100, 4096),
+                                        (1, 2300, 2048)])
+def test_gemm_pair_tiles_splitk_partials(splits, T, N):
     """Prefill tiles on CTA pairs (tcgen05 cta_group::2, 256 weight rows x 256
     tokens per cluster): split-K fp32 partials [splits][T][N] sum to the
     product; T = 600 leaves a ragged last token tile whose second half is
-    entirely out of bounds (TMA zero fill)."""
+    entirely out of bounds (TMA zero fill). (1100, 4096) x 2 splits and
+    (2300, 2048): more units than CTA pairs, so the persistent pair kernel walks
+    several (split, weight pair, token tile) units per cluster."""
     lib = _lib.load()
-    N, K = 1024, 1024
+    K = 1024
     g = torch.Generator(device="cuda").manual_seed(splits * 1000 + T)
     W = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) * (3.0 / K) ** 0.5
     X = (torch.rand(T, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
