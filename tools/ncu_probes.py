@@ -52,6 +52,31 @@ elif what == "prefill_gemm_time":
         us = e0.elapsed_time(e1) / 20 * 1e3
         tf = 2 * N * K * T / us / 1e6
         print(f"{name:8s} T={T}: {us:8.1f} us  {tf:7.1f} TFLOP/s  frac {tf / peak:.3f}")
+elif what == "decode_gemm_time":
+    # decode GEMM weight streaming (T = 64, inputs resident, L2 flushed between launches) vs weight-tile count
+    T = 64
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for name, N, K, epi in [("gate_up 224 tiles", 28672, 4096, 4), ("swiglu 296 tiles", 37888, 4096, 4),
+                            ("swiglu 148 tiles", 18944, 4096, 4), ("qkv", 6144, 4096, 3), ("o", 4096, 4096, 3),
+                            ("down", 4096, 14336, 3)]:
+        W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+        X = torch.randn(T, K, device="cuda").to(torch.bfloat16)
+        out = torch.zeros(16 * T * N, device="cuda", dtype=torch.float32)
+        call = lambda: lib.hkx_gemm_bf16(C.c_void_p(W.data_ptr()), C.c_void_p(X.data_ptr()), C.c_void_p(out.data_ptr()),
+                                         N, K, T, epi, None, 0, None)
+        for _ in range(3):
+            assert call() == 0, _lib.last_error()
+        ts = []
+        for _ in range(10):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            call()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3)
+        us = sorted(ts)[len(ts) // 2]
+        print(f"{name:18s} N={N:6d} K={K:6d}: {us:7.1f} us  {N * K * 2 / us / 1e3:7.0f} GB/s")
 elif what == "pool":
     from paper_2603_16104_b200.engine import LLAMA3_8B, Engine, EngineConfig
     eng = Engine(LLAMA3_8B, EngineConfig(pages_per_worker=1024, max_calls=8, max_step_tokens=256, max_ctx_tokens=2048))
