@@ -41,6 +41,17 @@ if not args.child:
                                  (5, "rows out")]):
         d = (sh[:, b] - sh[:, a]) / 1e3
         print(f"  {na:>12s} -> {nb:<12s} mean {d.mean():6.2f} max {d.max():6.2f} us   (end {us(sh[:, b]).max():.2f})")
+    # per-chunk clock64 stamps (chunks 0-7) of tile 0's softmax thread 0 and the MMA issuer, median over shared
+    # CTAs, cycles relative to chunk 0's "S ready": 0 S ready, 6 max done, 1 exps done, 3 P written, 4/5 PV_0/PV_1 issue
+    cs = t[16384:16384 + 148 * 64].reshape(148, 8, 8)
+    cs = cs[cta[:, 1] > 0]
+    if len(cs) and (cs[:, 0, 0] > 0).all():
+        rel = cs - cs[:, :1, :1]
+        print("  chunk  S_ready  max_done  exp_done  P_written  PV0_issue  PV1_issue (cycles, median over shared CTAs)")
+        for c in range(8):
+            if (cs[:, c, 0] > 0).all():
+                med = np.median(rel[:, c, :], axis=0)
+                print("  %5d %8.0f %9.0f %9.0f %10.0f %10.0f %10.0f" % (c, med[0], med[6], med[1], med[3], med[4], med[5]))
     items = t[32768:32768 + 6000 * 4].reshape(-1, 4)
     items = items[items[:, 0] > 0]
     if len(items):
