@@ -20,7 +20,7 @@ torch = pytest.importorskip("torch")
 
 pytestmark = pytest.mark.gpu
 
-from paper_2603_16104_b200.engine import TINY, LLAMA3_8B, Engine, EngineConfig, reduced  # noqa: E402
+from paper_2603_16104_b200.engine import TINY, LLAMA3_8B, QWEN25_32B, Engine, EngineConfig, reduced  # noqa: E402
 from paper_2603_16104_b200.exchange import buffer_tensor  # noqa: E402
 
 
@@ -33,8 +33,9 @@ def _ids(n, seed, vocab):
     return np.random.default_rng(seed).integers(0, vocab, n).astype(np.uint32)
 
 
-@pytest.mark.parametrize("model", [replace(TINY, fp32=True), TINY, reduced(LLAMA3_8B, 2, vocab=32768)],
-                         ids=["tiny_fp32", "tiny_bf16", "llama_width_bf16"])
+@pytest.mark.parametrize("model", [replace(TINY, fp32=True), TINY, reduced(LLAMA3_8B, 2, vocab=32768),
+                                   reduced(QWEN25_32B, 2, vocab=32768)],
+                         ids=["tiny_fp32", "tiny_bf16", "llama_width_bf16", "qwen_width_bf16"])
 def test_step_by_step_equals_generate(model):
     prompt, n_new = _ids(70, 1, model.vocab), 8
     ref = _engine(model)
